@@ -1,0 +1,144 @@
+/*
+ * contour.h -- C-ABI of the B200-native Contour connected-components hot path
+ * (libcontour.so, built from paper_2311_02811_b200/csrc/ for sm_100a).
+ *
+ * The reference (minmapcc, /root/reference/pkg) is a Python package whose hot
+ * path is reached through these Python call sites; each entry point below
+ * names the reference interface it replaces.  Plain pointers and sizes only:
+ * no torch / CUDA types appear in the signatures (streams and device buffers
+ * travel as void* / uint32_t*).
+ *
+ * Error convention: every int-returning function returns
+ *   CC_OK 0, CC_EINVAL 1 (-> ValueError), CC_ECAP 2 (-> IterationCapExceeded,
+ *   errors.py:12-13), CC_ECUDA 3 (-> RuntimeError).  cc_last_error() gives
+ *   the thread-local message of the last failure on the calling thread.
+ *
+ * Threading: a context serialises calls on itself (internal mutex); use one
+ * context per caller thread for concurrency (SPEC.md:212 reentrancy).
+ */
+#ifndef CONTOUR_H
+#define CONTOUR_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CC_OK 0
+#define CC_EINVAL 1
+#define CC_ECAP 2
+#define CC_ECUDA 3
+
+/* Variant codes, in the order of VARIANTS (engine.py:46). */
+#define CC_VAR_CSYN 0
+#define CC_VAR_C1 1
+#define CC_VAR_C2 2
+#define CC_VAR_CM 3
+#define CC_VAR_C11MM 4
+#define CC_VAR_C1M1M 5
+
+/* Schedule (engine.py:51-74): order_for(k) is evaluated per sweep. */
+typedef struct cc_schedule {
+    int32_t variant;
+    int32_t high_order;
+    int32_t warmup;
+    int32_t sync;   /* 1: read L, lower a shadow, commit after the sweep (engine.py:288-291,310-311) */
+    int32_t atomic; /* 1: lowering never lost (CAS loop, _kernels.py:79-93) -> red.global.min */
+} cc_schedule;
+
+/* cc_run flags */
+#define CC_RUN_EARLY_CHECK 1   /* early_convergence_check after each changing sweep (engine.py:318-320) */
+#define CC_RUN_COUNT_CHANGES 2 /* exact changed_per_sweep by label diff (engine.py:293,309) */
+#define CC_RUN_SWEEP_TIMES 4   /* per-sweep device times (IterationStats.sweep_seconds) */
+
+/* Output of cc_run, the IterationStats contract (engine.py:77-90). */
+typedef struct cc_stats {
+    int64_t sweeps_executed;
+    int64_t sweeps_until_stable;
+    int32_t converged_by;      /* 0 "change-flag", 1 "early-check" */
+    int32_t compress_rounds;   /* pointer-jumping rounds that changed something (0 after a correct run) */
+    int64_t capacity;          /* entries available in the two caller arrays below */
+    int64_t* changed_per_sweep;/* caller-owned or NULL; -1 = "changed, count not requested" */
+    double* sweep_seconds;     /* caller-owned or NULL */
+    double converge_seconds;   /* device time: label init -> compressed labels */
+} cc_stats;
+
+typedef struct cc_ctx cc_ctx;
+
+/* Context on CUDA device `device`.  `stream` is a cudaStream_t (e.g. torch's
+ * current stream) or NULL to create a private non-blocking stream. */
+int cc_create(int device, void* stream, cc_ctx** out);
+void cc_destroy(cc_ctx* ctx);
+const char* cc_last_error(void);
+int cc_version(void);
+
+/* ---- staging: the Graph input contract (graph.py:57-90, engine.py:268-270) ----
+ * edges: (m, 2) row-major pairs, elem_bytes 4 (int32) or 8 (int64), as the
+ * reference's g.edges.  Converted on device to packed uint32 SoA src[]/dst[]
+ * with the endpoint range check of graph.py:73-79 (-> CC_EINVAL).
+ * Host variant: the buffer is borrowed for the call only (pinned memory
+ * gives full PCIe rate; pageable works).  Device variant: device pointer. */
+int cc_stage_edges(cc_ctx* ctx, const void* edges_host, int elem_bytes, int64_t m, int64_t n);
+int cc_stage_edges_device(cc_ctx* ctx, const void* edges_dev, int elem_bytes, int64_t m, int64_t n);
+/* Borrow caller-owned device SoA arrays (must outlive their use). */
+int cc_attach_soa(cc_ctx* ctx, uint32_t* src_dev, uint32_t* dst_dev, int64_t m, int64_t n);
+/* Borrow a caller-owned device label buffer of n+1 uint32 (slot n = exchange flag). */
+int cc_attach_labels(cc_ctx* ctx, uint32_t* labels_dev);
+int cc_labels_device(cc_ctx* ctx, uint32_t** labels_dev);
+
+/* ---- the hot path: run_contour(g, schedule, threads, seed) (engine.py:248-328) ----
+ * Initialise labels = arange(n), sweep with order_for(k) until a sweep
+ * lowers nothing (ballot/OR flag) or the early check passes, then
+ * pointer-jump compress.  cap: sweeps allowed (the reference uses n+2,
+ * engine.py:275) -> CC_ECAP.  labels_out: host buffer of n elements of
+ * out_elem_bytes (4 or 8), or NULL to leave labels on device. */
+int cc_run(cc_ctx* ctx, const cc_schedule* sched, int flags, int64_t cap,
+           void* labels_out, int out_elem_bytes, cc_stats* stats);
+
+/* ---- building blocks (multi-GPU driver, tests) ---- */
+int cc_init_labels(cc_ctx* ctx);
+/* One sweep over the staged edges: sweep_edges(read, target, edges, 0, m, 0,
+ * order, use_cas) (_kernels.py:35-102).  Leaves the "wrote" flag on device;
+ * if wrote_out != NULL it is synchronously read back. */
+int cc_sweep(cc_ctx* ctx, int order, int sync, int atomic, int* wrote_out);
+/* Fold the wrote flag into label slot n for an allreduce-min exchange
+ * (SURVEY 8(e)): first=1: labels[n] = wrote ? 0 : 1; first=0:
+ * labels[n] = min(labels[n], wrote ? 0 : 1).  Clears the flag. */
+int cc_fold_flag(cc_ctx* ctx, int first);
+int cc_compress(cc_ctx* ctx, int* rounds_out);
+/* early_convergence_check(g, labels) (engine.py:331-365) on device. */
+int cc_early_check(cc_ctx* ctx, int* ok_out);
+int cc_read_labels(cc_ctx* ctx, void* out_host, int elem_bytes);
+int cc_synchronize(cc_ctx* ctx);
+
+/* Single-edge operator mm_order(target, read, w, v, order, atomic)
+ * (engine.py:209-231) run by the device edge routines on a private copy:
+ * inplace=1 -> target is read (async form), else target is separate
+ * (sync form).  Arrays are int64 host arrays of length n. */
+int cc_mm_order(const int64_t* read, int64_t* target, int64_t n, int64_t w, int64_t v,
+                int order, int inplace, int* changed_out);
+
+/* ---- seeded synthetic inputs (definitions: oracle/gen.py) ---- */
+/* RMAT rows [row_lo, row_hi) of the (symmetrised) edge list, generated on
+ * device straight into the context's SoA arrays (a shard for multi-GPU). */
+int cc_gen_rmat_device(cc_ctx* ctx, int scale, int edgefactor, uint64_t seed, uint32_t tA,
+                       uint32_t tAB, uint32_t tABC, int symmetrize, int permute,
+                       int64_t row_lo, int64_t row_hi);
+/* Host generators writing (m,2) AoS rows of elem_bytes; out may be NULL to
+ * count; *m_out receives the row count. */
+int cc_gen_rmat_host(int scale, int edgefactor, uint64_t seed, uint32_t tA, uint32_t tAB,
+                     uint32_t tABC, int symmetrize, int permute, int64_t row_lo, int64_t row_hi,
+                     void* out, int elem_bytes, int threads);
+int cc_gen_grid_host(int64_t rows, int64_t cols, uint32_t keep_thr, uint64_t seed, int permute,
+                     void* out, int elem_bytes, int64_t* m_out, int threads);
+int cc_gen_er_host(int64_t n, int64_t pairs, uint64_t seed, void* out, int elem_bytes,
+                   int64_t* m_out);
+int cc_gen_forest_host(const int64_t* sizes, int64_t components, int64_t n, uint64_t seed,
+                       void* out, int elem_bytes, int64_t* m_out, int threads);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CONTOUR_H */

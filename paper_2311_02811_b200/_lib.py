@@ -1,0 +1,140 @@
+"""ctypes binding of libcontour.so (include/contour.h).
+
+There is no CPU fallback: if the library is missing or no CUDA device is
+visible, the product entry points raise.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+from .errors import IterationCapExceeded
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "lib", "libcontour.so")
+
+CC_OK, CC_EINVAL, CC_ECAP, CC_ECUDA = 0, 1, 2, 3
+CC_RUN_EARLY_CHECK, CC_RUN_COUNT_CHANGES, CC_RUN_SWEEP_TIMES = 1, 2, 4
+
+_I64P = ctypes.POINTER(ctypes.c_int64)
+_U32P = ctypes.POINTER(ctypes.c_uint32)
+_DBLP = ctypes.POINTER(ctypes.c_double)
+
+
+class CCSchedule(ctypes.Structure):
+    _fields_ = [("variant", ctypes.c_int32), ("high_order", ctypes.c_int32),
+                ("warmup", ctypes.c_int32), ("sync", ctypes.c_int32), ("atomic", ctypes.c_int32)]
+
+
+class CCStats(ctypes.Structure):
+    _fields_ = [("sweeps_executed", ctypes.c_int64), ("sweeps_until_stable", ctypes.c_int64),
+                ("converged_by", ctypes.c_int32), ("compress_rounds", ctypes.c_int32),
+                ("capacity", ctypes.c_int64), ("changed_per_sweep", _I64P),
+                ("sweep_seconds", _DBLP), ("converge_seconds", ctypes.c_double)]
+
+
+# name -> (restype, argtypes); every symbol declared in include/contour.h
+SIGNATURES = {
+    "cc_create": (ctypes.c_int, [ctypes.c_int, ctypes.c_void_p, ctypes.POINTER(ctypes.c_void_p)]),
+    "cc_destroy": (None, [ctypes.c_void_p]),
+    "cc_last_error": (ctypes.c_char_p, []),
+    "cc_version": (ctypes.c_int, []),
+    "cc_stage_edges": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int,
+                                      ctypes.c_int64, ctypes.c_int64]),
+    "cc_stage_edges_device": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int,
+                                             ctypes.c_int64, ctypes.c_int64]),
+    "cc_attach_soa": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                     ctypes.c_int64, ctypes.c_int64]),
+    "cc_attach_labels": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p]),
+    "cc_labels_device": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_void_p)]),
+    "cc_run": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(CCSchedule), ctypes.c_int,
+                              ctypes.c_int64, ctypes.c_void_p, ctypes.c_int,
+                              ctypes.POINTER(CCStats)]),
+    "cc_init_labels": (ctypes.c_int, [ctypes.c_void_p]),
+    "cc_sweep": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                ctypes.POINTER(ctypes.c_int)]),
+    "cc_fold_flag": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
+    "cc_compress": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_int)]),
+    "cc_early_check": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_int)]),
+    "cc_read_labels": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]),
+    "cc_synchronize": (ctypes.c_int, [ctypes.c_void_p]),
+    "cc_mm_order": (ctypes.c_int, [_I64P, _I64P, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
+                                   ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_int)]),
+    "cc_gen_rmat_device": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
+                                          ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32,
+                                          ctypes.c_uint32, ctypes.c_int, ctypes.c_int,
+                                          ctypes.c_int64, ctypes.c_int64]),
+    "cc_gen_rmat_host": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_uint64,
+                                        ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32,
+                                        ctypes.c_int, ctypes.c_int, ctypes.c_int64,
+                                        ctypes.c_int64, ctypes.c_void_p, ctypes.c_int,
+                                        ctypes.c_int]),
+    "cc_gen_grid_host": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int64, ctypes.c_uint32,
+                                        ctypes.c_uint64, ctypes.c_int, ctypes.c_void_p,
+                                        ctypes.c_int, _I64P, ctypes.c_int]),
+    "cc_gen_er_host": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int64, ctypes.c_uint64,
+                                      ctypes.c_void_p, ctypes.c_int, _I64P]),
+    "cc_gen_forest_host": (ctypes.c_int, [_I64P, ctypes.c_int64, ctypes.c_int64, ctypes.c_uint64,
+                                          ctypes.c_void_p, ctypes.c_int, _I64P, ctypes.c_int]),
+}
+
+_lib = None
+
+
+def load():
+    """Load libcontour.so (raises if it has not been built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(
+                f"{LIB_PATH} is missing: build it with `python -m paper_2311_02811_b200.build` "
+                "(there is no CPU fallback)")
+        lib = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+    return _lib
+
+
+def last_error() -> str:
+    msg = load().cc_last_error()
+    return msg.decode() if msg else ""
+
+
+def check(rc: int, what: str = "") -> None:
+    if rc == CC_OK:
+        return
+    msg = last_error() or what
+    if rc == CC_EINVAL:
+        raise ValueError(msg)
+    if rc == CC_ECAP:
+        raise IterationCapExceeded(msg)
+    raise RuntimeError(f"CUDA error in libcontour: {msg}")
+
+
+class Context:
+    """Owns one cc_ctx (device buffers, streams) on one CUDA device."""
+
+    def __init__(self, device: int = 0, stream: int | None = None):
+        self.lib = load()
+        self.device = device
+        h = ctypes.c_void_p()
+        check(self.lib.cc_create(device, ctypes.c_void_p(stream or 0), ctypes.byref(h)),
+              "cc_create")
+        self.handle = h
+        self.n = 0
+        self.m = 0
+
+    def close(self):
+        if getattr(self, "handle", None):
+            self.lib.cc_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,798 @@
+// libcontour.so -- B200 (sm_100a) implementation of the Contour hot path behind
+// the C-ABI declared in include/contour.h.
+//
+// The host driver below restates the reference driver loop run_contour
+// (/root/reference/pkg/src/minmapcc/engine.py:248-328) over device kernels:
+// labels live in HBM as uint32 (4n B), edges as packed uint32 SoA (8m B),
+// each sweep is one kernel launch over all edges, and convergence is decided
+// from a one-word device flag instead of an n-sized label diff.
+#include <cuda_runtime.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <mutex>
+#include <thread>
+#include <vector>
+
+#include "contour.h"
+#include "gen_rng.cuh"
+#include "kernels.cuh"
+
+using cck::lab_t;
+using cck::kThreads;
+
+// ------------------------------------------------------------------ errors
+static thread_local char g_err[1024] = "";
+
+static int fail(int code, const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+    return code;
+}
+
+#define CUDA_TRY(x)                                                                        \
+    do {                                                                                   \
+        cudaError_t e_ = (x);                                                              \
+        if (e_ != cudaSuccess)                                                             \
+            return fail(CC_ECUDA, "%s failed: %s (%s:%d)", #x, cudaGetErrorString(e_),     \
+                        __FILE__, __LINE__);                                               \
+    } while (0)
+
+#define CC_TRY(x)                \
+    do {                         \
+        int rc_ = (x);           \
+        if (rc_ != CC_OK) return rc_; \
+    } while (0)
+
+// ------------------------------------------------------------------ kernels
+namespace {
+
+constexpr int kFlagWrote = 0;    // any lowering in the current sweep (ballot/OR)
+constexpr int kFlagBad = 1;      // early check / staging range violation
+constexpr int kFlagCompress = 2; // compress round changed something
+constexpr int kNumFlags = 4;
+
+__global__ void k_iota(lab_t* L, int64_t n) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        L[i] = (lab_t)i;
+}
+
+__device__ __forceinline__ unsigned long long block_sum(unsigned long long x) {
+    __shared__ unsigned long long part[kThreads / 32];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = x;
+    __syncthreads();
+    unsigned long long t = 0;
+    if (threadIdx.x < 32) {
+        t = threadIdx.x < (blockDim.x >> 5) ? part[threadIdx.x] : 0ull;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    }
+    return t;  // valid in thread 0
+}
+
+// Synchronous commit (engine.py:309-311): count cells where the shadow was
+// lowered, copy them into the labels.  Sets the wrote flag if any changed.
+__global__ void __launch_bounds__(kThreads) k_commit(lab_t* L, const lab_t* S, int64_t n,
+                                                     unsigned long long* count, int* flags) {
+    unsigned long long c = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const lab_t s = S[i];
+        if (s != L[i]) { L[i] = s; ++c; }
+    }
+    c = block_sum(c);
+    if (threadIdx.x == 0 && c) { atomicAdd(count, c); flags[kFlagWrote] = 1; }
+}
+
+// changed = count_nonzero(target != before) (engine.py:309), async mode.
+__global__ void __launch_bounds__(kThreads) k_diff(const lab_t* L, const lab_t* B, int64_t n,
+                                                   unsigned long long* count) {
+    unsigned long long c = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        c += (L[i] != B[i]);
+    c = block_sum(c);
+    if (threadIdx.x == 0 && c) atomicAdd(count, c);
+}
+
+// early_convergence_check (engine.py:331-348): idempotence, then agreement.
+__global__ void k_check_idem(const lab_t* L, int64_t n, int* flags) {
+    bool bad = false;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const lab_t l = L[i];
+        bad |= (L[l] != l);
+    }
+    if (__syncthreads_or(bad) && threadIdx.x == 0) flags[kFlagBad] = 1;
+}
+
+__global__ void k_check_edges(const lab_t* __restrict__ src, const lab_t* __restrict__ dst,
+                              int64_t m, const lab_t* L, int* flags) {
+    if (*(volatile int*)&flags[kFlagBad]) return;  // idempotence already failed
+    bool bad = false;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m;
+         e += (int64_t)gridDim.x * blockDim.x)
+        bad |= (L[__ldcs(src + e)] != L[__ldcs(dst + e)]);
+    if (__syncthreads_or(bad) && threadIdx.x == 0) flags[kFlagBad] = 1;
+}
+
+// Pointer-jumping compress L[v] = L[L[v]] (north-star step 4; the semantic
+// model is normalize_labels, baselines.py:146-152).
+__global__ void k_compress(lab_t* L, int64_t n, int* flags) {
+    bool ch = false;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const lab_t l = L[i];
+        const lab_t ll = L[l];
+        if (ll != l) { L[i] = ll; ch = true; }
+    }
+    if (__syncthreads_or(ch) && threadIdx.x == 0) flags[kFlagCompress] = 1;
+}
+
+// labels[n] = wrote ? 0 : 1, flag cleared: folds "did any rank write" into
+// an allreduce-min over n+1 elements.
+__global__ void k_fold(lab_t* L, int64_t n, int* flags, int first) {
+    const lab_t f = flags[kFlagWrote] ? 0u : 1u;
+    L[n] = first ? f : min(L[n], f);
+    flags[kFlagWrote] = 0;
+}
+
+// Staging: (m,2) AoS int32/int64 rows -> packed uint32 SoA + range check
+// (graph.py:73-79).
+template <typename T>
+__global__ void k_stage(const T* __restrict__ aos, int64_t rows, int64_t n, lab_t* src, lab_t* dst,
+                        int* flags) {
+    bool bad = false;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < rows;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const T a = aos[2 * e], b = aos[2 * e + 1];
+        bad |= (a < 0) | (b < 0) | ((int64_t)a >= n) | ((int64_t)b >= n);
+        src[e] = (lab_t)a;
+        dst[e] = (lab_t)b;
+    }
+    if (__syncthreads_or(bad) && threadIdx.x == 0) flags[kFlagBad] = 1;
+}
+
+__global__ void k_widen(const lab_t* L, int64_t n, int64_t* out) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = (int64_t)L[i];
+}
+
+__global__ void k_from64(const int64_t* in, int64_t n, lab_t* L) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        L[i] = (lab_t)in[i];
+}
+
+// Single-edge operator through the same device routines as the sweeps.
+__global__ void k_single_edge(const lab_t* R, lab_t* T, lab_t w, lab_t v, int order, int inplace,
+                              int* changed) {
+    lab_t u1[1] = {w}, v1[1] = {v};
+    bool c;
+    if (inplace) {
+        if (order == 1) c = cck::batch<1, 1, false>(T, T, u1, v1, order);
+        else if (order == 2) c = cck::batch<2, 1, false>(T, T, u1, v1, order);
+        else c = cck::batch<0, 1, false>(T, T, u1, v1, order);
+        *changed = c;
+    } else {
+        // sync form: lowering of a separate target; report whether it moved
+        lab_t before_w = T[w], before_v = T[v];
+        (void)before_w; (void)before_v;
+        if (order == 1) cck::batch<1, 1, true>(R, T, u1, v1, order);
+        else if (order == 2) cck::batch<2, 1, true>(R, T, u1, v1, order);
+        else cck::batch<0, 1, true>(R, T, u1, v1, order);
+    }
+}
+
+// RMAT rows [lo, hi) of the symmetrised list (rows >= M are (v,u) of row-M).
+__global__ void k_gen_rmat(ccgen::RmatParams rp, ccgen::Perm pm, int permute, int64_t M,
+                           int symmetrize, int64_t lo, int64_t hi, lab_t* src, lab_t* dst) {
+    for (int64_t r = lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < hi;
+         r += (int64_t)gridDim.x * blockDim.x) {
+        const bool back = symmetrize && r >= M;
+        const uint64_t i = back ? (uint64_t)(r - M) : (uint64_t)r;
+        uint64_t u, v;
+        ccgen::rmat_edge(rp, i, u, v);
+        if (permute) { u = ccgen::perm_apply(pm, u); v = ccgen::perm_apply(pm, v); }
+        src[r - lo] = (lab_t)(back ? v : u);
+        dst[r - lo] = (lab_t)(back ? u : v);
+    }
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ context
+struct cc_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    cudaStream_t copy_stream = nullptr;
+    bool own_stream = false;
+    int sm_count = 148;
+    int64_t n = 0, m = 0;
+    lab_t* src = nullptr;
+    lab_t* dst = nullptr;
+    int64_t edge_cap = 0;
+    bool own_edges = false;
+    lab_t* labels = nullptr;  // n + 1
+    int64_t label_cap = 0;
+    bool own_labels = false;
+    lab_t* shadow = nullptr;
+    lab_t* before = nullptr;
+    int64_t aux_cap = 0;
+    int* dflags = nullptr;
+    unsigned long long* dcount = nullptr;
+    int* hflags = nullptr;                // pinned mirror of dflags
+    unsigned long long* hcount = nullptr; // pinned
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr, evs = nullptr, eve = nullptr;
+    std::mutex mu;
+};
+
+namespace {
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+int grid_for(const cc_ctx* c, int64_t work, int per_sm = 8) {
+    int64_t b = (work + kThreads - 1) / kThreads;
+    int64_t cap = (int64_t)c->sm_count * per_sm;
+    if (b > cap) b = cap;
+    if (b < 1) b = 1;
+    return (int)b;
+}
+
+template <int OK, bool RED, int NV>
+int launch_sweep_t(cc_ctx* c, const lab_t* R, lab_t* T, int order) {
+    static int occ = 0;
+    if (occ == 0) {
+        int o = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, cck::k_sweep<OK, RED, NV>, kThreads, 0);
+        occ = o > 0 ? o : 1;
+    }
+    const int64_t units = (c->m + 4 * NV - 1) / (4 * NV);
+    const int blocks = grid_for(c, units, occ);
+    cck::k_sweep<OK, RED, NV><<<blocks, kThreads, 0, c->stream>>>(c->src, c->dst, c->m, R, T,
+                                                                   order, c->dflags + kFlagWrote);
+    CUDA_TRY(cudaGetLastError());
+    return CC_OK;
+}
+
+int ensure_aux(cc_ctx* c, bool need_shadow, bool need_before) {
+    if (c->aux_cap < c->n) {
+        if (c->shadow) cudaFree(c->shadow);
+        if (c->before) cudaFree(c->before);
+        c->shadow = c->before = nullptr;
+        c->aux_cap = c->n;
+    }
+    if (need_shadow && !c->shadow) CUDA_TRY(cudaMalloc(&c->shadow, sizeof(lab_t) * (c->n + 1)));
+    if (need_before && !c->before) CUDA_TRY(cudaMalloc(&c->before, sizeof(lab_t) * (c->n + 1)));
+    return CC_OK;
+}
+
+int ensure_labels(cc_ctx* c) {
+    if (c->labels && (c->label_cap >= c->n + 1 || !c->own_labels)) return CC_OK;
+    if (c->labels && c->own_labels) cudaFree(c->labels);
+    CUDA_TRY(cudaMalloc(&c->labels, sizeof(lab_t) * (c->n + 1)));
+    c->label_cap = c->n + 1;
+    c->own_labels = true;
+    return CC_OK;
+}
+
+int ensure_edges(cc_ctx* c, int64_t m) {
+    if (c->own_edges && c->edge_cap >= m && c->src) return CC_OK;
+    if (c->own_edges) {
+        if (c->src) cudaFree(c->src);
+        if (c->dst) cudaFree(c->dst);
+    }
+    c->src = c->dst = nullptr;
+    c->edge_cap = 0;
+    const int64_t cap = m > 0 ? m : 4;
+    CUDA_TRY(cudaMalloc(&c->src, sizeof(lab_t) * cap));
+    CUDA_TRY(cudaMalloc(&c->dst, sizeof(lab_t) * cap));
+    c->edge_cap = cap;
+    c->own_edges = true;
+    return CC_OK;
+}
+
+int set_graph(cc_ctx* c, int64_t m, int64_t n) {
+    if (n < 0 || m < 0) return fail(CC_EINVAL, "vertex and edge counts must be non-negative");
+    if (n > (int64_t)0xFFFFFFFFll)
+        return fail(CC_EINVAL, "n=%lld exceeds the uint32 vertex-ID range", (long long)n);
+    if (m > 0 && n == 0) return fail(CC_EINVAL, "edge endpoint out of range: n=0");
+    c->n = n;
+    c->m = m;
+    return ensure_labels(c);
+}
+
+int read_flags(cc_ctx* c) {
+    CUDA_TRY(cudaMemcpyAsync(c->hflags, c->dflags, sizeof(int) * kNumFlags,
+                             cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaMemcpyAsync(c->hcount, c->dcount, sizeof(unsigned long long),
+                             cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    return CC_OK;
+}
+
+int order_for(const cc_schedule* s, int64_t sweep) {  // engine.py:61-74
+    switch (s->variant) {
+        case CC_VAR_C2:
+        case CC_VAR_CSYN: return 2;
+        case CC_VAR_C1: return 1;
+        case CC_VAR_CM: return s->high_order;
+        case CC_VAR_C11MM: return sweep <= s->warmup ? 1 : s->high_order;
+        case CC_VAR_C1M1M: return (sweep % 2 == 1) ? 1 : s->high_order;
+    }
+    return -1;
+}
+
+// Enqueue one sweep; flag word (and count for sync) left on device.
+int enqueue_sweep(cc_ctx* c, int order, int sync, int atomic, bool count_changes) {
+    if (order < 1) return fail(CC_EINVAL, "operator order must be >= 1");
+    CUDA_TRY(cudaMemsetAsync(c->dflags + kFlagWrote, 0, sizeof(int), c->stream));
+    CUDA_TRY(cudaMemsetAsync(c->dcount, 0, sizeof(unsigned long long), c->stream));
+    if (c->m == 0) return CC_OK;
+    if (sync) {
+        CC_TRY(ensure_aux(c, true, false));
+        const lab_t* R = c->labels;
+        lab_t* T = c->shadow;
+        int rc = order == 1   ? launch_sweep_t<1, true, 2>(c, R, T, order)
+                 : order == 2 ? launch_sweep_t<2, true, 2>(c, R, T, order)
+                              : launch_sweep_t<0, true, 1>(c, R, T, order);
+        if (rc) return rc;
+        CUDA_TRY(cudaMemsetAsync(c->dflags + kFlagWrote, 0, sizeof(int), c->stream));
+        k_commit<<<grid_for(c, c->n), kThreads, 0, c->stream>>>(c->labels, c->shadow, c->n,
+                                                                c->dcount, c->dflags);
+        CUDA_TRY(cudaGetLastError());
+        return CC_OK;
+    }
+    if (count_changes) {
+        CC_TRY(ensure_aux(c, false, true));
+        CUDA_TRY(cudaMemcpyAsync(c->before, c->labels, sizeof(lab_t) * c->n,
+                                 cudaMemcpyDeviceToDevice, c->stream));
+    }
+    lab_t* L = c->labels;
+    int rc;
+    if (atomic) {
+        rc = order == 1   ? launch_sweep_t<1, true, 2>(c, L, L, order)
+             : order == 2 ? launch_sweep_t<2, true, 2>(c, L, L, order)
+                          : launch_sweep_t<0, true, 1>(c, L, L, order);
+    } else {
+        rc = order == 1   ? launch_sweep_t<1, false, 2>(c, L, L, order)
+             : order == 2 ? launch_sweep_t<2, false, 2>(c, L, L, order)
+                          : launch_sweep_t<0, false, 1>(c, L, L, order);
+    }
+    if (rc) return rc;
+    if (count_changes) {
+        k_diff<<<grid_for(c, c->n), kThreads, 0, c->stream>>>(c->labels, c->before, c->n,
+                                                              c->dcount);
+        CUDA_TRY(cudaGetLastError());
+    }
+    return CC_OK;
+}
+
+int enqueue_init(cc_ctx* c, bool sync) {
+    if (c->n == 0) return CC_OK;
+    k_iota<<<grid_for(c, c->n), kThreads, 0, c->stream>>>(c->labels, c->n);
+    CUDA_TRY(cudaGetLastError());
+    if (sync) {
+        CC_TRY(ensure_aux(c, true, false));
+        CUDA_TRY(cudaMemcpyAsync(c->shadow, c->labels, sizeof(lab_t) * c->n,
+                                 cudaMemcpyDeviceToDevice, c->stream));
+    }
+    return CC_OK;
+}
+
+int early_check(cc_ctx* c, int* ok) {  // engine.py:331-348
+    if (c->n == 0) { *ok = 1; return CC_OK; }
+    CUDA_TRY(cudaMemsetAsync(c->dflags + kFlagBad, 0, sizeof(int), c->stream));
+    k_check_idem<<<grid_for(c, c->n), kThreads, 0, c->stream>>>(c->labels, c->n, c->dflags);
+    CUDA_TRY(cudaGetLastError());
+    if (c->m > 0) {
+        k_check_edges<<<grid_for(c, c->m), kThreads, 0, c->stream>>>(c->src, c->dst, c->m,
+                                                                     c->labels, c->dflags);
+        CUDA_TRY(cudaGetLastError());
+    }
+    CC_TRY(read_flags(c));
+    *ok = c->hflags[kFlagBad] == 0;
+    return CC_OK;
+}
+
+int compress(cc_ctx* c, int* rounds) {
+    int r = 0;
+    if (c->n > 0) {
+        for (int it = 0; it < 70; ++it) {
+            CUDA_TRY(cudaMemsetAsync(c->dflags + kFlagCompress, 0, sizeof(int), c->stream));
+            k_compress<<<grid_for(c, c->n), kThreads, 0, c->stream>>>(c->labels, c->n, c->dflags);
+            CUDA_TRY(cudaGetLastError());
+            CC_TRY(read_flags(c));
+            if (!c->hflags[kFlagCompress]) break;
+            ++r;
+        }
+    }
+    if (rounds) *rounds = r;
+    return CC_OK;
+}
+
+int copy_out(cc_ctx* c, void* out, int eb) {
+    if (c->n == 0 || !out) return CC_OK;
+    if (eb == 4) {
+        CUDA_TRY(cudaMemcpyAsync(out, c->labels, sizeof(lab_t) * c->n, cudaMemcpyDeviceToHost,
+                                 c->stream));
+    } else if (eb == 8) {
+        int64_t* tmp = nullptr;
+        CUDA_TRY(cudaMallocAsync((void**)&tmp, sizeof(int64_t) * c->n, c->stream));
+        k_widen<<<grid_for(c, c->n), kThreads, 0, c->stream>>>(c->labels, c->n, tmp);
+        CUDA_TRY(cudaGetLastError());
+        CUDA_TRY(cudaMemcpyAsync(out, tmp, sizeof(int64_t) * c->n, cudaMemcpyDeviceToHost,
+                                 c->stream));
+        CUDA_TRY(cudaFreeAsync(tmp, c->stream));
+    } else {
+        return fail(CC_EINVAL, "label element size must be 4 or 8");
+    }
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    return CC_OK;
+}
+
+template <typename T>
+int stage_impl(cc_ctx* c, const T* edges, int64_t m, bool host) {
+    CUDA_TRY(cudaMemsetAsync(c->dflags + kFlagBad, 0, sizeof(int), c->stream));
+    if (m > 0) {
+        if (!host) {
+            k_stage<T><<<grid_for(c, m), kThreads, 0, c->stream>>>(edges, m, c->n, c->src, c->dst,
+                                                                   c->dflags);
+            CUDA_TRY(cudaGetLastError());
+        } else {
+            // double-buffered H2D chunks on copy_stream overlapped with the
+            // AoS->SoA conversion on the compute stream
+            const int64_t chunk = (int64_t)1 << 23;  // rows per chunk
+            const int64_t cr = std::min<int64_t>(chunk, m);
+            T* buf[2] = {nullptr, nullptr};
+            cudaEvent_t copied[2], freed[2];
+            for (int b = 0; b < 2; ++b) {
+                CUDA_TRY(cudaMalloc(&buf[b], sizeof(T) * 2 * cr));
+                CUDA_TRY(cudaEventCreateWithFlags(&copied[b], cudaEventDisableTiming));
+                CUDA_TRY(cudaEventCreateWithFlags(&freed[b], cudaEventDisableTiming));
+                CUDA_TRY(cudaEventRecord(freed[b], c->stream));
+            }
+            int64_t k = 0;
+            for (int64_t off = 0; off < m; off += cr, ++k) {
+                const int b = (int)(k & 1);
+                const int64_t rows = std::min<int64_t>(cr, m - off);
+                CUDA_TRY(cudaStreamWaitEvent(c->copy_stream, freed[b], 0));
+                CUDA_TRY(cudaMemcpyAsync(buf[b], edges + 2 * off, sizeof(T) * 2 * rows,
+                                         cudaMemcpyHostToDevice, c->copy_stream));
+                CUDA_TRY(cudaEventRecord(copied[b], c->copy_stream));
+                CUDA_TRY(cudaStreamWaitEvent(c->stream, copied[b], 0));
+                k_stage<T><<<grid_for(c, rows), kThreads, 0, c->stream>>>(
+                    buf[b], rows, c->n, c->src + off, c->dst + off, c->dflags);
+                CUDA_TRY(cudaGetLastError());
+                CUDA_TRY(cudaEventRecord(freed[b], c->stream));
+            }
+            CUDA_TRY(cudaStreamSynchronize(c->stream));
+            for (int b = 0; b < 2; ++b) {
+                cudaFree(buf[b]);
+                cudaEventDestroy(copied[b]);
+                cudaEventDestroy(freed[b]);
+            }
+        }
+    }
+    CC_TRY(read_flags(c));
+    if (c->hflags[kFlagBad]) return fail(CC_EINVAL, "edge endpoint out of range (n=%lld)",
+                                         (long long)c->n);
+    return CC_OK;
+}
+
+int stage(cc_ctx* c, const void* edges, int eb, int64_t m, int64_t n, bool host) {
+    if (eb != 4 && eb != 8) return fail(CC_EINVAL, "edge element size must be 4 or 8");
+    if (m > 0 && !edges) return fail(CC_EINVAL, "null edge buffer");
+    CC_TRY(set_graph(c, m, n));
+    CC_TRY(ensure_edges(c, m));
+    if (eb == 4) return stage_impl<int32_t>(c, (const int32_t*)edges, m, host);
+    return stage_impl<int64_t>(c, (const int64_t*)edges, m, host);
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ C-ABI
+extern "C" {
+
+const char* cc_last_error(void) { return g_err; }
+int cc_version(void) { return 1; }
+
+int cc_create(int device, void* stream, cc_ctx** out) {
+    if (!out) return fail(CC_EINVAL, "null output pointer");
+    *out = nullptr;
+    int ndev = 0;
+    CUDA_TRY(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev)
+        return fail(CC_EINVAL, "device %d out of range (%d devices)", device, ndev);
+    DeviceGuard g(device);
+    cc_ctx* c = new cc_ctx();
+    c->device = device;
+    cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device);
+    if (stream) {
+        c->stream = (cudaStream_t)stream;
+    } else {
+        CUDA_TRY(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        c->own_stream = true;
+    }
+    CUDA_TRY(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+    CUDA_TRY(cudaMalloc(&c->dflags, sizeof(int) * kNumFlags));
+    CUDA_TRY(cudaMemset(c->dflags, 0, sizeof(int) * kNumFlags));
+    CUDA_TRY(cudaMalloc(&c->dcount, sizeof(unsigned long long)));
+    CUDA_TRY(cudaHostAlloc(&c->hflags, sizeof(int) * kNumFlags, cudaHostAllocDefault));
+    CUDA_TRY(cudaHostAlloc(&c->hcount, sizeof(unsigned long long), cudaHostAllocDefault));
+    CUDA_TRY(cudaEventCreate(&c->ev0));
+    CUDA_TRY(cudaEventCreate(&c->ev1));
+    CUDA_TRY(cudaEventCreate(&c->evs));
+    CUDA_TRY(cudaEventCreate(&c->eve));
+    *out = c;
+    return CC_OK;
+}
+
+void cc_destroy(cc_ctx* c) {
+    if (!c) return;
+    DeviceGuard g(c->device);
+    cudaStreamSynchronize(c->stream);
+    if (c->own_edges) { cudaFree(c->src); cudaFree(c->dst); }
+    if (c->own_labels) cudaFree(c->labels);
+    cudaFree(c->shadow);
+    cudaFree(c->before);
+    cudaFree(c->dflags);
+    cudaFree(c->dcount);
+    cudaFreeHost(c->hflags);
+    cudaFreeHost(c->hcount);
+    cudaEventDestroy(c->ev0);
+    cudaEventDestroy(c->ev1);
+    cudaEventDestroy(c->evs);
+    cudaEventDestroy(c->eve);
+    cudaStreamDestroy(c->copy_stream);
+    if (c->own_stream) cudaStreamDestroy(c->stream);
+    delete c;
+}
+
+int cc_stage_edges(cc_ctx* c, const void* edges, int eb, int64_t m, int64_t n) {
+    if (!c) return fail(CC_EINVAL, "null context");
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard g(c->device);
+    return stage(c, edges, eb, m, n, true);
+}
+
+int cc_stage_edges_device(cc_ctx* c, const void* edges, int eb, int64_t m, int64_t n) {
+    if (!c) return fail(CC_EINVAL, "null context");
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard g(c->device);
+    return stage(c, edges, eb, m, n, false);
+}
+
+int cc_attach_soa(cc_ctx* c, uint32_t* src, uint32_t* dst, int64_t m, int64_t n) {
+    if (!c) return fail(CC_EINVAL, "null context");
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard g(c->device);
+    if (m > 0 && (!src || !dst)) return fail(CC_EINVAL, "null edge arrays");
+    if (((uintptr_t)src | (uintptr_t)dst) & 15)
+        return fail(CC_EINVAL, "SoA edge arrays must be 16-byte aligned");
+    if (c->own_edges) { cudaFree(c->src); cudaFree(c->dst); }
+    c->src = src;
+    c->dst = dst;
+    c->own_edges = false;
+    c->edge_cap = m;
+    return set_graph(c, m, n);
+}
+
+int cc_attach_labels(cc_ctx* c, uint32_t* labels) {
+    if (!c || !labels) return fail(CC_EINVAL, "null argument");
+    std::lock_guard<std::mutex> lk(c->mu);
+    if (c->own_labels && c->labels) cudaFree(c->labels);
+    c->labels = labels;
+    c->own_labels = false;
+    c->label_cap = c->n + 1;
+    return CC_OK;
+}
+
+int cc_labels_device(cc_ctx* c, uint32_t** out) {
+    if (!c || !out) return fail(CC_EINVAL, "null argument");
+    *out = c->labels;
+    return CC_OK;
+}
+
+int cc_init_labels(cc_ctx* c) {
+    if (!c) return fail(CC_EINVAL, "null context");
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard g(c->device);
+    return enqueue_init(c, false);
+}
+
+int cc_sweep(cc_ctx* c, int order, int sync, int atomic, int* wrote_out) {
+    if (!c) return fail(CC_EINVAL, "null context");
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard g(c->device);
+    if (sync) {
+        CC_TRY(ensure_aux(c, true, false));
+        CUDA_TRY(cudaMemcpyAsync(c->shadow, c->labels, sizeof(lab_t) * c->n,
+                                 cudaMemcpyDeviceToDevice, c->stream));
+    }
+    CC_TRY(enqueue_sweep(c, order, sync, atomic, false));
+    if (wrote_out) {
+        CC_TRY(read_flags(c));
+        *wrote_out = c->hflags[kFlagWrote] != 0;
+    }
+    return CC_OK;
+}
+
+int cc_fold_flag(cc_ctx* c, int first) {
+    if (!c) return fail(CC_EINVAL, "null context");
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard g(c->device);
+    k_fold<<<1, 1, 0, c->stream>>>(c->labels, c->n, c->dflags, first);
+    CUDA_TRY(cudaGetLastError());
+    return CC_OK;
+}
+
+int cc_compress(cc_ctx* c, int* rounds) {
+    if (!c) return fail(CC_EINVAL, "null context");
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard g(c->device);
+    return compress(c, rounds);
+}
+
+int cc_early_check(cc_ctx* c, int* ok) {
+    if (!c || !ok) return fail(CC_EINVAL, "null argument");
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard g(c->device);
+    return early_check(c, ok);
+}
+
+int cc_read_labels(cc_ctx* c, void* out, int eb) {
+    if (!c) return fail(CC_EINVAL, "null context");
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard g(c->device);
+    return copy_out(c, out, eb);
+}
+
+int cc_synchronize(cc_ctx* c) {
+    if (!c) return fail(CC_EINVAL, "null context");
+    DeviceGuard g(c->device);
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    return CC_OK;
+}
+
+// run_contour (engine.py:248-328) over the device kernels.
+int cc_run(cc_ctx* c, const cc_schedule* s, int flags, int64_t cap, void* labels_out, int out_eb,
+           cc_stats* st) {
+    if (!c || !s) return fail(CC_EINVAL, "null argument");
+    if (s->variant < CC_VAR_CSYN || s->variant > CC_VAR_C1M1M)
+        return fail(CC_EINVAL, "unknown variant code %d", s->variant);
+    if (labels_out && out_eb != 4 && out_eb != 8)
+        return fail(CC_EINVAL, "label element size must be 4 or 8");
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard g(c->device);
+    const bool sync = s->sync != 0;
+    const bool count = (flags & CC_RUN_COUNT_CHANGES) != 0;
+    const bool check = (flags & CC_RUN_EARLY_CHECK) != 0;
+    const bool times = (flags & CC_RUN_SWEEP_TIMES) != 0;
+    CUDA_TRY(cudaEventRecord(c->evs, c->stream));
+    CC_TRY(enqueue_init(c, sync));
+    int64_t sweep = 0, until_stable = 0;
+    int converged_by = 0;
+    while (true) {
+        ++sweep;
+        if (sweep > cap)
+            return fail(CC_ECAP, "no convergence after %lld sweeps on n=%lld, m=%lld",
+                        (long long)cap, (long long)c->n, (long long)c->m);
+        const int order = order_for(s, sweep);
+        if (times) CUDA_TRY(cudaEventRecord(c->ev0, c->stream));
+        CC_TRY(enqueue_sweep(c, order, sync, s->atomic, count));
+        if (times) CUDA_TRY(cudaEventRecord(c->ev1, c->stream));
+        CC_TRY(read_flags(c));
+        const bool wrote = c->hflags[kFlagWrote] != 0;
+        const int64_t changed = (sync || count) ? (int64_t)*c->hcount : (wrote ? -1 : 0);
+        if (st && st->changed_per_sweep && sweep <= st->capacity)
+            st->changed_per_sweep[sweep - 1] = changed;
+        if (st && st->sweep_seconds && sweep <= st->capacity) {
+            float ms = 0.f;
+            if (times) cudaEventElapsedTime(&ms, c->ev0, c->ev1);
+            st->sweep_seconds[sweep - 1] = ms * 1e-3;
+        }
+        if (!wrote && changed == 0) { converged_by = 0; break; }
+        until_stable = sweep;
+        if (check) {
+            int ok = 0;
+            CC_TRY(early_check(c, &ok));
+            if (ok) { converged_by = 1; break; }
+        }
+    }
+    int rounds = 0;
+    CC_TRY(compress(c, &rounds));
+    CUDA_TRY(cudaEventRecord(c->eve, c->stream));
+    CUDA_TRY(cudaEventSynchronize(c->eve));
+    float total_ms = 0.f;
+    cudaEventElapsedTime(&total_ms, c->evs, c->eve);
+    if (st) {
+        st->sweeps_executed = sweep;
+        st->sweeps_until_stable = until_stable;
+        st->converged_by = converged_by;
+        st->compress_rounds = rounds;
+        st->converge_seconds = total_ms * 1e-3;
+    }
+    return copy_out(c, labels_out, out_eb);
+}
+
+int cc_mm_order(const int64_t* read, int64_t* target, int64_t n, int64_t w, int64_t v, int order,
+                int inplace, int* changed_out) {
+    if (order < 1) return fail(CC_EINVAL, "operator order must be >= 1");
+    if (!read || !target || n <= 0 || w < 0 || v < 0 || w >= n || v >= n)
+        return fail(CC_EINVAL, "bad single-edge arguments");
+    int64_t* d64 = nullptr;
+    lab_t *R = nullptr, *T = nullptr;
+    int* dch = nullptr;
+    CUDA_TRY(cudaMalloc(&d64, sizeof(int64_t) * n));
+    CUDA_TRY(cudaMalloc(&R, sizeof(lab_t) * n));
+    CUDA_TRY(cudaMalloc(&T, sizeof(lab_t) * n));
+    CUDA_TRY(cudaMalloc(&dch, sizeof(int)));
+    CUDA_TRY(cudaMemset(dch, 0, sizeof(int)));
+    CUDA_TRY(cudaMemcpy(d64, read, sizeof(int64_t) * n, cudaMemcpyHostToDevice));
+    k_from64<<<1, 256>>>(d64, n, R);
+    CUDA_TRY(cudaMemcpy(d64, inplace ? read : target, sizeof(int64_t) * n, cudaMemcpyHostToDevice));
+    k_from64<<<1, 256>>>(d64, n, T);
+    k_single_edge<<<1, 1>>>(R, T, (lab_t)w, (lab_t)v, order, inplace, dch);
+    CUDA_TRY(cudaGetLastError());
+    k_widen<<<1, 256>>>(T, n, d64);
+    std::vector<int64_t> before(target, target + n);
+    if (inplace) before.assign(read, read + n);
+    CUDA_TRY(cudaMemcpy(target, d64, sizeof(int64_t) * n, cudaMemcpyDeviceToHost));
+    int ch = 0;
+    CUDA_TRY(cudaMemcpy(&ch, dch, sizeof(int), cudaMemcpyDeviceToHost));
+    if (!inplace) {
+        ch = 0;
+        for (int64_t i = 0; i < n; ++i) ch |= (target[i] != before[i]);
+    }
+    if (changed_out) *changed_out = ch;
+    cudaFree(d64);
+    cudaFree(R);
+    cudaFree(T);
+    cudaFree(dch);
+    return CC_OK;
+}
+
+int cc_gen_rmat_device(cc_ctx* c, int scale, int ef, uint64_t seed, uint32_t tA, uint32_t tAB,
+                       uint32_t tABC, int symmetrize, int permute, int64_t lo, int64_t hi) {
+    if (!c) return fail(CC_EINVAL, "null context");
+    if (scale < 1 || scale > 32 || ef < 1) return fail(CC_EINVAL, "bad RMAT scale/edgefactor");
+    const int64_t n = (int64_t)1 << scale;
+    const int64_t M = (int64_t)ef * n;
+    const int64_t rows = symmetrize ? 2 * M : M;
+    if (lo < 0 || hi > rows || lo > hi) return fail(CC_EINVAL, "bad RMAT row range");
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard g(c->device);
+    CC_TRY(set_graph(c, hi - lo, n));
+    CC_TRY(ensure_edges(c, hi - lo));
+    ccgen::RmatParams rp{ccgen::key(seed, ccgen::STREAM_RMAT), (uint32_t)scale, tA, tAB, tABC};
+    ccgen::Perm pm = ccgen::perm_init((uint64_t)n, ccgen::key(seed, ccgen::STREAM_PERM));
+    if (hi > lo) {
+        k_gen_rmat<<<grid_for(c, hi - lo, 16), kThreads, 0, c->stream>>>(rp, pm, permute, M, symmetrize,
+                                                                         lo, hi, c->src, c->dst);
+        CUDA_TRY(cudaGetLastError());
+    }
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    return CC_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,197 @@
+// Device side of the Contour hot path for sm_100a.
+//
+// Semantics follow the reference sweep kernel sweep_edges
+// (/root/reference/pkg/src/minmapcc/_kernels.py:35-102):
+//   per edge (w, v), w != v: walk both label chains x0 = w, x_{j+1} = L[x_j]
+//   for up to `order` steps, stopping at a fixed point; z = min of the two
+//   h-fold values; lower every chain cell t to z if L[t] > z.
+// Labels are uint32 (every vertex ID < n <= 2^32-1), edges packed uint32 SoA.
+//
+// Layout / bytes per edge for the order-2 asynchronous sweep (the hot path):
+//   edge stream  : 8 B/edge, read once with 128-bit streaming loads (ld.global.cs)
+//   label gathers: L[u], L[v], then L[L[u]], L[L[v]] (4 x 4 B random, L2-resident
+//                  when 4n bytes fit the 126 MB L2) -- predicated off at fixed points
+//   label stores : <= 4 plain conditional 4 B stores, only where a cell is lowered
+// The "something was lowered" bit is a per-thread bool folded by
+// __syncthreads_or and published with ONE plain store per block (no atomics).
+#pragma once
+#include <stdint.h>
+#include <cuda_runtime.h>
+
+namespace cck {
+
+typedef uint32_t lab_t;
+
+constexpr int kThreads = 256;
+constexpr int kChainBuf = 16;  // buffered chain cells per endpoint for order >= 3
+
+// Store z into cell t.  Async plain (the reference's non-atomic mode,
+// _kernels.py:94-102), or a fire-and-forget atomic min (red.global.min.u32) for
+// the reference's CAS mode (_kernels.py:79-93) and for every synchronous sweep.
+template <bool RED>
+__device__ __forceinline__ void lower(lab_t* T, lab_t t, lab_t z) {
+    if (RED) {
+        atomicMin(T + t, z);
+    } else {
+        T[t] = z;
+    }
+}
+
+// ---- order 1 (C-1 sweeps): z = min(L[w], L[v]); targets w, v -------------
+template <int NE, bool RED>
+__device__ __forceinline__ bool batch_o1(const lab_t* R, lab_t* T, const lab_t (&u)[NE],
+                                         const lab_t (&v)[NE]) {
+    lab_t lu[NE], lv[NE];
+#pragma unroll
+    for (int k = 0; k < NE; ++k) {
+        const bool live = u[k] != v[k];
+        lu[k] = live ? R[u[k]] : 0u;
+        lv[k] = live ? R[v[k]] : 0u;
+    }
+    bool wrote = false;
+#pragma unroll
+    for (int k = 0; k < NE; ++k) {
+        if (u[k] == v[k]) continue;  // self-loop inert (_kernels.py:55-56)
+        const lab_t z = min(lu[k], lv[k]);
+        if (lu[k] > z) { lower<RED>(T, u[k], z); wrote = true; }
+        if (lv[k] > z) { lower<RED>(T, v[k], z); wrote = true; }
+    }
+    return wrote;
+}
+
+// ---- order 2 (C-2 / C-Syn): z = min(L[L[w]], L[L[v]]); targets w, L[w], v, L[v]
+// All four target cells' current values were read while walking the chains
+// (L[w]=lu, L[L[w]]=zu, ...), so the conditional stores need no re-read.
+template <int NE, bool RED>
+__device__ __forceinline__ bool batch_o2(const lab_t* R, lab_t* T, const lab_t (&u)[NE],
+                                         const lab_t (&v)[NE]) {
+    lab_t lu[NE], lv[NE], zu[NE], zv[NE];
+#pragma unroll
+    for (int k = 0; k < NE; ++k) {
+        const bool live = u[k] != v[k];
+        lu[k] = live ? R[u[k]] : u[k];
+        lv[k] = live ? R[v[k]] : v[k];
+    }
+#pragma unroll
+    for (int k = 0; k < NE; ++k) {
+        // second hop only off a fixed point (early stop, _kernels.py:63-65)
+        zu[k] = (lu[k] != u[k]) ? R[lu[k]] : lu[k];
+        zv[k] = (lv[k] != v[k]) ? R[lv[k]] : lv[k];
+    }
+    bool wrote = false;
+#pragma unroll
+    for (int k = 0; k < NE; ++k) {
+        if (u[k] == v[k]) continue;
+        const lab_t z = min(zu[k], zv[k]);
+        if (lu[k] > z) { lower<RED>(T, u[k], z); wrote = true; }
+        if (lu[k] != u[k] && zu[k] > z) { lower<RED>(T, lu[k], z); wrote = true; }
+        if (lv[k] > z) { lower<RED>(T, v[k], z); wrote = true; }
+        if (lv[k] != v[k] && zv[k] > z) { lower<RED>(T, lv[k], z); wrote = true; }
+    }
+    return wrote;
+}
+
+// ---- generic order h (C-m, C-11mm, C-1m1m high sweeps) --------------------
+// Walk both chains buffering up to kChainBuf (cell, value) pairs each, then
+// lower the buffered cells.  Cells beyond the buffer (chains longer than 16
+// hops before a fixed point -- rare) are re-walked from the last buffered
+// successor; re-walking is safe under races because a store needs
+// L[t] > z, and t >= L[t] > z keeps the forest invariant.
+template <bool RED>
+__device__ __forceinline__ bool edge_oh(const lab_t* R, lab_t* T, lab_t w, lab_t v, int order) {
+    if (w == v) return false;
+    lab_t cw[kChainBuf], vw[kChainBuf], cv[kChainBuf], vv[kChainBuf];
+    int nw = 0, nv = 0;
+    lab_t c = w;
+    for (int j = 0; j < order; ++j) {
+        const lab_t nxt = R[c];
+        if (nw < kChainBuf) { cw[nw] = c; vw[nw] = nxt; }
+        ++nw;
+        if (nxt == c) break;
+        c = nxt;
+    }
+    const lab_t zw = c;
+    c = v;
+    for (int j = 0; j < order; ++j) {
+        const lab_t nxt = R[c];
+        if (nv < kChainBuf) { cv[nv] = c; vv[nv] = nxt; }
+        ++nv;
+        if (nxt == c) break;
+        c = nxt;
+    }
+    const lab_t zv = c;
+    const lab_t z = min(zw, zv);
+    bool wrote = false;
+    const int bw = nw < kChainBuf ? nw : kChainBuf;
+    for (int i = 0; i < bw; ++i)
+        if (vw[i] > z) { lower<RED>(T, cw[i], z); wrote = true; }
+    if (nw > kChainBuf) {
+        lab_t x = vw[kChainBuf - 1];
+        for (int j = kChainBuf; j < nw; ++j) {
+            const lab_t nxt = R[x];
+            if (nxt > z) { lower<RED>(T, x, z); wrote = true; }
+            if (nxt == x) break;
+            x = nxt;
+        }
+    }
+    const int bv = nv < kChainBuf ? nv : kChainBuf;
+    for (int i = 0; i < bv; ++i)
+        if (vv[i] > z) { lower<RED>(T, cv[i], z); wrote = true; }
+    if (nv > kChainBuf) {
+        lab_t x = vv[kChainBuf - 1];
+        for (int j = kChainBuf; j < nv; ++j) {
+            const lab_t nxt = R[x];
+            if (nxt > z) { lower<RED>(T, x, z); wrote = true; }
+            if (nxt == x) break;
+            x = nxt;
+        }
+    }
+    return wrote;
+}
+
+template <int OK, int NE, bool RED>
+__device__ __forceinline__ bool batch(const lab_t* R, lab_t* T, const lab_t (&u)[NE],
+                                      const lab_t (&v)[NE], int order) {
+    if (OK == 1) return batch_o1<NE, RED>(R, T, u, v);
+    if (OK == 2) return batch_o2<NE, RED>(R, T, u, v);
+    bool wrote = false;
+#pragma unroll 1
+    for (int k = 0; k < NE; ++k) wrote |= edge_oh<RED>(R, T, u[k], v[k], order);
+    return wrote;
+}
+
+// One sweep over edges [0, m) of the SoA arrays (16-byte aligned).
+// OK: 1, 2 or 0 (generic order).  SYNC: R = labels, T = shadow (atomic min);
+// otherwise R == T (in place).  RED: atomic lowering.  NV: uint4 vectors per
+// array per thread per iteration (4*NV edges in flight per thread).
+template <int OK, bool RED, int NV>
+__global__ void __launch_bounds__(kThreads) k_sweep(const lab_t* __restrict__ src,
+                                                    const lab_t* __restrict__ dst, int64_t m,
+                                                    const lab_t* R, lab_t* T, int order,
+                                                    int* __restrict__ flag) {
+    const int64_t nvec = m >> 2;
+    const uint4* __restrict__ s4 = reinterpret_cast<const uint4*>(src);
+    const uint4* __restrict__ d4 = reinterpret_cast<const uint4*>(dst);
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    bool wrote = false;
+    for (int64_t base = tid; base < nvec; base += stride * NV) {
+        lab_t u[4 * NV], v[4 * NV];
+#pragma unroll
+        for (int q = 0; q < NV; ++q) {
+            const int64_t i = base + (int64_t)q * stride;
+            uint4 a = make_uint4(0, 0, 0, 0), b = make_uint4(0, 0, 0, 0);
+            if (i < nvec) { a = __ldcs(s4 + i); b = __ldcs(d4 + i); }
+            u[4 * q + 0] = a.x; u[4 * q + 1] = a.y; u[4 * q + 2] = a.z; u[4 * q + 3] = a.w;
+            v[4 * q + 0] = b.x; v[4 * q + 1] = b.y; v[4 * q + 2] = b.z; v[4 * q + 3] = b.w;
+        }
+        wrote |= batch<OK, 4 * NV, RED>(R, T, u, v, order);
+    }
+    for (int64_t e = (nvec << 2) + tid; e < m; e += stride) {
+        lab_t u[1] = {src[e]}, v[1] = {dst[e]};
+        wrote |= batch<OK, 1, RED>(R, T, u, v, order);
+    }
+    if (__syncthreads_or(wrote) && threadIdx.x == 0) *flag = 1;
+}
+
+}  // namespace cck

@@ -1,0 +1,103 @@
+"""Multi-GPU driver: edge-sharded sweeps, replicated labels, allreduce-MIN.
+
+One process per GPU (torch.distributed, NCCL over NVLink 5 / NVSwitch).  Each
+rank owns a contiguous shard of the edge rows (the reference's static edge
+chunks per thread, engine.py:296-308, lifted to devices) and a full replica
+of the n labels plus one exchange slot.  A round is ``cadence`` local sweeps
+followed by an in-place ``all_reduce(labels[0:n+1], MIN)``:
+
+* correctness: the element-wise min of valid label arrays is valid (each
+  entry stays in its component and <= its index), so replicas only ever
+  move toward the component minima;
+* termination: slot n holds 1 if this rank's sweeps in the round lowered
+  nothing, else 0, so after the MIN it is 1 iff no rank wrote -- every shard
+  was then at a fixed point of the same replicated array, i.e. converged.
+
+The per-rank compute sits behind a small shard interface so the host logic
+can be exercised with gloo on CPU (tests/test_distributed_gloo.py):
+``labels`` (int32 tensor, n+1), ``init()``, ``sweep(order)``,
+``fold(first)``, ``compress()``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+from . import _lib, graphgen
+
+
+class CudaShard:
+    """A rank's edge shard + label replica on its GPU (libcontour.so)."""
+
+    def __init__(self, ctx: _lib.Context, n: int):
+        import torch
+        if n >= 2 ** 31:
+            raise ValueError("multi-GPU exchange uses int32 labels: n must be < 2^31")
+        self.ctx = ctx
+        self.n = n
+        self.labels = torch.empty(n + 1, dtype=torch.int32, device=f"cuda:{ctx.device}")
+        _lib.check(ctx.lib.cc_attach_labels(ctx.handle, ctypes.c_void_p(self.labels.data_ptr())))
+
+    def init(self):
+        _lib.check(self.ctx.lib.cc_init_labels(self.ctx.handle))
+
+    def sweep(self, order: int, sync: bool = False, atomic: bool = False):
+        _lib.check(self.ctx.lib.cc_sweep(self.ctx.handle, order, int(sync), int(atomic), None))
+
+    def fold(self, first: bool):
+        _lib.check(self.ctx.lib.cc_fold_flag(self.ctx.handle, int(first)))
+
+    def compress(self) -> int:
+        r = ctypes.c_int(0)
+        _lib.check(self.ctx.lib.cc_compress(self.ctx.handle, ctypes.byref(r)))
+        return r.value
+
+
+def shard_rows(total: int, rank: int, world: int, align: int = 4) -> tuple[int, int]:
+    """Contiguous [lo, hi) of `total` rows for `rank`, boundaries aligned."""
+    lo = (total * rank // world) // align * align
+    hi = total if rank == world - 1 else (total * (rank + 1) // world) // align * align
+    return lo, hi
+
+
+class ShardedContour:
+    def __init__(self, shard, n: int, m_total: int, *, order_for=lambda k: 2, cadence: int = 1,
+                 group=None, cap=None):
+        self.shard = shard
+        self.n = n
+        self.m_total = m_total
+        self.order_for = order_for
+        self.cadence = max(1, int(cadence))
+        self.group = group
+        self.cap = n + 2 if cap is None else cap
+
+    @classmethod
+    def from_rmat(cls, scale: int, edgefactor: int, seed: int, rank: int, world: int,
+                  device: int, **kw):
+        import torch
+        ctx = _lib.Context(device, torch.cuda.current_stream(device).cuda_stream)
+        n = 1 << scale
+        total = 2 * edgefactor * n
+        lo, hi = shard_rows(total, rank, world)
+        graphgen.rmat_device(ctx, scale, edgefactor, seed, row_lo=lo, row_hi=hi)
+        return cls(CudaShard(ctx, n), n, total, **kw)
+
+    def run(self) -> int:
+        """Converge; returns the number of exchange rounds."""
+        import torch.distributed as dist
+        self.shard.init()
+        sweep, rounds = 0, 0
+        while True:
+            rounds += 1
+            for k in range(self.cadence):
+                sweep += 1
+                if sweep > self.cap:
+                    from .errors import IterationCapExceeded
+                    raise IterationCapExceeded(f"no convergence after {self.cap} sweeps")
+                self.shard.sweep(self.order_for(sweep))
+                self.shard.fold(first=(k == 0))
+            dist.all_reduce(self.shard.labels, op=dist.ReduceOp.MIN, group=self.group)
+            if int(self.shard.labels[self.n].item()) == 1:
+                break
+        self.shard.compress()
+        return rounds

@@ -1,0 +1,245 @@
+"""Drop-in host mirror of the reference engine's hot-path API.
+
+Mirrors /root/reference/pkg/src/minmapcc/engine.py: the same ``Schedule``,
+``make_schedule``, ``IterationStats`` and ``run_contour(g, schedule,
+threads=1, seed=None)`` signature and return types, so the reference's
+callers (bench.py:136-137, cli.py:126, its tests) can import
+``run_contour``/``make_schedule`` from here instead.  Every sweep runs on the
+B200 through libcontour.so (include/contour.h); there is no CPU path.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+
+from . import _lib
+from .errors import IterationCapExceeded
+
+__all__ = [
+    "LabelArray", "Schedule", "IterationStats", "VARIANTS", "canonical_variant",
+    "make_schedule", "run_contour", "mm_order", "IterationCapExceeded", "stage_graph",
+]
+
+LabelArray = np.ndarray  # (n,) int64, as engine.py:44
+
+VARIANTS = ("C-Syn", "C-1", "C-2", "C-m", "C-11mm", "C-1m1m")  # engine.py:46
+_ORDERED_VARIANTS = {"C-m", "C-11mm", "C-1m1m"}                 # engine.py:48
+_VARIANT_CODE = {v: i for i, v in enumerate(VARIANTS)}          # include/contour.h CC_VAR_*
+
+
+@dataclass(frozen=True)
+class Schedule:
+    """Per-iteration operator orders plus execution-mode flags (engine.py:51-74)."""
+
+    variant: str
+    high_order: int = 1024
+    warmup: int = 2
+    sync: bool = False
+    atomic: bool = True
+
+    def order_for(self, sweep: int) -> int:
+        v = self.variant
+        if v in ("C-2", "C-Syn"):
+            return 2
+        if v == "C-1":
+            return 1
+        if v == "C-m":
+            return self.high_order
+        if v == "C-11mm":
+            return 1 if sweep <= self.warmup else self.high_order
+        if v == "C-1m1m":
+            return 1 if sweep % 2 == 1 else self.high_order
+        raise ValueError(f"unknown variant '{v}'")
+
+
+@dataclass
+class IterationStats:
+    """Sweep accounting for one run (engine.py:77-90).
+
+    ``sweep_seconds`` are CUDA-event device times per sweep.  With
+    ``count_changes=False`` the entries of ``changed_per_sweep`` are -1 for
+    "changed, not counted" and 0 for the final no-change sweep.
+    ``device_seconds`` (extra) is the device time from label init to the
+    compressed labels.
+    """
+
+    sweeps_executed: int
+    sweeps_until_stable: int
+    changed_per_sweep: list = field(default_factory=list)
+    converged_by: str = "change-flag"
+    sweep_seconds: list = field(default_factory=list)
+    device_seconds: float = 0.0
+
+
+_ALIAS = {  # engine.py:108-115
+    "csyn": "C-Syn", "c-syn": "C-Syn", "c1": "C-1", "c-1": "C-1", "c2": "C-2", "c-2": "C-2",
+    "cm": "C-m", "c-m": "C-m", "c11mm": "C-11mm", "c-11mm": "C-11mm",
+    "c1m1m": "C-1m1m", "c-1m1m": "C-1m1m",
+}
+
+
+def canonical_variant(name: str) -> str:
+    canon = _ALIAS.get(name.strip().lower())
+    if canon is None:
+        raise ValueError(f"unknown variant '{name}' (choose from {', '.join(VARIANTS)})")
+    return canon
+
+
+def make_schedule(variant: str, high_order: int = 1024, warmup: int = 2, *,
+                  sync: Optional[bool] = None, atomic: bool = True) -> Schedule:
+    """engine.py:125-152, same validation and ValueError messages."""
+    canon = canonical_variant(variant)
+    if canon in _ORDERED_VARIANTS and high_order < 2:
+        raise ValueError(f"{canon} requires high_order >= 2, got {high_order}")
+    if warmup < 1:
+        raise ValueError(f"warmup must be >= 1, got {warmup}")
+    if canon == "C-Syn":
+        if sync is False:
+            raise ValueError("C-Syn always runs synchronously")
+        sync = True
+    elif sync is None:
+        sync = False
+    return Schedule(variant=canon, high_order=high_order, warmup=warmup, sync=sync, atomic=atomic)
+
+
+def _cc_schedule(s: Schedule) -> _lib.CCSchedule:
+    return _lib.CCSchedule(_VARIANT_CODE[canonical_variant(s.variant)], int(s.high_order),
+                           int(s.warmup), int(bool(s.sync)), int(bool(s.atomic)))
+
+
+_tls = threading.local()
+
+
+def _context(device: int) -> _lib.Context:
+    """One cached context per (caller thread, device) -- SPEC.md:212 reentrancy."""
+    cache = getattr(_tls, "ctx", None)
+    if cache is None:
+        cache = _tls.ctx = {}
+    ctx = cache.get(device)
+    if ctx is None:
+        ctx = cache[device] = _lib.Context(device)
+    return ctx
+
+
+def _unpack_graph(g):
+    if isinstance(g, tuple) and len(g) == 2:
+        n, edges = g
+    else:
+        n, edges = g.n, g.edges  # the duck-typed contract of engine.py:268-270
+    return int(n), edges
+
+
+def stage_graph(ctx: _lib.Context, n: int, edges) -> None:
+    """Stage an (m, 2) edge array (numpy int32/int64 on the host, or a CUDA
+    tensor) as packed uint32 SoA in HBM, with the graph.py:73-79 range check."""
+    lib = ctx.lib
+    if hasattr(edges, "data_ptr") and getattr(edges, "is_cuda", False):
+        e = edges.reshape(-1, 2).contiguous()
+        eb = e.element_size()
+        if eb not in (4, 8):
+            raise ValueError("edges must be int32 or int64")
+        _lib.check(lib.cc_stage_edges_device(ctx.handle, ctypes.c_void_p(e.data_ptr()), eb,
+                                             e.shape[0], n))
+        m = e.shape[0]
+    else:
+        e = np.asarray(edges)
+        if e.size == 0:
+            e = np.zeros((0, 2), dtype=np.int64)
+        if e.ndim != 2 or e.shape[1] != 2:
+            raise ValueError("edges must be a sequence of (u, v) pairs")
+        if e.dtype not in (np.int32, np.int64):
+            e = e.astype(np.int64)
+        e = np.ascontiguousarray(e)
+        m = e.shape[0]
+        _lib.check(lib.cc_stage_edges(ctx.handle, ctypes.c_void_p(e.ctypes.data),
+                                      e.dtype.itemsize, m, n))
+    ctx.n, ctx.m = n, m
+
+
+def run_staged(ctx: _lib.Context, schedule: Schedule, *, count_changes: bool = True,
+               early_check: bool = True, sweep_times: bool = True, cap: Optional[int] = None,
+               labels_out: Optional[np.ndarray] = None):
+    """cc_run on already-staged edges; returns (labels or None, IterationStats)."""
+    n = ctx.n
+    cap = n + 2 if cap is None else int(cap)  # engine.py:275
+    capacity = max(1, min(cap, 1 << 16))
+    changed = np.zeros(capacity, dtype=np.int64)
+    secs = np.zeros(capacity, dtype=np.float64)
+    st = _lib.CCStats()
+    st.capacity = capacity
+    st.changed_per_sweep = changed.ctypes.data_as(_lib._I64P)
+    st.sweep_seconds = secs.ctypes.data_as(_lib._DBLP)
+    flags = ((_lib.CC_RUN_EARLY_CHECK if early_check else 0)
+             | (_lib.CC_RUN_COUNT_CHANGES if count_changes else 0)
+             | (_lib.CC_RUN_SWEEP_TIMES if sweep_times else 0))
+    sched = _cc_schedule(schedule)
+    out_ptr, eb = None, 8
+    if labels_out is not None:
+        if labels_out.dtype not in (np.int64, np.uint32, np.int32) or labels_out.size != n:
+            raise ValueError("labels_out must be a length-n int64/int32/uint32 array")
+        eb = labels_out.dtype.itemsize
+        out_ptr = ctypes.c_void_p(labels_out.ctypes.data)
+    _lib.check(ctx.lib.cc_run(ctx.handle, ctypes.byref(sched), flags, cap, out_ptr, eb,
+                              ctypes.byref(st)))
+    k = int(st.sweeps_executed)
+    cnt = changed[:min(k, capacity)].tolist() + [-1] * max(0, k - capacity)
+    sec = secs[:min(k, capacity)].tolist() + [0.0] * max(0, k - capacity)
+    stats = IterationStats(
+        sweeps_executed=k, sweeps_until_stable=int(st.sweeps_until_stable),
+        changed_per_sweep=[int(x) for x in cnt],
+        converged_by="early-check" if st.converged_by == 1 else "change-flag",
+        sweep_seconds=sec, device_seconds=float(st.converge_seconds))
+    return labels_out, stats
+
+
+def run_contour(g, schedule: Schedule, threads: int = 1, seed: Optional[int] = None, *,
+                device: int = 0, count_changes: bool = True, early_check: bool = True,
+                sweep_times: bool = True) -> tuple[LabelArray, IterationStats]:
+    """Run minimum-mapping sweeps to convergence on the GPU (engine.py:248-328).
+
+    ``g`` is anything with ``.n`` and ``.edges`` ((m, 2) int32/int64 pairs,
+    numpy or CUDA tensor), or an ``(n, edges)`` tuple.  ``threads`` and
+    ``seed`` are validated as in the reference but do not change GPU
+    semantics (every sweep already runs on all SMs).  Returns int64 labels
+    (every entry the minimum vertex ID of its component) and IterationStats.
+    Raises IterationCapExceeded after n+2 sweeps, ValueError on bad input.
+    """
+    if threads < 1:
+        raise ValueError("threads must be >= 1")
+    n, edges = _unpack_graph(g)
+    if n < 0:
+        raise ValueError("vertex count must be non-negative")
+    ctx = _context(device)
+    stage_graph(ctx, n, edges)
+    labels = np.empty(n, dtype=np.int64)
+    _, stats = run_staged(ctx, schedule, count_changes=count_changes, early_check=early_check,
+                          sweep_times=sweep_times, labels_out=labels)
+    return labels, stats
+
+
+def mm_order(target: np.ndarray, read: np.ndarray, w: int, v: int, order: int,
+             atomic: bool = False) -> bool:
+    """Single-edge order-h update (engine.py:209-231) executed by the device
+    edge routines.  ``target is read`` is the asynchronous (in-place) form."""
+    if order < 1:
+        raise ValueError("operator order must be >= 1")
+    if w == v:
+        return False
+    inplace = target is read
+    r = np.ascontiguousarray(read, dtype=np.int64)
+    t = r if inplace else np.ascontiguousarray(target, dtype=np.int64).copy()
+    out = np.empty_like(r) if inplace else t
+    if inplace:
+        out[:] = r
+    ch = ctypes.c_int(0)
+    lib = _lib.load()
+    _lib.check(lib.cc_mm_order(r.ctypes.data_as(_lib._I64P), out.ctypes.data_as(_lib._I64P),
+                               r.size, int(w), int(v), int(order), int(inplace),
+                               ctypes.byref(ch)))
+    target[:] = out
+    return bool(ch.value)

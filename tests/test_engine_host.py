@@ -1,0 +1,58 @@
+"""Host-side logic of the drop-in engine (schedules, validation) -- the same
+known answers as the reference's test_engine.py:99-132, 181-183.  CPU only."""
+
+import pytest
+
+from oracle import oracle
+from paper_2311_02811_b200 import VARIANTS, make_schedule, run_contour
+from paper_2311_02811_b200.engine import Schedule, canonical_variant
+
+
+def test_alternating_variant():
+    s = make_schedule("c1m1m", 1024)
+    assert [s.order_for(k) for k in range(1, 7)] == [1, 1024, 1, 1024, 1, 1024]
+
+
+def test_constant_high_order():
+    assert {make_schedule("cm", 1024).order_for(k) for k in range(1, 9)} == {1024}
+
+
+def test_warmup_then_high():
+    s = make_schedule("c11mm", 8, warmup=2)
+    assert [s.order_for(k) for k in range(1, 7)] == [1, 1, 8, 8, 8, 8]
+
+
+def test_csyn_is_sync_order_two():
+    s = make_schedule("csyn")
+    assert s.sync is True and s.order_for(3) == 2
+    with pytest.raises(ValueError):
+        make_schedule("csyn", sync=False)
+
+
+def test_validation():
+    with pytest.raises(ValueError):
+        make_schedule("c3")
+    with pytest.raises(ValueError):
+        make_schedule("cm", high_order=1)
+    with pytest.raises(ValueError):
+        make_schedule("c2", warmup=0)
+    make_schedule("c1", high_order=1)
+    assert make_schedule("C-2").variant == "C-2"
+    assert canonical_variant(" c-11MM ") == "C-11mm"
+
+
+def test_order_for_matches_oracle_restatement():
+    for v in VARIANTS:
+        s = make_schedule(v, 16, warmup=3)
+        assert [s.order_for(k) for k in range(1, 12)] == \
+            [oracle.order_for(v, k, 16, 3) for k in range(1, 12)]
+
+
+def test_defaults_match_reference():
+    s = Schedule("C-2")
+    assert (s.high_order, s.warmup, s.sync, s.atomic) == (1024, 2, False, True)
+
+
+def test_threads_validated_before_any_device_work():
+    with pytest.raises(ValueError):
+        run_contour((3, [(0, 1), (1, 2)]), make_schedule("c2"), threads=0)

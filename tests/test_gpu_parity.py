@@ -1,0 +1,236 @@
+"""GPU parity: the sm_100a path (through the C-ABI) against the CPU oracle and
+the fixtures made from the reference.  Labels must be bit-exact; synchronous
+runs must also reproduce the reference's per-sweep accounting exactly
+(SURVEY.md Finding 4)."""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+from oracle import gen as spec
+from oracle import oracle
+from paper_2311_02811_b200 import (IterationCapExceeded, VARIANTS, make_schedule, mm_order,
+                                   run_contour)
+from paper_2311_02811_b200 import _lib, engine, graphgen
+
+pytestmark = pytest.mark.gpu
+
+ALL_MODES = [(v, s) for v in VARIANTS for s in ((True,) if v == "C-Syn" else (True, False))]
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a, dtype=np.int64).tobytes()).hexdigest()
+
+
+def check_invariants(labels, stats):
+    assert stats.sweeps_until_stable <= stats.sweeps_executed <= stats.sweeps_until_stable + 1
+    assert stats.converged_by in ("change-flag", "early-check")
+    assert len(stats.changed_per_sweep) == stats.sweeps_executed
+    assert len(stats.sweep_seconds) == stats.sweeps_executed
+    assert oracle.is_star_forest(labels)
+
+
+# ---------------------------------------------------------------- operator
+def test_mm_order_known_answers_on_device(golden):
+    for case in golden["mm_order"]:
+        read = np.asarray(case["labels"], dtype=np.int64)
+        tgt = read.copy()
+        ch = mm_order(tgt, read, case["w"], case["v"], case["order"])
+        assert tgt.tolist() == case["target"] and ch == case["changed"], case
+        inplace = read.copy()
+        ch2 = mm_order(inplace, inplace, case["w"], case["v"], case["order"])
+        assert inplace.tolist() == case["inplace"] and ch2 == case["inplace_changed"], case
+
+
+# ---------------------------------------------------------------- small graphs
+def test_small_graphs_all_modes(golden):
+    for g in golden["graphs"]:
+        e = np.asarray(g["edges"], dtype=np.int64).reshape(-1, 2)
+        for key, exp in g["runs"].items():
+            variant, mode, ho = key.split("|")
+            sync = mode == "sync"
+            sched = make_schedule(variant, int(ho), sync=sync)
+            labels, st = run_contour((g["n"], e), sched)
+            assert labels.tolist() == g["labels"], (g["name"], key)
+            check_invariants(labels, st)
+            if sync:  # deterministic: every stat equals the reference's
+                assert st.sweeps_executed == exp["executed"], (g["name"], key)
+                assert st.sweeps_until_stable == exp["until_stable"], (g["name"], key)
+                assert st.changed_per_sweep == exp["changed"], (g["name"], key)
+                assert st.converged_by == exp["converged_by"], (g["name"], key)
+
+
+def test_small_graphs_plain_and_atomic_async(golden):
+    for g in golden["graphs"][:60]:
+        e = np.asarray(g["edges"], dtype=np.int64).reshape(-1, 2)
+        for atomic in (False, True):
+            for early in (False, True):
+                labels, st = run_contour((g["n"], e), make_schedule("c2", atomic=atomic),
+                                         early_check=early, count_changes=early)
+                assert labels.tolist() == g["labels"], g["name"]
+                check_invariants(labels, st)
+
+
+# ---------------------------------------------------------------- configs
+def _config_edges(params):
+    k = params["kind"]
+    if k == "er":
+        return graphgen.erdos_renyi(params["n"], params["pairs"], params["seed"])
+    if k == "rmat":
+        return graphgen.rmat(params["scale"], params["ef"], params["seed"])
+    if k == "grid":
+        return graphgen.grid(params["rows"], params["cols"], params["p"], params["seed"])
+    return graphgen.forest(params["components"], params["seed"])
+
+
+def test_config_shaped_inputs_against_reference_fixtures(golden):
+    for c in golden["configs"]:
+        n, e = _config_edges(c["params"])
+        assert sha(e) == c["edges_sha256"]
+        for key, exp in c["runs"].items():
+            variant, mode, ho = key.split("|")
+            sync = mode == "sync"
+            labels, st = run_contour((n, e), make_schedule(variant, int(ho), sync=sync))
+            assert sha(labels) == c["labels_sha256"], (c["name"], key)
+            check_invariants(labels, st)
+            if sync:
+                assert (st.sweeps_executed, st.sweeps_until_stable, st.changed_per_sweep,
+                        st.converged_by) == (exp["executed"], exp["until_stable"],
+                                             exp["changed"], exp["converged_by"]), (c["name"], key)
+
+
+@pytest.mark.parametrize("cfg", ["er", "grid1024", "rmat18", "forest2k"])
+def test_mid_size_against_oracle(cfg):
+    if cfg == "er":
+        n, e = graphgen.erdos_renyi(65536, 524288, 1)
+    elif cfg == "grid1024":
+        n, e = graphgen.grid(1024, 1024, 0.55, 2)
+    elif cfg == "rmat18":
+        n, e = graphgen.rmat(18, 16, 3)
+    else:
+        n, e = graphgen.forest(2000, 5)
+    exp = oracle.rem_union_find(n, e)
+    for sched in (make_schedule("c2", atomic=False), make_schedule("c2"), make_schedule("cm"),
+                  make_schedule("c2", sync=True), make_schedule("c1m1m")):
+        labels, st = run_contour((n, e), sched)
+        assert np.array_equal(labels, exp), (cfg, sched)
+        check_invariants(labels, st)
+    ref_sync = oracle.run_contour(n, e, "C-2", sync=True, threads=8)[1]
+    st = run_contour((n, e), make_schedule("c2", sync=True))[1]
+    assert st.changed_per_sweep == ref_sync.changed_per_sweep
+    assert st.sweeps_executed == ref_sync.sweeps_executed
+
+
+def test_rmat22_bench_config_exact():
+    """configs[1] at full size (the bench workload), generated on device."""
+    n, e = graphgen.rmat(22, 16, 1, elem_bytes=4)
+    exp = oracle.rem_union_find(n, e)
+    ctx = _lib.Context(0)
+    graphgen.rmat_device(ctx, 22, 16, 1)
+    labels = np.empty(n, dtype=np.int64)
+    _, st = engine.run_staged(ctx, make_schedule("c2", atomic=False), count_changes=False,
+                              early_check=False, labels_out=labels)
+    assert np.array_equal(labels, exp)
+    assert st.converged_by == "change-flag" and st.changed_per_sweep[-1] == 0
+    labels2, st2 = run_contour((n, e), make_schedule("c2", atomic=False))
+    assert np.array_equal(labels2, exp)
+    ctx.close()
+
+
+def test_device_rmat_generator_matches_host():
+    ctx = _lib.Context(0)
+    n, m = graphgen.rmat_device(ctx, 12, 16, 9)
+    labels = np.empty(n, dtype=np.int64)
+    engine.run_staged(ctx, make_schedule("c2"), labels_out=labels)
+    _, e = graphgen.rmat(12, 16, 9)
+    assert np.array_equal(labels, oracle.rem_union_find(n, e))
+    # shard generation: rows [lo, hi)
+    lo, hi = 1000, 70000
+    graphgen.rmat_device(ctx, 12, 16, 9, row_lo=lo, row_hi=hi)
+    labels2 = np.empty(n, dtype=np.int64)
+    engine.run_staged(ctx, make_schedule("c2"), labels_out=labels2)
+    assert np.array_equal(labels2, oracle.rem_union_find(n, e[lo:hi]))
+    ctx.close()
+
+
+# ---------------------------------------------------------------- edge cases
+def test_edge_cases():
+    labels, st = run_contour((0, np.zeros((0, 2), np.int64)), make_schedule("c2"))
+    assert labels.size == 0 and st.sweeps_until_stable == 0
+    labels, st = run_contour((4, []), make_schedule("c2"))
+    assert labels.tolist() == [0, 1, 2, 3]
+    assert (st.sweeps_executed, st.sweeps_until_stable, st.converged_by) == (1, 0, "change-flag")
+    labels, _ = run_contour((3, [(0, 0), (2, 2)]), make_schedule("c2"))
+    assert labels.tolist() == [0, 1, 2]
+    labels, _ = run_contour((1, [(0, 0)]), make_schedule("cm"))
+    assert labels.tolist() == [0]
+    with pytest.raises(ValueError):
+        run_contour((3, [(0, 3)]), make_schedule("c2"))
+    with pytest.raises(ValueError):
+        run_contour((3, [(-1, 2)]), make_schedule("c2"))
+    with pytest.raises(ValueError):
+        run_contour((3, np.zeros((2, 3), np.int64)), make_schedule("c2"))
+
+
+def test_ragged_tails_and_int32_and_device_inputs():
+    import torch
+    for m in (1, 2, 3, 4, 5, 7, 9, 31, 33, 1023, 1025):
+        n, e = spec.erdos_renyi(200, m, m)
+        exp = oracle.rem_union_find(n, e)
+        for sched in (make_schedule("c2", atomic=False), make_schedule("c1", sync=True),
+                      make_schedule("cm", 5)):
+            assert np.array_equal(run_contour((n, e), sched)[0], exp)
+            assert np.array_equal(run_contour((n, e.astype(np.int32)), sched)[0], exp)
+        t = torch.from_numpy(e).cuda()
+        assert np.array_equal(run_contour((n, t), make_schedule("c2"))[0], exp)
+
+
+def test_iteration_cap_raises():
+    ctx = _lib.Context(0)
+    engine.stage_graph(ctx, 6, np.array([[5, 4], [4, 3], [3, 2], [2, 1], [1, 0]]))
+    with pytest.raises(IterationCapExceeded):
+        engine.run_staged(ctx, make_schedule("c1", sync=True), cap=2)
+    ctx.close()
+
+
+def test_long_chain_high_order_buffer_overflow():
+    """Permuted paths make chains longer than the 16-cell device buffer."""
+    rng = np.random.default_rng(3)
+    for d in (100, 5000):
+        perm = rng.permutation(d + 1)
+        e = np.stack([perm[:-1], perm[1:]], axis=1).astype(np.int64)
+        exp = oracle.rem_union_find(d + 1, e)
+        for sched in (make_schedule("cm", 1024), make_schedule("c11mm", 64),
+                      make_schedule("cm", 1024, sync=True)):
+            assert np.array_equal(run_contour((d + 1, e), sched)[0], exp)
+
+
+def test_sync_c2_log_bound_on_permuted_paths():
+    """Acceptance C2 (test_acceptance.py:132-154) on the device path."""
+    import math
+    rng = np.random.default_rng(20260810)
+    for d in (10, 100, 1000, 100_000):
+        bound = math.ceil(math.log(d, 1.5)) + 1
+        for _ in range(5):
+            perm = rng.permutation(d + 1)
+            e = np.stack([perm[np.arange(d)], perm[np.arange(1, d + 1)]], axis=1)
+            _, st = run_contour((d + 1, e), make_schedule("c2", sync=True))
+            assert st.sweeps_until_stable <= bound
+
+
+def test_increasing_path_c1_sync_is_n_minus_1():
+    """Acceptance C3 (test_acceptance.py:157-166)."""
+    for n in (5, 50, 500):
+        e = np.stack([np.arange(n - 1), np.arange(1, n)], axis=1)
+        _, st = run_contour((n, e), make_schedule("c1", sync=True))
+        assert st.sweeps_until_stable == n - 1
+
+
+def test_race_tolerance_repeated_runs():
+    """Acceptance C5 analogue: racy async sweeps always give identical labels."""
+    n, e = graphgen.erdos_renyi(100_000, 400_000, 99)
+    exp = oracle.rem_union_find(n, e)
+    for _ in range(10):
+        labels, _ = run_contour((n, e), make_schedule("c2", atomic=False))
+        assert np.array_equal(labels, exp)
