@@ -52,6 +52,10 @@ def parse():
     p.add_argument("--early-check", action="store_true",
                    help="run the reference early check after each changing sweep")
     p.add_argument("--seed", type=int, default=1)
+    p.add_argument("--layout", default="input", choices=["input", "src_sorted", "chunk_sorted"],
+                   help="staging-time edge layout (src_sorted: device radix sort by src)")
+    p.add_argument("--no-first-scatter", action="store_true",
+                   help="run sweep 1 with the gathering kernel")
     return p.parse_args()
 
 
@@ -226,13 +230,16 @@ def run_single(args, device):
     # ---- inputs resident in HBM (not timed)
     if spec["kind"] == "rmat":
         n, m = graphgen.rmat_device(ctx, spec["scale"], spec.get("edgefactor", 16), args.seed)
+        if args.layout != "input":
+            _lib.check(ctx.lib.cc_reorder_edges(ctx.handle, engine.LAYOUTS[args.layout]))
         host_edges = None
     else:
         n, host_edges = graphgen.make(spec, args.seed, elem_bytes=4)
-        engine.stage_graph(ctx, n, host_edges)
+        engine.stage_graph(ctx, n, host_edges, args.layout)
         m = host_edges.shape[0]
     sched = make_schedule("c2", atomic=False)
-    kw = dict(count_changes=False, early_check=args.early_check)
+    kw = dict(count_changes=False, early_check=args.early_check,
+              first_scatter=not args.no_first_scatter)
 
     for _ in range(args.warmup):
         engine.run_staged(ctx, sched, sweep_times=False, **kw)
@@ -281,7 +288,7 @@ def run_single(args, device):
         torch.cuda.synchronize()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
-        engine.stage_graph(ctx, n, host_edges)
+        engine.stage_graph(ctx, n, host_edges, args.layout)
         engine.run_staged(ctx, sched, sweep_times=False, labels_out=labels_host, **kw)
         b.record(stream)
         torch.cuda.synchronize()
@@ -308,10 +315,13 @@ def run_single(args, device):
         "vs_baseline": None, "dtype": "u32", "data": "synthetic",
         "config": {"workload": workload_name(args.config, n, m), "n": n, "m_input": m,
                    "schedule": "C-2 async plain stores, ballot/OR flag"
-                               + (", early check" if args.early_check else ""),
+                               + (", early check" if args.early_check else "")
+                               + ("" if args.no_first_scatter else ", load-free sweep 1"),
+                   "layout": args.layout,
                    "parallelism": "single GPU",
                    "l2": "inputs larger than L2 (edge stream 8m B > 126 MB); no flush"},
         "sweeps_per_run": sweeps,
+        "sweep_ms": [round(t * 1e3, 4) for t in stats[-1].sweep_seconds],
         "reference_sweeps": ref_sweeps,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,

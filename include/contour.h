@@ -51,6 +51,8 @@ typedef struct cc_schedule {
 #define CC_RUN_EARLY_CHECK 1   /* early_convergence_check after each changing sweep (engine.py:318-320) */
 #define CC_RUN_COUNT_CHANGES 2 /* exact changed_per_sweep by label diff (engine.py:293,309) */
 #define CC_RUN_SWEEP_TIMES 4   /* per-sweep device times (IterationStats.sweep_seconds) */
+#define CC_RUN_NO_FIRST_SCATTER 8 /* run sweep 1 with the gathering kernel instead of the
+                                     load-free identity scatter (see cc_sweep) */
 
 /* Output of cc_run, the IterationStats contract (engine.py:77-90). */
 typedef struct cc_stats {
@@ -99,9 +101,26 @@ int cc_run(cc_ctx* ctx, const cc_schedule* sched, int flags, int64_t cap,
 /* ---- building blocks (multi-GPU driver, tests) ---- */
 int cc_init_labels(cc_ctx* ctx);
 /* One sweep over the staged edges: sweep_edges(read, target, edges, 0, m, 0,
- * order, use_cas) (_kernels.py:35-102).  Leaves the "wrote" flag on device;
- * if wrote_out != NULL it is synchronously read back. */
-int cc_sweep(cc_ctx* ctx, int order, int sync, int atomic, int* wrote_out);
+ * order, use_cas) (_kernels.py:35-102).  first=1 asserts the labels are the
+ * identity (right after cc_init_labels): the sweep is then the load-free
+ * scatter L[max(u,v)] min= min(u,v), identical to the reference's sweep 1 in
+ * sync mode and a legal interleaving of it in async mode.  Leaves the
+ * "wrote" flag on device; if wrote_out != NULL it is synchronously read back. */
+int cc_sweep(cc_ctx* ctx, int order, int sync, int atomic, int first, int* wrote_out);
+/* Staging-time edge layout (the analogue of the reference's CSR build at
+ * Graph construction, graph.py:80,109-122): mode 0 keeps the input order,
+ * mode 1 stably sorts all rows by src (radix sort on device, m < 2^31),
+ * mode 2 sorts each consecutive chunk of CC_OPT_SORT_CHUNK rows by src, so
+ * label gathers of consecutive rows coalesce. */
+int cc_reorder_edges(cc_ctx* ctx, int mode);
+
+/* Tuning knobs of a context.  Store modes for async sweeps:
+ * 0 plain store, 1 red.global.min, 2 L2 re-check then plain store,
+ * 3 L2 re-check then red.min (atomic schedules accept only 1 and 3). */
+#define CC_OPT_STORE_MODE_PLAIN 1  /* Schedule.atomic == False (default 0) */
+#define CC_OPT_STORE_MODE_ATOMIC 2 /* Schedule.atomic == True (default 1) */
+#define CC_OPT_SORT_CHUNK 3        /* rows per chunk of layout mode 2 (default 2^23) */
+int cc_set_option(cc_ctx* ctx, int option, int64_t value);
 /* Fold the wrote flag into label slot n for an allreduce-min exchange
  * (SURVEY 8(e)): first=1: labels[n] = wrote ? 0 : 1; first=0:
  * labels[n] = min(labels[n], wrote ? 0 : 1).  Clears the flag. */

@@ -15,7 +15,10 @@ _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_PKG, "lib", "libcontour.so")
 
 CC_OK, CC_EINVAL, CC_ECAP, CC_ECUDA = 0, 1, 2, 3
-CC_RUN_EARLY_CHECK, CC_RUN_COUNT_CHANGES, CC_RUN_SWEEP_TIMES = 1, 2, 4
+CC_RUN_EARLY_CHECK, CC_RUN_COUNT_CHANGES, CC_RUN_SWEEP_TIMES, CC_RUN_NO_FIRST_SCATTER = 1, 2, 4, 8
+
+CC_OPT_STORE_MODE_PLAIN, CC_OPT_STORE_MODE_ATOMIC, CC_OPT_SORT_CHUNK = 1, 2, 3
+STORE_PLAIN, STORE_RED, STORE_CHECK_PLAIN, STORE_CHECK_RED = 0, 1, 2, 3
 
 _I64P = ctypes.POINTER(ctypes.c_int64)
 _U32P = ctypes.POINTER(ctypes.c_uint32)
@@ -53,7 +56,9 @@ SIGNATURES = {
                               ctypes.POINTER(CCStats)]),
     "cc_init_labels": (ctypes.c_int, [ctypes.c_void_p]),
     "cc_sweep": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
-                                ctypes.POINTER(ctypes.c_int)]),
+                                ctypes.c_int, ctypes.POINTER(ctypes.c_int)]),
+    "cc_reorder_edges": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
+    "cc_set_option": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int64]),
     "cc_fold_flag": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
     "cc_compress": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_int)]),
     "cc_early_check": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_int)]),
@@ -127,6 +132,9 @@ class Context:
         self.handle = h
         self.n = 0
         self.m = 0
+
+    def set_option(self, option: int, value: int) -> None:
+        check(self.lib.cc_set_option(self.handle, option, value), "cc_set_option")
 
     def close(self):
         if getattr(self, "handle", None):

@@ -7,6 +7,7 @@
 // each sweep is one kernel launch over all edges, and convergence is decided
 // from a one-word device flag instead of an n-sized label diff.
 #include <cuda_runtime.h>
+#include <cub/cub.cuh>
 #include <stdarg.h>
 #include <stdio.h>
 #include <string.h>
@@ -232,6 +233,9 @@ struct cc_ctx {
     int* hflags = nullptr;                // pinned mirror of dflags
     unsigned long long* hcount = nullptr; // pinned
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, evs = nullptr, eve = nullptr;
+    int store_mode_plain = cck::kStorePlain;  // async, Schedule.atomic == False
+    int store_mode_atomic = cck::kStoreRed;   // async, Schedule.atomic == True
+    int64_t sort_chunk = (int64_t)1 << 23;    // rows per chunk for layout mode 2
     std::mutex mu;
 };
 
@@ -258,20 +262,39 @@ int grid_for(const cc_ctx* c, int64_t work, int per_sm = 8) {
     return (int)b;
 }
 
-template <int OK, bool RED, int NV>
+template <int OK, int SM, int NV>
 int launch_sweep_t(cc_ctx* c, const lab_t* R, lab_t* T, int order) {
     static int occ = 0;
     if (occ == 0) {
         int o = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, cck::k_sweep<OK, RED, NV>, kThreads, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, cck::k_sweep<OK, SM, NV>, kThreads, 0);
         occ = o > 0 ? o : 1;
     }
     const int64_t units = (c->m + 4 * NV - 1) / (4 * NV);
     const int blocks = grid_for(c, units, occ);
-    cck::k_sweep<OK, RED, NV><<<blocks, kThreads, 0, c->stream>>>(c->src, c->dst, c->m, R, T,
-                                                                   order, c->dflags + kFlagWrote);
+    cck::k_sweep<OK, SM, NV><<<blocks, kThreads, 0, c->stream>>>(c->src, c->dst, c->m, R, T,
+                                                                  order, c->dflags + kFlagWrote);
     CUDA_TRY(cudaGetLastError());
     return CC_OK;
+}
+
+template <int OK, int NV>
+int launch_store_mode(cc_ctx* c, const lab_t* R, lab_t* T, int order, int sm) {
+    switch (sm) {
+        case cck::kStorePlain: return launch_sweep_t<OK, cck::kStorePlain, NV>(c, R, T, order);
+        case cck::kStoreRed: return launch_sweep_t<OK, cck::kStoreRed, NV>(c, R, T, order);
+        case cck::kStoreCheckPlain:
+            return launch_sweep_t<OK, cck::kStoreCheckPlain, NV>(c, R, T, order);
+        default: return launch_sweep_t<OK, cck::kStoreCheckRed, NV>(c, R, T, order);
+    }
+}
+
+// Order-specialised sweep: order 1 and 2 get unrolled batch kernels, any
+// other order the buffered chain walker.
+int launch_order(cc_ctx* c, const lab_t* R, lab_t* T, int order, int sm) {
+    if (order == 1) return launch_store_mode<1, 2>(c, R, T, order, sm);
+    if (order == 2) return launch_store_mode<2, 2>(c, R, T, order, sm);
+    return launch_store_mode<0, 1>(c, R, T, order, sm);
 }
 
 int ensure_aux(cc_ctx* c, bool need_shadow, bool need_before) {
@@ -343,7 +366,23 @@ int order_for(const cc_schedule* s, int64_t sweep) {  // engine.py:61-74
 }
 
 // Enqueue one sweep; flag word (and count for sync) left on device.
-int enqueue_sweep(cc_ctx* c, int order, int sync, int atomic, bool count_changes) {
+int launch_first(cc_ctx* c, lab_t* T) {
+    static int occ = 0;
+    if (occ == 0) {
+        int o = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, cck::k_sweep_first<2>, kThreads, 0);
+        occ = o > 0 ? o : 1;
+    }
+    const int64_t units = (c->m + 7) / 8;
+    cck::k_sweep_first<2><<<grid_for(c, units, occ), kThreads, 0, c->stream>>>(
+        c->src, c->dst, c->m, T, c->dflags + kFlagWrote);
+    CUDA_TRY(cudaGetLastError());
+    return CC_OK;
+}
+
+// first: labels are the identity (sweep 1 after init) -> load-free scatter.
+int enqueue_sweep(cc_ctx* c, int order, int sync, int atomic, bool count_changes,
+                  bool first = false) {
     if (order < 1) return fail(CC_EINVAL, "operator order must be >= 1");
     CUDA_TRY(cudaMemsetAsync(c->dflags + kFlagWrote, 0, sizeof(int), c->stream));
     CUDA_TRY(cudaMemsetAsync(c->dcount, 0, sizeof(unsigned long long), c->stream));
@@ -352,9 +391,7 @@ int enqueue_sweep(cc_ctx* c, int order, int sync, int atomic, bool count_changes
         CC_TRY(ensure_aux(c, true, false));
         const lab_t* R = c->labels;
         lab_t* T = c->shadow;
-        int rc = order == 1   ? launch_sweep_t<1, true, 2>(c, R, T, order)
-                 : order == 2 ? launch_sweep_t<2, true, 2>(c, R, T, order)
-                              : launch_sweep_t<0, true, 1>(c, R, T, order);
+        int rc = first ? launch_first(c, T) : launch_order(c, R, T, order, cck::kStoreRed);
         if (rc) return rc;
         CUDA_TRY(cudaMemsetAsync(c->dflags + kFlagWrote, 0, sizeof(int), c->stream));
         k_commit<<<grid_for(c, c->n), kThreads, 0, c->stream>>>(c->labels, c->shadow, c->n,
@@ -369,14 +406,10 @@ int enqueue_sweep(cc_ctx* c, int order, int sync, int atomic, bool count_changes
     }
     lab_t* L = c->labels;
     int rc;
-    if (atomic) {
-        rc = order == 1   ? launch_sweep_t<1, true, 2>(c, L, L, order)
-             : order == 2 ? launch_sweep_t<2, true, 2>(c, L, L, order)
-                          : launch_sweep_t<0, true, 1>(c, L, L, order);
+    if (first) {
+        rc = launch_first(c, L);
     } else {
-        rc = order == 1   ? launch_sweep_t<1, false, 2>(c, L, L, order)
-             : order == 2 ? launch_sweep_t<2, false, 2>(c, L, L, order)
-                          : launch_sweep_t<0, false, 1>(c, L, L, order);
+        rc = launch_order(c, L, L, order, atomic ? c->store_mode_atomic : c->store_mode_plain);
     }
     if (rc) return rc;
     if (count_changes) {
@@ -620,7 +653,7 @@ int cc_init_labels(cc_ctx* c) {
     return enqueue_init(c, false);
 }
 
-int cc_sweep(cc_ctx* c, int order, int sync, int atomic, int* wrote_out) {
+int cc_sweep(cc_ctx* c, int order, int sync, int atomic, int first, int* wrote_out) {
     if (!c) return fail(CC_EINVAL, "null context");
     std::lock_guard<std::mutex> lk(c->mu);
     DeviceGuard g(c->device);
@@ -629,7 +662,7 @@ int cc_sweep(cc_ctx* c, int order, int sync, int atomic, int* wrote_out) {
         CUDA_TRY(cudaMemcpyAsync(c->shadow, c->labels, sizeof(lab_t) * c->n,
                                  cudaMemcpyDeviceToDevice, c->stream));
     }
-    CC_TRY(enqueue_sweep(c, order, sync, atomic, false));
+    CC_TRY(enqueue_sweep(c, order, sync, atomic, false, first != 0));
     if (wrote_out) {
         CC_TRY(read_flags(c));
         *wrote_out = c->hflags[kFlagWrote] != 0;
@@ -699,7 +732,8 @@ int cc_run(cc_ctx* c, const cc_schedule* s, int flags, int64_t cap, void* labels
                         (long long)cap, (long long)c->n, (long long)c->m);
         const int order = order_for(s, sweep);
         if (times) CUDA_TRY(cudaEventRecord(c->ev0, c->stream));
-        CC_TRY(enqueue_sweep(c, order, sync, s->atomic, count));
+        CC_TRY(enqueue_sweep(c, order, sync, s->atomic, count,
+                             sweep == 1 && !(flags & CC_RUN_NO_FIRST_SCATTER)));
         if (times) CUDA_TRY(cudaEventRecord(c->ev1, c->stream));
         CC_TRY(read_flags(c));
         const bool wrote = c->hflags[kFlagWrote] != 0;
@@ -733,6 +767,70 @@ int cc_run(cc_ctx* c, const cc_schedule* s, int flags, int64_t cap, void* labels
         st->converge_seconds = total_ms * 1e-3;
     }
     return copy_out(c, labels_out, out_eb);
+}
+
+int cc_set_option(cc_ctx* c, int option, int64_t value) {
+    if (!c) return fail(CC_EINVAL, "null context");
+    std::lock_guard<std::mutex> lk(c->mu);
+    switch (option) {
+        case CC_OPT_STORE_MODE_PLAIN:
+        case CC_OPT_STORE_MODE_ATOMIC:
+            if (value < cck::kStorePlain || value > cck::kStoreCheckRed)
+                return fail(CC_EINVAL, "store mode must be 0..3");
+            // a non-atomic schedule may use any mode (atomic min is one legal
+            // interleaving of plain stores); an atomic one must never lose a
+            // lowering, so it only accepts the red.min modes
+            if (option == CC_OPT_STORE_MODE_ATOMIC &&
+                (value == cck::kStorePlain || value == cck::kStoreCheckPlain))
+                return fail(CC_EINVAL, "atomic schedules need store mode 1 or 3");
+            (option == CC_OPT_STORE_MODE_PLAIN ? c->store_mode_plain : c->store_mode_atomic) =
+                (int)value;
+            return CC_OK;
+        case CC_OPT_SORT_CHUNK:
+            if (value < 1 || value >= ((int64_t)1 << 31))
+                return fail(CC_EINVAL, "sort chunk must be in [1, 2^31)");
+            c->sort_chunk = value;
+            return CC_OK;
+    }
+    return fail(CC_EINVAL, "unknown option %d", option);
+}
+
+int cc_reorder_edges(cc_ctx* c, int mode) {
+    if (!c) return fail(CC_EINVAL, "null context");
+    if (mode == 0) return CC_OK;
+    if (mode != 1 && mode != 2) return fail(CC_EINVAL, "unknown edge layout mode %d", mode);
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard g(c->device);
+    if (c->m < 2) return CC_OK;
+    // mode 1: one global sort by src; mode 2: independent sorts of
+    // consecutive chunks of c->sort_chunk rows (each chunk's label gathers
+    // coalesce almost as well, and chunks can be sorted while later chunks
+    // are still being copied in).
+    const int64_t chunk = mode == 1 ? c->m : std::min<int64_t>(c->sort_chunk, c->m);
+    if (chunk >= ((int64_t)1 << 31)) return fail(CC_EINVAL, "edge reorder needs chunks < 2^31 rows");
+    const int bits = std::max<int>(1, (int)ccgen::perm_bits((uint64_t)c->n));
+    lab_t *ks = nullptr, *vs = nullptr;
+    void* tmp = nullptr;
+    size_t tmp_bytes = 0;
+    CUDA_TRY(cudaMalloc(&ks, sizeof(lab_t) * chunk));
+    CUDA_TRY(cudaMalloc(&vs, sizeof(lab_t) * chunk));
+    CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, c->src, ks, c->dst, vs,
+                                             (int)chunk, 0, bits, c->stream));
+    CUDA_TRY(cudaMalloc(&tmp, tmp_bytes));
+    for (int64_t off = 0; off < c->m; off += chunk) {
+        const int64_t len = std::min<int64_t>(chunk, c->m - off);
+        CUDA_TRY(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, c->src + off, ks, c->dst + off,
+                                                 vs, (int)len, 0, bits, c->stream));
+        CUDA_TRY(cudaMemcpyAsync(c->src + off, ks, sizeof(lab_t) * len, cudaMemcpyDeviceToDevice,
+                                 c->stream));
+        CUDA_TRY(cudaMemcpyAsync(c->dst + off, vs, sizeof(lab_t) * len, cudaMemcpyDeviceToDevice,
+                                 c->stream));
+    }
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    cudaFree(tmp);
+    cudaFree(ks);
+    cudaFree(vs);
+    return CC_OK;
 }
 
 int cc_mm_order(const int64_t* read, int64_t* target, int64_t n, int64_t w, int64_t v, int order,

@@ -25,20 +25,33 @@ typedef uint32_t lab_t;
 constexpr int kThreads = 256;
 constexpr int kChainBuf = 16;  // buffered chain cells per endpoint for order >= 3
 
-// Store z into cell t.  Async plain (the reference's non-atomic mode,
-// _kernels.py:94-102), or a fire-and-forget atomic min (red.global.min.u32) for
-// the reference's CAS mode (_kernels.py:79-93) and for every synchronous sweep.
-template <bool RED>
+// Store modes for lowering cell t to z (the caller already saw L[t] > z):
+//   0 plain store (the reference's non-atomic mode, _kernels.py:94-102)
+//   1 fire-and-forget atomic min, red.global.min.u32 (the reference's CAS
+//     mode, _kernels.py:79-93, and every synchronous sweep)
+//   2 re-check the L2 copy (ld.global.cg) and store plainly only if still > z
+//   3 re-check, then red.min
+// Modes 2/3 trade one L2 load for skipping stores that a concurrent thread
+// already made redundant -- on hot cells those stores invalidate L1 lines
+// that every SM is reading.
+enum { kStorePlain = 0, kStoreRed = 1, kStoreCheckPlain = 2, kStoreCheckRed = 3 };
+
+template <int SM>
 __device__ __forceinline__ void lower(lab_t* T, lab_t t, lab_t z) {
-    if (RED) {
+    if (SM == kStoreRed) {
         atomicMin(T + t, z);
-    } else {
+    } else if (SM == kStorePlain) {
         T[t] = z;
+    } else {
+        if (__ldcg(T + t) > z) {
+            if (SM == kStoreCheckRed) atomicMin(T + t, z);
+            else T[t] = z;
+        }
     }
 }
 
 // ---- order 1 (C-1 sweeps): z = min(L[w], L[v]); targets w, v -------------
-template <int NE, bool RED>
+template <int NE, int SM>
 __device__ __forceinline__ bool batch_o1(const lab_t* R, lab_t* T, const lab_t (&u)[NE],
                                          const lab_t (&v)[NE]) {
     lab_t lu[NE], lv[NE];
@@ -53,8 +66,8 @@ __device__ __forceinline__ bool batch_o1(const lab_t* R, lab_t* T, const lab_t (
     for (int k = 0; k < NE; ++k) {
         if (u[k] == v[k]) continue;  // self-loop inert (_kernels.py:55-56)
         const lab_t z = min(lu[k], lv[k]);
-        if (lu[k] > z) { lower<RED>(T, u[k], z); wrote = true; }
-        if (lv[k] > z) { lower<RED>(T, v[k], z); wrote = true; }
+        if (lu[k] > z) { lower<SM>(T, u[k], z); wrote = true; }
+        if (lv[k] > z) { lower<SM>(T, v[k], z); wrote = true; }
     }
     return wrote;
 }
@@ -62,7 +75,7 @@ __device__ __forceinline__ bool batch_o1(const lab_t* R, lab_t* T, const lab_t (
 // ---- order 2 (C-2 / C-Syn): z = min(L[L[w]], L[L[v]]); targets w, L[w], v, L[v]
 // All four target cells' current values were read while walking the chains
 // (L[w]=lu, L[L[w]]=zu, ...), so the conditional stores need no re-read.
-template <int NE, bool RED>
+template <int NE, int SM>
 __device__ __forceinline__ bool batch_o2(const lab_t* R, lab_t* T, const lab_t (&u)[NE],
                                          const lab_t (&v)[NE]) {
     lab_t lu[NE], lv[NE], zu[NE], zv[NE];
@@ -83,10 +96,10 @@ __device__ __forceinline__ bool batch_o2(const lab_t* R, lab_t* T, const lab_t (
     for (int k = 0; k < NE; ++k) {
         if (u[k] == v[k]) continue;
         const lab_t z = min(zu[k], zv[k]);
-        if (lu[k] > z) { lower<RED>(T, u[k], z); wrote = true; }
-        if (lu[k] != u[k] && zu[k] > z) { lower<RED>(T, lu[k], z); wrote = true; }
-        if (lv[k] > z) { lower<RED>(T, v[k], z); wrote = true; }
-        if (lv[k] != v[k] && zv[k] > z) { lower<RED>(T, lv[k], z); wrote = true; }
+        if (lu[k] > z) { lower<SM>(T, u[k], z); wrote = true; }
+        if (lu[k] != u[k] && zu[k] > z) { lower<SM>(T, lu[k], z); wrote = true; }
+        if (lv[k] > z) { lower<SM>(T, v[k], z); wrote = true; }
+        if (lv[k] != v[k] && zv[k] > z) { lower<SM>(T, lv[k], z); wrote = true; }
     }
     return wrote;
 }
@@ -97,7 +110,7 @@ __device__ __forceinline__ bool batch_o2(const lab_t* R, lab_t* T, const lab_t (
 // hops before a fixed point -- rare) are re-walked from the last buffered
 // successor; re-walking is safe under races because a store needs
 // L[t] > z, and t >= L[t] > z keeps the forest invariant.
-template <bool RED>
+template <int SM>
 __device__ __forceinline__ bool edge_oh(const lab_t* R, lab_t* T, lab_t w, lab_t v, int order) {
     if (w == v) return false;
     lab_t cw[kChainBuf], vw[kChainBuf], cv[kChainBuf], vv[kChainBuf];
@@ -124,24 +137,24 @@ __device__ __forceinline__ bool edge_oh(const lab_t* R, lab_t* T, lab_t w, lab_t
     bool wrote = false;
     const int bw = nw < kChainBuf ? nw : kChainBuf;
     for (int i = 0; i < bw; ++i)
-        if (vw[i] > z) { lower<RED>(T, cw[i], z); wrote = true; }
+        if (vw[i] > z) { lower<SM>(T, cw[i], z); wrote = true; }
     if (nw > kChainBuf) {
         lab_t x = vw[kChainBuf - 1];
         for (int j = kChainBuf; j < nw; ++j) {
             const lab_t nxt = R[x];
-            if (nxt > z) { lower<RED>(T, x, z); wrote = true; }
+            if (nxt > z) { lower<SM>(T, x, z); wrote = true; }
             if (nxt == x) break;
             x = nxt;
         }
     }
     const int bv = nv < kChainBuf ? nv : kChainBuf;
     for (int i = 0; i < bv; ++i)
-        if (vv[i] > z) { lower<RED>(T, cv[i], z); wrote = true; }
+        if (vv[i] > z) { lower<SM>(T, cv[i], z); wrote = true; }
     if (nv > kChainBuf) {
         lab_t x = vv[kChainBuf - 1];
         for (int j = kChainBuf; j < nv; ++j) {
             const lab_t nxt = R[x];
-            if (nxt > z) { lower<RED>(T, x, z); wrote = true; }
+            if (nxt > z) { lower<SM>(T, x, z); wrote = true; }
             if (nxt == x) break;
             x = nxt;
         }
@@ -149,22 +162,22 @@ __device__ __forceinline__ bool edge_oh(const lab_t* R, lab_t* T, lab_t w, lab_t
     return wrote;
 }
 
-template <int OK, int NE, bool RED>
+template <int OK, int NE, int SM>
 __device__ __forceinline__ bool batch(const lab_t* R, lab_t* T, const lab_t (&u)[NE],
                                       const lab_t (&v)[NE], int order) {
-    if (OK == 1) return batch_o1<NE, RED>(R, T, u, v);
-    if (OK == 2) return batch_o2<NE, RED>(R, T, u, v);
+    if (OK == 1) return batch_o1<NE, SM>(R, T, u, v);
+    if (OK == 2) return batch_o2<NE, SM>(R, T, u, v);
     bool wrote = false;
 #pragma unroll 1
-    for (int k = 0; k < NE; ++k) wrote |= edge_oh<RED>(R, T, u[k], v[k], order);
+    for (int k = 0; k < NE; ++k) wrote |= edge_oh<SM>(R, T, u[k], v[k], order);
     return wrote;
 }
 
 // One sweep over edges [0, m) of the SoA arrays (16-byte aligned).
-// OK: 1, 2 or 0 (generic order).  SYNC: R = labels, T = shadow (atomic min);
-// otherwise R == T (in place).  RED: atomic lowering.  NV: uint4 vectors per
+// OK: 1, 2 or 0 (generic order).  Sync sweeps pass R = labels, T = shadow
+// with SM = kStoreRed; async sweeps R == T (in place).  SM: store mode.  NV: uint4 vectors per
 // array per thread per iteration (4*NV edges in flight per thread).
-template <int OK, bool RED, int NV>
+template <int OK, int SM, int NV>
 __global__ void __launch_bounds__(kThreads) k_sweep(const lab_t* __restrict__ src,
                                                     const lab_t* __restrict__ dst, int64_t m,
                                                     const lab_t* R, lab_t* T, int order,
@@ -185,11 +198,59 @@ __global__ void __launch_bounds__(kThreads) k_sweep(const lab_t* __restrict__ sr
             u[4 * q + 0] = a.x; u[4 * q + 1] = a.y; u[4 * q + 2] = a.z; u[4 * q + 3] = a.w;
             v[4 * q + 0] = b.x; v[4 * q + 1] = b.y; v[4 * q + 2] = b.z; v[4 * q + 3] = b.w;
         }
-        wrote |= batch<OK, 4 * NV, RED>(R, T, u, v, order);
+        wrote |= batch<OK, 4 * NV, SM>(R, T, u, v, order);
     }
     for (int64_t e = (nvec << 2) + tid; e < m; e += stride) {
         lab_t u[1] = {src[e]}, v[1] = {dst[e]};
-        wrote |= batch<OK, 1, RED>(R, T, u, v, order);
+        wrote |= batch<OK, 1, SM>(R, T, u, v, order);
+    }
+    if (__syncthreads_or(wrote) && threadIdx.x == 0) *flag = 1;
+}
+
+// First sweep from freshly initialised labels (L[x] = x for all x).
+// Every chain is a single fixed point, so for any order h the operator on
+// edge (u, v) is z = min(u, v) with targets u and v: only the cell max(u, v)
+// can be lowered, to min(u, v).  Reading the start-of-sweep (identity)
+// values instead of gathering them is a legal asynchronous interleaving, and
+// the store is an atomic min (never loses a lowering), so the sweep needs
+// NO label loads: one fire-and-forget red.global.min.u32 per edge.  In sync
+// mode T is the shadow and the result is exactly the reference's sweep 1
+// (shadow = element-wise min over all proposals).
+template <int NV>
+__global__ void __launch_bounds__(kThreads) k_sweep_first(const lab_t* __restrict__ src,
+                                                          const lab_t* __restrict__ dst, int64_t m,
+                                                          lab_t* T, int* __restrict__ flag) {
+    const int64_t nvec = m >> 2;
+    const uint4* __restrict__ s4 = reinterpret_cast<const uint4*>(src);
+    const uint4* __restrict__ d4 = reinterpret_cast<const uint4*>(dst);
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    bool wrote = false;
+    for (int64_t base = tid; base < nvec; base += stride * NV) {
+        uint4 a[NV], b[NV];
+#pragma unroll
+        for (int q = 0; q < NV; ++q) {
+            const int64_t i = base + (int64_t)q * stride;
+            a[q] = make_uint4(0, 0, 0, 0);
+            b[q] = a[q];
+            if (i < nvec) { a[q] = __ldcs(s4 + i); b[q] = __ldcs(d4 + i); }
+        }
+#pragma unroll
+        for (int q = 0; q < NV; ++q) {
+            const lab_t u[4] = {a[q].x, a[q].y, a[q].z, a[q].w};
+            const lab_t v[4] = {b[q].x, b[q].y, b[q].z, b[q].w};
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                if (u[k] != v[k]) {
+                    atomicMin(T + max(u[k], v[k]), min(u[k], v[k]));
+                    wrote = true;
+                }
+            }
+        }
+    }
+    for (int64_t e = (nvec << 2) + tid; e < m; e += stride) {
+        const lab_t u = src[e], v = dst[e];
+        if (u != v) { atomicMin(T + max(u, v), min(u, v)); wrote = true; }
     }
     if (__syncthreads_or(wrote) && threadIdx.x == 0) *flag = 1;
 }

@@ -15,7 +15,7 @@ followed by an in-place ``all_reduce(labels[0:n+1], MIN)``:
 
 The per-rank compute sits behind a small shard interface so the host logic
 can be exercised with gloo on CPU (tests/test_distributed_gloo.py):
-``labels`` (int32 tensor, n+1), ``init()``, ``sweep(order)``,
+``labels`` (int32 tensor, n+1), ``init()``, ``sweep(order, first)``,
 ``fold(first)``, ``compress()``.
 """
 
@@ -41,8 +41,8 @@ class CudaShard:
     def init(self):
         _lib.check(self.ctx.lib.cc_init_labels(self.ctx.handle))
 
-    def sweep(self, order: int, sync: bool = False, atomic: bool = False):
-        _lib.check(self.ctx.lib.cc_sweep(self.ctx.handle, order, int(sync), int(atomic), None))
+    def sweep(self, order: int, first: bool = False):
+        _lib.check(self.ctx.lib.cc_sweep(self.ctx.handle, order, 0, 0, int(first), None))
 
     def fold(self, first: bool):
         _lib.check(self.ctx.lib.cc_fold_flag(self.ctx.handle, int(first)))
@@ -94,7 +94,7 @@ class ShardedContour:
                 if sweep > self.cap:
                     from .errors import IterationCapExceeded
                     raise IterationCapExceeded(f"no convergence after {self.cap} sweeps")
-                self.shard.sweep(self.order_for(sweep))
+                self.shard.sweep(self.order_for(sweep), first=(sweep == 1))
                 self.shard.fold(first=(k == 0))
             dist.all_reduce(self.shard.labels, op=dist.ReduceOp.MIN, group=self.group)
             if int(self.shard.labels[self.n].item()) == 1:

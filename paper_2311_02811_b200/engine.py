@@ -134,9 +134,16 @@ def _unpack_graph(g):
     return int(n), edges
 
 
-def stage_graph(ctx: _lib.Context, n: int, edges) -> None:
+LAYOUTS = {"input": 0, "src_sorted": 1, "chunk_sorted": 2}
+
+
+def stage_graph(ctx: _lib.Context, n: int, edges, layout: str = "input") -> None:
     """Stage an (m, 2) edge array (numpy int32/int64 on the host, or a CUDA
-    tensor) as packed uint32 SoA in HBM, with the graph.py:73-79 range check."""
+    tensor) as packed uint32 SoA in HBM, with the graph.py:73-79 range check.
+    ``layout="src_sorted"`` additionally sorts the rows by src on device
+    (cc_reorder_edges; the analogue of the reference's CSR build)."""
+    if layout not in LAYOUTS:
+        raise ValueError(f"unknown edge layout '{layout}'")
     lib = ctx.lib
     if hasattr(edges, "data_ptr") and getattr(edges, "is_cuda", False):
         e = edges.reshape(-1, 2).contiguous()
@@ -159,11 +166,13 @@ def stage_graph(ctx: _lib.Context, n: int, edges) -> None:
         _lib.check(lib.cc_stage_edges(ctx.handle, ctypes.c_void_p(e.ctypes.data),
                                       e.dtype.itemsize, m, n))
     ctx.n, ctx.m = n, m
+    if LAYOUTS[layout]:
+        _lib.check(lib.cc_reorder_edges(ctx.handle, LAYOUTS[layout]))
 
 
 def run_staged(ctx: _lib.Context, schedule: Schedule, *, count_changes: bool = True,
                early_check: bool = True, sweep_times: bool = True, cap: Optional[int] = None,
-               labels_out: Optional[np.ndarray] = None):
+               labels_out: Optional[np.ndarray] = None, first_scatter: bool = True):
     """cc_run on already-staged edges; returns (labels or None, IterationStats)."""
     n = ctx.n
     cap = n + 2 if cap is None else int(cap)  # engine.py:275
@@ -176,7 +185,8 @@ def run_staged(ctx: _lib.Context, schedule: Schedule, *, count_changes: bool = T
     st.sweep_seconds = secs.ctypes.data_as(_lib._DBLP)
     flags = ((_lib.CC_RUN_EARLY_CHECK if early_check else 0)
              | (_lib.CC_RUN_COUNT_CHANGES if count_changes else 0)
-             | (_lib.CC_RUN_SWEEP_TIMES if sweep_times else 0))
+             | (_lib.CC_RUN_SWEEP_TIMES if sweep_times else 0)
+             | (0 if first_scatter else _lib.CC_RUN_NO_FIRST_SCATTER))
     sched = _cc_schedule(schedule)
     out_ptr, eb = None, 8
     if labels_out is not None:
@@ -199,7 +209,8 @@ def run_staged(ctx: _lib.Context, schedule: Schedule, *, count_changes: bool = T
 
 def run_contour(g, schedule: Schedule, threads: int = 1, seed: Optional[int] = None, *,
                 device: int = 0, count_changes: bool = True, early_check: bool = True,
-                sweep_times: bool = True) -> tuple[LabelArray, IterationStats]:
+                sweep_times: bool = True, layout: str = "input",
+                first_scatter: bool = True) -> tuple[LabelArray, IterationStats]:
     """Run minimum-mapping sweeps to convergence on the GPU (engine.py:248-328).
 
     ``g`` is anything with ``.n`` and ``.edges`` ((m, 2) int32/int64 pairs,
@@ -215,10 +226,10 @@ def run_contour(g, schedule: Schedule, threads: int = 1, seed: Optional[int] = N
     if n < 0:
         raise ValueError("vertex count must be non-negative")
     ctx = _context(device)
-    stage_graph(ctx, n, edges)
+    stage_graph(ctx, n, edges, layout)
     labels = np.empty(n, dtype=np.int64)
     _, stats = run_staged(ctx, schedule, count_changes=count_changes, early_check=early_check,
-                          sweep_times=sweep_times, labels_out=labels)
+                          sweep_times=sweep_times, labels_out=labels, first_scatter=first_scatter)
     return labels, stats
 
 

@@ -1,0 +1,73 @@
+"""Quick per-sweep timing matrix for kernel/layout variants (development aid).
+
+    python tools/explore.py [--layouts a,b] [--stores 0,1] [config ...]
+"""
+import argparse
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+
+from paper_2311_02811_b200 import _lib, engine, graphgen  # noqa: E402
+from paper_2311_02811_b200.engine import make_schedule  # noqa: E402
+
+
+def prepare(cfg, layout, chunk):
+    ctx = _lib.Context(0, torch.cuda.current_stream().cuda_stream)
+    ctx.set_option(_lib.CC_OPT_SORT_CHUNK, chunk)
+    spec = graphgen.CONFIGS[cfg]
+    if spec["kind"] == "rmat":
+        graphgen.rmat_device(ctx, spec["scale"], spec["edgefactor"], 1)
+    else:
+        n, e = graphgen.make(spec, 1, elem_bytes=4)
+        engine.stage_graph(ctx, n, e)
+    ts = []
+    for _ in range(2):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        _lib.check(ctx.lib.cc_reorder_edges(ctx.handle, engine.LAYOUTS[layout]))
+        torch.cuda.synchronize()
+        ts.append(time.perf_counter() - t0)
+    return ctx, min(ts)
+
+
+def measure(ctx, sched, **kw):
+    for _ in range(2):
+        engine.run_staged(ctx, sched, count_changes=False, sweep_times=False, **kw)
+    best = None
+    for _ in range(3):
+        _, st = engine.run_staged(ctx, sched, count_changes=False, **kw)
+        if best is None or st.device_seconds < best.device_seconds:
+            best = st
+    return best
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("configs", nargs="*", default=["rmat22", "grid4096", "er"])
+    ap.add_argument("--layouts", default="input")
+    ap.add_argument("--stores", default="1")
+    ap.add_argument("--chunk", type=int, default=1 << 23)
+    ap.add_argument("--atomic", type=int, default=1)
+    a = ap.parse_args()
+    for cfg in a.configs:
+        for layout in a.layouts.split(","):
+            ctx, tr = prepare(cfg, layout, a.chunk)
+            for sm in map(int, a.stores.split(",")):
+                ctx.set_option(_lib.CC_OPT_STORE_MODE_ATOMIC if a.atomic else
+                               _lib.CC_OPT_STORE_MODE_PLAIN, sm)
+                for fs in (False, True):
+                    st = measure(ctx, make_schedule("c2", atomic=bool(a.atomic)),
+                                 early_check=False, first_scatter=fs)
+                    print(f"{cfg:9s} layout={layout:12s} reorder={tr*1e3:6.2f}ms store={sm} "
+                          f"first_scatter={fs:d} total={st.device_seconds*1e3:8.3f}ms "
+                          f"sweeps={st.sweeps_executed} "
+                          f"sweep_ms={[round(t*1e3,3) for t in st.sweep_seconds]}", flush=True)
+            ctx.close()
+
+
+if __name__ == "__main__":
+    main()
