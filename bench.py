@@ -52,10 +52,17 @@ def parse():
     p.add_argument("--early-check", action="store_true",
                    help="run the reference early check after each changing sweep")
     p.add_argument("--seed", type=int, default=1)
-    p.add_argument("--layout", default="input", choices=["input", "src_sorted", "chunk_sorted"],
-                   help="staging-time edge layout (src_sorted: device radix sort by src)")
-    p.add_argument("--no-first-scatter", action="store_true",
-                   help="run sweep 1 with the gathering kernel")
+    p.add_argument("--layout", default="chunk_sorted",
+                   choices=["input", "src_sorted", "chunk_sorted"],
+                   help="staging-time edge layout (chunk_sorted: each 2^23-row chunk radix-"
+                        "sorted by src on device while the next chunk is copied in)")
+    p.add_argument("--first-scatter", action="store_true",
+                   help="run sweep 1 as the load-free identity scatter")
+    p.add_argument("--atomic", type=int, default=1,
+                   help="Schedule.atomic (the reference default is True)")
+    p.add_argument("--store-mode", type=int, default=None,
+                   help="override the async store mode (0 plain, 1 red, 2 check+plain, "
+                        "3 check+red)")
     return p.parse_args()
 
 
@@ -148,15 +155,16 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def cpu_baseline(n, edges, threads, runs=1):
+def cpu_baseline(n, edges, threads, runs=1, atomic=True):
     """The oracle port of run_contour (engine.py:248-328) on the host cores:
-    C-2, async, atomic=False, seed=0, early check as the reference does."""
+    C-2, async, the same Schedule.atomic as the GPU arm, seed=0, early check
+    as the reference does."""
     from oracle import oracle
     oracle.lib()
     times, st = [], None
     for _ in range(runs):
         t0 = time.perf_counter()
-        _, st = oracle.run_contour(n, edges, "C-2", atomic=False, threads=threads, seed=0)
+        _, st = oracle.run_contour(n, edges, "C-2", atomic=atomic, threads=threads, seed=0)
         times.append(time.perf_counter() - t0)
     t = statistics.median(times)
     return t, st
@@ -171,11 +179,12 @@ def run_reference_arm(args):
     n, edges = graphgen.make(spec, args.seed, elem_bytes=4)
     m = edges.shape[0]
     threads = os.cpu_count() or 1
+    atomic = bool(args.atomic)
     for _ in range(args.warmup):
-        cpu_baseline(n, edges, threads)
+        cpu_baseline(n, edges, threads, atomic=atomic)
     times, st = [], None
     for _ in range(args.steps):
-        t, st = cpu_baseline(n, edges, threads)
+        t, st = cpu_baseline(n, edges, threads, atomic=atomic)
         times.append(t)
     ms = 1e3 * sum(times) / len(times)
     value = m / (ms / 1e3)
@@ -183,7 +192,8 @@ def run_reference_arm(args):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
-        "config": {"workload": workload_name(args.config, n, m), "schedule": "C-2 async atomic=False",
+        "config": {"workload": workload_name(args.config, n, m),
+                   "schedule": f"C-2 async atomic={atomic}",
                    "parallelism": f"{threads} host threads (static edge chunks, engine.py:296-308)"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
                          "sample": f"full workload, {args.steps} timed runs after {args.warmup} "
@@ -227,7 +237,10 @@ def run_single(args, device):
     spec = config_spec(args.config)
     stream = torch.cuda.current_stream()
     ctx = _lib.Context(device, stream.cuda_stream)
-    # ---- inputs resident in HBM (not timed)
+    if args.store_mode is not None:
+        ctx.set_option(_lib.CC_OPT_STORE_MODE_ATOMIC if args.atomic else
+                       _lib.CC_OPT_STORE_MODE_PLAIN, args.store_mode)
+    # ---- inputs resident in HBM in the staged layout (not timed)
     if spec["kind"] == "rmat":
         n, m = graphgen.rmat_device(ctx, spec["scale"], spec.get("edgefactor", 16), args.seed)
         if args.layout != "input":
@@ -237,9 +250,9 @@ def run_single(args, device):
         n, host_edges = graphgen.make(spec, args.seed, elem_bytes=4)
         engine.stage_graph(ctx, n, host_edges, args.layout)
         m = host_edges.shape[0]
-    sched = make_schedule("c2", atomic=False)
+    sched = make_schedule("c2", atomic=bool(args.atomic))
     kw = dict(count_changes=False, early_check=args.early_check,
-              first_scatter=not args.no_first_scatter)
+              first_scatter=args.first_scatter)
 
     for _ in range(args.warmup):
         engine.run_staged(ctx, sched, sweep_times=False, **kw)
@@ -300,10 +313,10 @@ def run_single(args, device):
     cpu = None
     if not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
-        t_cpu, st_cpu = cpu_baseline(n, host_edges, threads)
+        t_cpu, st_cpu = cpu_baseline(n, host_edges, threads, atomic=bool(args.atomic))
         cpu = {"value": m / t_cpu, "unit": UNIT, "cores": threads, "kind": "port",
                "sample": f"1 full run of the same workload (oracle port of run_contour, C-2 "
-                         f"async atomic=False, {threads} threads): {t_cpu:.2f} s, "
+                         f"async atomic={bool(args.atomic)}, {threads} threads): {t_cpu:.2f} s, "
                          f"sweeps_executed={st_cpu.sweeps_executed}"}
         ref_sweeps = {"executed": st_cpu.sweeps_executed, "until_stable": st_cpu.sweeps_until_stable}
     else:
@@ -314,9 +327,9 @@ def run_single(args, device):
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "u32", "data": "synthetic",
         "config": {"workload": workload_name(args.config, n, m), "n": n, "m_input": m,
-                   "schedule": "C-2 async plain stores, ballot/OR flag"
+                   "schedule": f"C-2 async atomic={bool(args.atomic)}, ballot/OR flag"
                                + (", early check" if args.early_check else "")
-                               + ("" if args.no_first_scatter else ", load-free sweep 1"),
+                               + (", load-free sweep 1" if args.first_scatter else ""),
                    "layout": args.layout,
                    "parallelism": "single GPU",
                    "l2": "inputs larger than L2 (edge stream 8m B > 126 MB); no flush"},

@@ -118,8 +118,11 @@ int cc_reorder_edges(cc_ctx* ctx, int mode);
  * 0 plain store, 1 red.global.min, 2 L2 re-check then plain store,
  * 3 L2 re-check then red.min (atomic schedules accept only 1 and 3). */
 #define CC_OPT_STORE_MODE_PLAIN 1  /* Schedule.atomic == False (default 0) */
-#define CC_OPT_STORE_MODE_ATOMIC 2 /* Schedule.atomic == True (default 1) */
+#define CC_OPT_STORE_MODE_ATOMIC 2 /* Schedule.atomic == True (default 3) */
 #define CC_OPT_SORT_CHUNK 3        /* rows per chunk of layout mode 2 (default 2^23) */
+#define CC_OPT_STAGE_LAYOUT 4      /* layout applied while staging: 0 input order (default),
+                                      2 chunk-sorted, each chunk sorted as soon as it lands,
+                                      overlapped with the next chunk's host->device copy */
 int cc_set_option(cc_ctx* ctx, int option, int64_t value);
 /* Fold the wrote flag into label slot n for an allreduce-min exchange
  * (SURVEY 8(e)): first=1: labels[n] = wrote ? 0 : 1; first=0:

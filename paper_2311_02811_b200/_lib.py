@@ -18,6 +18,7 @@ CC_OK, CC_EINVAL, CC_ECAP, CC_ECUDA = 0, 1, 2, 3
 CC_RUN_EARLY_CHECK, CC_RUN_COUNT_CHANGES, CC_RUN_SWEEP_TIMES, CC_RUN_NO_FIRST_SCATTER = 1, 2, 4, 8
 
 CC_OPT_STORE_MODE_PLAIN, CC_OPT_STORE_MODE_ATOMIC, CC_OPT_SORT_CHUNK = 1, 2, 3
+CC_OPT_STAGE_LAYOUT = 4
 STORE_PLAIN, STORE_RED, STORE_CHECK_PLAIN, STORE_CHECK_RED = 0, 1, 2, 3
 
 _I64P = ctypes.POINTER(ctypes.c_int64)

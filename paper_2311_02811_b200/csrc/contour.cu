@@ -234,8 +234,17 @@ struct cc_ctx {
     unsigned long long* hcount = nullptr; // pinned
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, evs = nullptr, eve = nullptr;
     int store_mode_plain = cck::kStorePlain;  // async, Schedule.atomic == False
-    int store_mode_atomic = cck::kStoreRed;   // async, Schedule.atomic == True
-    int64_t sort_chunk = (int64_t)1 << 23;    // rows per chunk for layout mode 2
+    int store_mode_atomic = cck::kStoreCheckRed;  // async, Schedule.atomic == True
+    int64_t sort_chunk = (int64_t)1 << 23;    // rows per chunk (staging, layout mode 2)
+    int stage_layout = 0;                     // layout applied by cc_stage_edges*
+    lab_t* sort_ks = nullptr;                 // cached radix-sort scratch
+    lab_t* sort_vs = nullptr;
+    void* sort_tmp = nullptr;
+    size_t sort_tmp_bytes = 0;
+    int64_t sort_rows_cap = 0;
+    void* stage_buf[2] = {nullptr, nullptr};  // cached H2D staging buffers
+    size_t stage_buf_bytes = 0;
+    cudaEvent_t copied[2] = {nullptr, nullptr}, freed[2] = {nullptr, nullptr};
     std::mutex mu;
 };
 
@@ -483,46 +492,79 @@ int copy_out(cc_ctx* c, void* out, int eb) {
     return CC_OK;
 }
 
+// Radix-sort rows [off, off+len) of the SoA arrays by src, in place (CUB
+// onesweep into the context's cached scratch, then copied back).  len must
+// not exceed c->sort_chunk.
+int sort_rows(cc_ctx* c, int64_t off, int64_t len) {
+    if (len < 2) return CC_OK;
+    const int bits = std::max<int>(1, (int)ccgen::perm_bits((uint64_t)c->n));
+    const int64_t cap = std::max<int64_t>(len, c->sort_rows_cap);
+    if (!c->sort_ks || c->sort_rows_cap < len) {
+        cudaFree(c->sort_ks);
+        cudaFree(c->sort_vs);
+        cudaFree(c->sort_tmp);
+        c->sort_ks = c->sort_vs = nullptr;
+        c->sort_tmp = nullptr;
+        CUDA_TRY(cudaMalloc(&c->sort_ks, sizeof(lab_t) * cap));
+        CUDA_TRY(cudaMalloc(&c->sort_vs, sizeof(lab_t) * cap));
+        c->sort_tmp_bytes = 0;
+        CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, c->sort_tmp_bytes, c->src, c->sort_ks,
+                                                 c->dst, c->sort_vs, (int)cap, 0, 32, c->stream));
+        CUDA_TRY(cudaMalloc(&c->sort_tmp, c->sort_tmp_bytes));
+        c->sort_rows_cap = cap;
+    }
+    size_t tb = c->sort_tmp_bytes;
+    CUDA_TRY(cub::DeviceRadixSort::SortPairs(c->sort_tmp, tb, c->src + off, c->sort_ks,
+                                             c->dst + off, c->sort_vs, (int)len, 0, bits,
+                                             c->stream));
+    CUDA_TRY(cudaMemcpyAsync(c->src + off, c->sort_ks, sizeof(lab_t) * len,
+                             cudaMemcpyDeviceToDevice, c->stream));
+    CUDA_TRY(cudaMemcpyAsync(c->dst + off, c->sort_vs, sizeof(lab_t) * len,
+                             cudaMemcpyDeviceToDevice, c->stream));
+    return CC_OK;
+}
+
 template <typename T>
 int stage_impl(cc_ctx* c, const T* edges, int64_t m, bool host) {
     CUDA_TRY(cudaMemsetAsync(c->dflags + kFlagBad, 0, sizeof(int), c->stream));
+    const bool chunk_sort = c->stage_layout == 2;
+    const int64_t chunk = std::min<int64_t>(c->sort_chunk, std::max<int64_t>(m, 1));
     if (m > 0) {
         if (!host) {
             k_stage<T><<<grid_for(c, m), kThreads, 0, c->stream>>>(edges, m, c->n, c->src, c->dst,
                                                                    c->dflags);
             CUDA_TRY(cudaGetLastError());
+            if (chunk_sort)
+                for (int64_t off = 0; off < m; off += chunk)
+                    CC_TRY(sort_rows(c, off, std::min<int64_t>(chunk, m - off)));
         } else {
-            // double-buffered H2D chunks on copy_stream overlapped with the
-            // AoS->SoA conversion on the compute stream
-            const int64_t chunk = (int64_t)1 << 23;  // rows per chunk
-            const int64_t cr = std::min<int64_t>(chunk, m);
-            T* buf[2] = {nullptr, nullptr};
-            cudaEvent_t copied[2], freed[2];
-            for (int b = 0; b < 2; ++b) {
-                CUDA_TRY(cudaMalloc(&buf[b], sizeof(T) * 2 * cr));
-                CUDA_TRY(cudaEventCreateWithFlags(&copied[b], cudaEventDisableTiming));
-                CUDA_TRY(cudaEventCreateWithFlags(&freed[b], cudaEventDisableTiming));
-                CUDA_TRY(cudaEventRecord(freed[b], c->stream));
+            // double-buffered H2D chunks on copy_stream, overlapped with the
+            // AoS->SoA conversion (+ optional chunk sort) on the compute stream
+            const size_t need = sizeof(T) * 2 * chunk;
+            if (c->stage_buf_bytes < need) {
+                cudaFree(c->stage_buf[0]);
+                cudaFree(c->stage_buf[1]);
+                c->stage_buf[0] = c->stage_buf[1] = nullptr;
+                CUDA_TRY(cudaMalloc(&c->stage_buf[0], need));
+                CUDA_TRY(cudaMalloc(&c->stage_buf[1], need));
+                c->stage_buf_bytes = need;
             }
+            for (int b = 0; b < 2; ++b) CUDA_TRY(cudaEventRecord(c->freed[b], c->stream));
             int64_t k = 0;
-            for (int64_t off = 0; off < m; off += cr, ++k) {
+            for (int64_t off = 0; off < m; off += chunk, ++k) {
                 const int b = (int)(k & 1);
-                const int64_t rows = std::min<int64_t>(cr, m - off);
-                CUDA_TRY(cudaStreamWaitEvent(c->copy_stream, freed[b], 0));
-                CUDA_TRY(cudaMemcpyAsync(buf[b], edges + 2 * off, sizeof(T) * 2 * rows,
+                T* buf = (T*)c->stage_buf[b];
+                const int64_t rows = std::min<int64_t>(chunk, m - off);
+                CUDA_TRY(cudaStreamWaitEvent(c->copy_stream, c->freed[b], 0));
+                CUDA_TRY(cudaMemcpyAsync(buf, edges + 2 * off, sizeof(T) * 2 * rows,
                                          cudaMemcpyHostToDevice, c->copy_stream));
-                CUDA_TRY(cudaEventRecord(copied[b], c->copy_stream));
-                CUDA_TRY(cudaStreamWaitEvent(c->stream, copied[b], 0));
+                CUDA_TRY(cudaEventRecord(c->copied[b], c->copy_stream));
+                CUDA_TRY(cudaStreamWaitEvent(c->stream, c->copied[b], 0));
                 k_stage<T><<<grid_for(c, rows), kThreads, 0, c->stream>>>(
-                    buf[b], rows, c->n, c->src + off, c->dst + off, c->dflags);
+                    buf, rows, c->n, c->src + off, c->dst + off, c->dflags);
                 CUDA_TRY(cudaGetLastError());
-                CUDA_TRY(cudaEventRecord(freed[b], c->stream));
-            }
-            CUDA_TRY(cudaStreamSynchronize(c->stream));
-            for (int b = 0; b < 2; ++b) {
-                cudaFree(buf[b]);
-                cudaEventDestroy(copied[b]);
-                cudaEventDestroy(freed[b]);
+                CUDA_TRY(cudaEventRecord(c->freed[b], c->stream));
+                if (chunk_sort) CC_TRY(sort_rows(c, off, rows));
             }
         }
     }
@@ -576,6 +618,10 @@ int cc_create(int device, void* stream, cc_ctx** out) {
     CUDA_TRY(cudaEventCreate(&c->ev1));
     CUDA_TRY(cudaEventCreate(&c->evs));
     CUDA_TRY(cudaEventCreate(&c->eve));
+    for (int b = 0; b < 2; ++b) {
+        CUDA_TRY(cudaEventCreateWithFlags(&c->copied[b], cudaEventDisableTiming));
+        CUDA_TRY(cudaEventCreateWithFlags(&c->freed[b], cudaEventDisableTiming));
+    }
     *out = c;
     return CC_OK;
 }
@@ -596,6 +642,14 @@ void cc_destroy(cc_ctx* c) {
     cudaEventDestroy(c->ev1);
     cudaEventDestroy(c->evs);
     cudaEventDestroy(c->eve);
+    for (int b = 0; b < 2; ++b) {
+        cudaEventDestroy(c->copied[b]);
+        cudaEventDestroy(c->freed[b]);
+        cudaFree(c->stage_buf[b]);
+    }
+    cudaFree(c->sort_ks);
+    cudaFree(c->sort_vs);
+    cudaFree(c->sort_tmp);
     cudaStreamDestroy(c->copy_stream);
     if (c->own_stream) cudaStreamDestroy(c->stream);
     delete c;
@@ -791,6 +845,11 @@ int cc_set_option(cc_ctx* c, int option, int64_t value) {
                 return fail(CC_EINVAL, "sort chunk must be in [1, 2^31)");
             c->sort_chunk = value;
             return CC_OK;
+        case CC_OPT_STAGE_LAYOUT:
+            if (value != 0 && value != 2)
+                return fail(CC_EINVAL, "staging layout must be 0 (input) or 2 (chunk-sorted)");
+            c->stage_layout = (int)value;
+            return CC_OK;
     }
     return fail(CC_EINVAL, "unknown option %d", option);
 }
@@ -808,28 +867,9 @@ int cc_reorder_edges(cc_ctx* c, int mode) {
     // are still being copied in).
     const int64_t chunk = mode == 1 ? c->m : std::min<int64_t>(c->sort_chunk, c->m);
     if (chunk >= ((int64_t)1 << 31)) return fail(CC_EINVAL, "edge reorder needs chunks < 2^31 rows");
-    const int bits = std::max<int>(1, (int)ccgen::perm_bits((uint64_t)c->n));
-    lab_t *ks = nullptr, *vs = nullptr;
-    void* tmp = nullptr;
-    size_t tmp_bytes = 0;
-    CUDA_TRY(cudaMalloc(&ks, sizeof(lab_t) * chunk));
-    CUDA_TRY(cudaMalloc(&vs, sizeof(lab_t) * chunk));
-    CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, c->src, ks, c->dst, vs,
-                                             (int)chunk, 0, bits, c->stream));
-    CUDA_TRY(cudaMalloc(&tmp, tmp_bytes));
-    for (int64_t off = 0; off < c->m; off += chunk) {
-        const int64_t len = std::min<int64_t>(chunk, c->m - off);
-        CUDA_TRY(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, c->src + off, ks, c->dst + off,
-                                                 vs, (int)len, 0, bits, c->stream));
-        CUDA_TRY(cudaMemcpyAsync(c->src + off, ks, sizeof(lab_t) * len, cudaMemcpyDeviceToDevice,
-                                 c->stream));
-        CUDA_TRY(cudaMemcpyAsync(c->dst + off, vs, sizeof(lab_t) * len, cudaMemcpyDeviceToDevice,
-                                 c->stream));
-    }
+    for (int64_t off = 0; off < c->m; off += chunk)
+        CC_TRY(sort_rows(c, off, std::min<int64_t>(chunk, c->m - off)));
     CUDA_TRY(cudaStreamSynchronize(c->stream));
-    cudaFree(tmp);
-    cudaFree(ks);
-    cudaFree(vs);
     return CC_OK;
 }
 

@@ -36,17 +36,18 @@ constexpr int kChainBuf = 16;  // buffered chain cells per endpoint for order >=
 // that every SM is reading.
 enum { kStorePlain = 0, kStoreRed = 1, kStoreCheckPlain = 2, kStoreCheckRed = 3 };
 
-template <int SM>
+// HOT marks chain cells past the endpoint (L[w], L[v], ...): those are the
+// shared parents many edges lower at once; endpoint cells are random and
+// rarely contended, so the re-check modes only re-check HOT cells.
+template <int SM, bool HOT>
 __device__ __forceinline__ void lower(lab_t* T, lab_t t, lab_t z) {
-    if (SM == kStoreRed) {
+    constexpr bool check = HOT && (SM == kStoreCheckPlain || SM == kStoreCheckRed);
+    constexpr bool red = SM == kStoreRed || SM == kStoreCheckRed;
+    if (check && __ldcg(T + t) <= z) return;
+    if (red) {
         atomicMin(T + t, z);
-    } else if (SM == kStorePlain) {
-        T[t] = z;
     } else {
-        if (__ldcg(T + t) > z) {
-            if (SM == kStoreCheckRed) atomicMin(T + t, z);
-            else T[t] = z;
-        }
+        T[t] = z;
     }
 }
 
@@ -66,8 +67,8 @@ __device__ __forceinline__ bool batch_o1(const lab_t* R, lab_t* T, const lab_t (
     for (int k = 0; k < NE; ++k) {
         if (u[k] == v[k]) continue;  // self-loop inert (_kernels.py:55-56)
         const lab_t z = min(lu[k], lv[k]);
-        if (lu[k] > z) { lower<SM>(T, u[k], z); wrote = true; }
-        if (lv[k] > z) { lower<SM>(T, v[k], z); wrote = true; }
+        if (lu[k] > z) { lower<SM, false>(T, u[k], z); wrote = true; }
+        if (lv[k] > z) { lower<SM, false>(T, v[k], z); wrote = true; }
     }
     return wrote;
 }
@@ -96,10 +97,10 @@ __device__ __forceinline__ bool batch_o2(const lab_t* R, lab_t* T, const lab_t (
     for (int k = 0; k < NE; ++k) {
         if (u[k] == v[k]) continue;
         const lab_t z = min(zu[k], zv[k]);
-        if (lu[k] > z) { lower<SM>(T, u[k], z); wrote = true; }
-        if (lu[k] != u[k] && zu[k] > z) { lower<SM>(T, lu[k], z); wrote = true; }
-        if (lv[k] > z) { lower<SM>(T, v[k], z); wrote = true; }
-        if (lv[k] != v[k] && zv[k] > z) { lower<SM>(T, lv[k], z); wrote = true; }
+        if (lu[k] > z) { lower<SM, false>(T, u[k], z); wrote = true; }
+        if (lu[k] != u[k] && zu[k] > z) { lower<SM, true>(T, lu[k], z); wrote = true; }
+        if (lv[k] > z) { lower<SM, false>(T, v[k], z); wrote = true; }
+        if (lv[k] != v[k] && zv[k] > z) { lower<SM, true>(T, lv[k], z); wrote = true; }
     }
     return wrote;
 }
@@ -136,25 +137,27 @@ __device__ __forceinline__ bool edge_oh(const lab_t* R, lab_t* T, lab_t w, lab_t
     const lab_t z = min(zw, zv);
     bool wrote = false;
     const int bw = nw < kChainBuf ? nw : kChainBuf;
-    for (int i = 0; i < bw; ++i)
-        if (vw[i] > z) { lower<SM>(T, cw[i], z); wrote = true; }
+    if (vw[0] > z) { lower<SM, false>(T, cw[0], z); wrote = true; }
+    for (int i = 1; i < bw; ++i)
+        if (vw[i] > z) { lower<SM, true>(T, cw[i], z); wrote = true; }
     if (nw > kChainBuf) {
         lab_t x = vw[kChainBuf - 1];
         for (int j = kChainBuf; j < nw; ++j) {
             const lab_t nxt = R[x];
-            if (nxt > z) { lower<SM>(T, x, z); wrote = true; }
+            if (nxt > z) { lower<SM, true>(T, x, z); wrote = true; }
             if (nxt == x) break;
             x = nxt;
         }
     }
     const int bv = nv < kChainBuf ? nv : kChainBuf;
-    for (int i = 0; i < bv; ++i)
-        if (vv[i] > z) { lower<SM>(T, cv[i], z); wrote = true; }
+    if (vv[0] > z) { lower<SM, false>(T, cv[0], z); wrote = true; }
+    for (int i = 1; i < bv; ++i)
+        if (vv[i] > z) { lower<SM, true>(T, cv[i], z); wrote = true; }
     if (nv > kChainBuf) {
         lab_t x = vv[kChainBuf - 1];
         for (int j = kChainBuf; j < nv; ++j) {
             const lab_t nxt = R[x];
-            if (nxt > z) { lower<SM>(T, x, z); wrote = true; }
+            if (nxt > z) { lower<SM, true>(T, x, z); wrote = true; }
             if (nxt == x) break;
             x = nxt;
         }

@@ -135,15 +135,32 @@ def _unpack_graph(g):
 
 
 LAYOUTS = {"input": 0, "src_sorted": 1, "chunk_sorted": 2}
+AUTO_SORT_MIN_ROWS = 1 << 20
 
 
-def stage_graph(ctx: _lib.Context, n: int, edges, layout: str = "input") -> None:
-    """Stage an (m, 2) edge array (numpy int32/int64 on the host, or a CUDA
-    tensor) as packed uint32 SoA in HBM, with the graph.py:73-79 range check.
-    ``layout="src_sorted"`` additionally sorts the rows by src on device
-    (cc_reorder_edges; the analogue of the reference's CSR build)."""
+def resolve_layout(layout: str, m: int) -> str:
+    """"auto": chunk-sorted staging for graphs with >= 2^20 rows (hides under
+    the host->device copy, ~2x faster sweeps), input order below that."""
+    if layout == "auto":
+        return "chunk_sorted" if m >= AUTO_SORT_MIN_ROWS else "input"
     if layout not in LAYOUTS:
         raise ValueError(f"unknown edge layout '{layout}'")
+    return layout
+
+
+def stage_graph(ctx: _lib.Context, n: int, edges, layout: str = "auto") -> None:
+    """Stage an (m, 2) edge array (numpy int32/int64 on the host, or a CUDA
+    tensor) as packed uint32 SoA in HBM, with the graph.py:73-79 range check.
+
+    ``layout`` is the staging-time edge order -- the analogue of the
+    reference building CSR at Graph construction (graph.py:80,109-122):
+    "input" keeps the caller's order, "chunk_sorted" radix-sorts every 2^23-row
+    chunk by src as it lands (overlapped with the next chunk's copy),
+    "src_sorted" sorts all rows by src afterwards, "auto" picks."""
+    m_rows = int(edges.shape[0]) if hasattr(edges, "shape") and len(edges.shape) == 2 \
+        else len(edges)
+    layout = resolve_layout(layout, m_rows)
+    ctx.set_option(_lib.CC_OPT_STAGE_LAYOUT, 2 if layout == "chunk_sorted" else 0)
     lib = ctx.lib
     if hasattr(edges, "data_ptr") and getattr(edges, "is_cuda", False):
         e = edges.reshape(-1, 2).contiguous()
@@ -166,7 +183,7 @@ def stage_graph(ctx: _lib.Context, n: int, edges, layout: str = "input") -> None
         _lib.check(lib.cc_stage_edges(ctx.handle, ctypes.c_void_p(e.ctypes.data),
                                       e.dtype.itemsize, m, n))
     ctx.n, ctx.m = n, m
-    if LAYOUTS[layout]:
+    if layout == "src_sorted":
         _lib.check(lib.cc_reorder_edges(ctx.handle, LAYOUTS[layout]))
 
 
@@ -209,7 +226,7 @@ def run_staged(ctx: _lib.Context, schedule: Schedule, *, count_changes: bool = T
 
 def run_contour(g, schedule: Schedule, threads: int = 1, seed: Optional[int] = None, *,
                 device: int = 0, count_changes: bool = True, early_check: bool = True,
-                sweep_times: bool = True, layout: str = "input",
+                sweep_times: bool = True, layout: str = "auto",
                 first_scatter: bool = True) -> tuple[LabelArray, IterationStats]:
     """Run minimum-mapping sweeps to convergence on the GPU (engine.py:248-328).
 

@@ -234,3 +234,50 @@ def test_race_tolerance_repeated_runs():
     for _ in range(10):
         labels, _ = run_contour((n, e), make_schedule("c2", atomic=False))
         assert np.array_equal(labels, exp)
+
+
+# ---------------------------------------------------------------- tuning knobs
+def test_store_modes_layouts_and_first_scatter_are_exact():
+    n, e = graphgen.rmat(14, 16, 4)
+    n2, e2 = graphgen.grid(300, 300, 0.55, 6)
+    cases = [(n, e, oracle.rem_union_find(n, e)), (n2, e2, oracle.rem_union_find(n2, e2))]
+    ctx = _lib.Context(0)
+    ctx.set_option(_lib.CC_OPT_SORT_CHUNK, 5000)  # many chunks on a small graph
+    for nn, ee, exp in cases:
+        for layout in ("input", "chunk_sorted", "src_sorted"):
+            engine.stage_graph(ctx, nn, ee, layout)
+            for atomic, modes in ((False, (0, 1, 2, 3)), (True, (1, 3))):
+                for sm in modes:
+                    ctx.set_option(_lib.CC_OPT_STORE_MODE_ATOMIC if atomic
+                                   else _lib.CC_OPT_STORE_MODE_PLAIN, sm)
+                    for fs in (False, True):
+                        labels = np.empty(nn, dtype=np.int64)
+                        _, st = engine.run_staged(ctx, make_schedule("c2", atomic=atomic),
+                                                  labels_out=labels, first_scatter=fs)
+                        assert np.array_equal(labels, exp), (layout, atomic, sm, fs)
+                        check_invariants(labels, st)
+    with pytest.raises(ValueError):
+        ctx.set_option(_lib.CC_OPT_STORE_MODE_ATOMIC, 0)  # atomic never loses a lowering
+    with pytest.raises(ValueError):
+        ctx.set_option(99, 1)
+    ctx.close()
+
+
+def test_sync_first_scatter_keeps_reference_stats(golden):
+    """The load-free sweep 1 is exactly the reference's sync sweep 1."""
+    for g in golden["graphs"][:80]:
+        e = np.asarray(g["edges"], dtype=np.int64).reshape(-1, 2)
+        exp = g["runs"]["C-2|sync|4"]
+        for fs in (False, True):
+            labels, st = run_contour((g["n"], e), make_schedule("c2", sync=True),
+                                     first_scatter=fs)
+            assert labels.tolist() == g["labels"]
+            assert (st.sweeps_executed, st.changed_per_sweep) == (exp["executed"], exp["changed"])
+
+
+def test_staged_chunk_sort_from_host_matches_device_reorder():
+    n, e = graphgen.rmat(16, 16, 2, elem_bytes=4)
+    exp = oracle.rem_union_find(n, e)
+    for layout in ("chunk_sorted", "src_sorted", "auto"):
+        labels, st = run_contour((n, e), make_schedule("c2"), layout=layout)
+        assert np.array_equal(labels, exp), layout
