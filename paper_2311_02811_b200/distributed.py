@@ -60,15 +60,27 @@ def shard_rows(total: int, rank: int, world: int, align: int = 4) -> tuple[int, 
     return lo, hi
 
 
+def nccl_allreduce_min(group=None):
+    import torch.distributed as dist
+
+    def reduce(t):
+        dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
+    return reduce
+
+
 class ShardedContour:
+    """Per-rank driver.  ``allreduce`` performs the in-place MIN exchange of
+    the (n+1)-slot label tensor (default: torch.distributed over the default
+    NCCL/gloo group)."""
+
     def __init__(self, shard, n: int, m_total: int, *, order_for=lambda k: 2, cadence: int = 1,
-                 group=None, cap=None):
+                 group=None, cap=None, allreduce=None):
         self.shard = shard
         self.n = n
         self.m_total = m_total
         self.order_for = order_for
         self.cadence = max(1, int(cadence))
-        self.group = group
+        self.allreduce = allreduce or nccl_allreduce_min(group)
         self.cap = n + 2 if cap is None else cap
 
     @classmethod
@@ -84,7 +96,6 @@ class ShardedContour:
 
     def run(self) -> int:
         """Converge; returns the number of exchange rounds."""
-        import torch.distributed as dist
         self.shard.init()
         sweep, rounds = 0, 0
         while True:
@@ -96,7 +107,7 @@ class ShardedContour:
                     raise IterationCapExceeded(f"no convergence after {self.cap} sweeps")
                 self.shard.sweep(self.order_for(sweep), first=(sweep == 1))
                 self.shard.fold(first=(k == 0))
-            dist.all_reduce(self.shard.labels, op=dist.ReduceOp.MIN, group=self.group)
+            self.allreduce(self.shard.labels)
             if int(self.shard.labels[self.n].item()) == 1:
                 break
         self.shard.compress()

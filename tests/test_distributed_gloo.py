@@ -1,0 +1,113 @@
+"""Multi-rank host logic of the edge-sharded driver (paper_2311_02811_b200/
+distributed.py) on CPU: world_size 2 over gloo, the per-rank sweep done by the
+CPU oracle behind the same shard interface the CUDA shard implements.
+Checks sharding, flag folding into the MIN all-reduce, termination and the
+final compress give the exact union-find labels."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import gen, oracle
+from paper_2311_02811_b200.distributed import ShardedContour, shard_rows
+
+
+class OracleShard:
+    """CPU stand-in for CudaShard (test-only): same interface."""
+
+    def __init__(self, n, edges):
+        self.n = n
+        self.edges = np.ascontiguousarray(edges, dtype=np.int64)
+        self.labels = torch.zeros(n + 1, dtype=torch.int32)
+        self.wrote = False
+
+    def init(self):
+        self.labels[: self.n] = torch.arange(self.n, dtype=torch.int32)
+
+    def sweep(self, order, first=False):
+        lab = self.labels[: self.n].numpy().astype(np.int64)
+        L = oracle.lib()
+        p = lab.ctypes.data_as(oracle._I64P)
+        stores = L.oc_sweep_edges(p, p, self.edges.ctypes.data, 8, 0, self.edges.shape[0], 0,
+                                  order, 1)
+        self.labels[: self.n] = torch.from_numpy(lab.astype(np.int32))
+        self.wrote = self.wrote or stores > 0
+
+    def fold(self, first):
+        f = 0 if self.wrote else 1
+        self.labels[self.n] = f if first else min(int(self.labels[self.n]), f)
+        self.wrote = False
+
+    def compress(self):
+        lab = self.labels[: self.n].numpy()
+        rounds = 0
+        while True:
+            nxt = lab[lab]
+            if np.array_equal(nxt, lab):
+                break
+            lab[:] = nxt
+            rounds += 1
+        return rounds
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, cfg, cadence, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        n, e = cfg
+        lo, hi = shard_rows(e.shape[0], rank, world)
+        runner = ShardedContour(OracleShard(n, e[lo:hi]), n, e.shape[0], cadence=cadence)
+        rounds = runner.run()
+        q.put((rank, runner.shard.labels[:n].numpy().astype(np.int64), rounds))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("graph,cadence", [("rmat", 1), ("grid", 1), ("grid", 3), ("forest", 2)])
+def test_two_rank_gloo_matches_union_find(graph, cadence):
+    if graph == "rmat":
+        cfg = gen.rmat(10, 8, 3)
+    elif graph == "grid":
+        cfg = gen.grid(40, 40, 0.55, 2)
+    else:
+        cfg = gen.forest(6, 4)
+    n, e = cfg
+    exp = oracle.rem_union_find(n, e)
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, cfg, cadence, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    results = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    rounds = {r for _, _, r in results}
+    assert len(rounds) == 1  # every rank agrees when to stop
+    for _, labels, _ in results:
+        assert np.array_equal(labels, exp)
+
+
+def test_shard_rows_cover_and_align():
+    for total in (0, 1, 7, 1000, 1 << 20):
+        for world in (1, 2, 3, 8):
+            spans = [shard_rows(total, r, world) for r in range(world)]
+            assert spans[0][0] == 0 and spans[-1][1] == total
+            for (a, b), (c, d) in zip(spans, spans[1:]):
+                assert b == c and a <= b
+            for lo, _ in spans:
+                assert lo % 4 == 0

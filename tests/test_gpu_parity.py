@@ -275,6 +275,63 @@ def test_sync_first_scatter_keeps_reference_stats(golden):
             assert (st.sweeps_executed, st.changed_per_sweep) == (exp["executed"], exp["changed"])
 
 
+@pytest.mark.parametrize("cadence", [1, 2])
+def test_sharded_driver_two_shards_on_one_gpu(cadence):
+    """The multi-GPU driver's CUDA shards, two ranks emulated as host threads
+    on one GPU (no kernel waits on another; the MIN exchange is a host
+    barrier + torch.minimum), must give the exact labels."""
+    import threading
+
+    import torch
+
+    from paper_2311_02811_b200.distributed import CudaShard, ShardedContour, shard_rows
+
+    n, e = graphgen.rmat(15, 16, 7)
+    exp = oracle.rem_union_find(n, e)
+    world = 2
+    slots = [None] * world
+    barrier = threading.Barrier(world)
+    results, errors = {}, []
+
+    def allreduce_for(r):
+        def ar(t):
+            slots[r] = t
+            torch.cuda.synchronize()
+            barrier.wait()
+            if r == 0:
+                m = torch.minimum(slots[0], slots[1])
+                for x in slots:
+                    x.copy_(m)
+                torch.cuda.synchronize()
+            barrier.wait()
+        return ar
+
+    def work(r):
+        try:
+            torch.cuda.set_device(0)
+            ctx = _lib.Context(0)
+            lo, hi = shard_rows(e.shape[0], r, world)
+            engine.stage_graph(ctx, n, e[lo:hi], "input")
+            shard = CudaShard(ctx, n)
+            runner = ShardedContour(shard, n, e.shape[0], cadence=cadence,
+                                    allreduce=allreduce_for(r))
+            runner.run()
+            torch.cuda.synchronize()
+            results[r] = shard.labels[:n].cpu().numpy().astype(np.int64)
+        except Exception as exc:  # pragma: no cover - surfaced below
+            errors.append(exc)
+            barrier.abort()
+
+    threads = [threading.Thread(target=work, args=(r,)) for r in range(world)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join(timeout=300)
+    assert not errors, errors
+    for r in range(world):
+        assert np.array_equal(results[r], exp)
+
+
 def test_staged_chunk_sort_from_host_matches_device_reorder():
     n, e = graphgen.rmat(16, 16, 2, elem_bytes=4)
     exp = oracle.rem_union_find(n, e)
