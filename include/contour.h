@@ -51,8 +51,12 @@ typedef struct cc_schedule {
 #define CC_RUN_EARLY_CHECK 1   /* early_convergence_check after each changing sweep (engine.py:318-320) */
 #define CC_RUN_COUNT_CHANGES 2 /* exact changed_per_sweep by label diff (engine.py:293,309) */
 #define CC_RUN_SWEEP_TIMES 4   /* per-sweep device times (IterationStats.sweep_seconds) */
-#define CC_RUN_NO_FIRST_SCATTER 8 /* run sweep 1 with the gathering kernel instead of the
-                                     load-free identity scatter (see cc_sweep) */
+#define CC_RUN_FIRST_SCATTER 8 /* run sweep 1 as the load-free identity scatter (see cc_sweep) */
+#define CC_RUN_HOST_LOOP 16    /* drive sweeps from the host even when the device-side
+                                  loop applies.  Without COUNT_CHANGES / EARLY_CHECK /
+                                  FIRST_SCATTER and in async mode, cc_run otherwise runs the
+                                  whole convergence loop as ONE CUDA-graph launch (a
+                                  conditional WHILE node around sweep + control kernels). */
 
 /* Output of cc_run, the IterationStats contract (engine.py:77-90). */
 typedef struct cc_stats {

@@ -15,7 +15,8 @@ _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_PKG, "lib", "libcontour.so")
 
 CC_OK, CC_EINVAL, CC_ECAP, CC_ECUDA = 0, 1, 2, 3
-CC_RUN_EARLY_CHECK, CC_RUN_COUNT_CHANGES, CC_RUN_SWEEP_TIMES, CC_RUN_NO_FIRST_SCATTER = 1, 2, 4, 8
+CC_RUN_EARLY_CHECK, CC_RUN_COUNT_CHANGES, CC_RUN_SWEEP_TIMES = 1, 2, 4
+CC_RUN_FIRST_SCATTER, CC_RUN_HOST_LOOP = 8, 16
 
 CC_OPT_STORE_MODE_PLAIN, CC_OPT_STORE_MODE_ATOMIC, CC_OPT_SORT_CHUNK = 1, 2, 3
 CC_OPT_STAGE_LAYOUT = 4

@@ -193,6 +193,73 @@ __global__ void k_single_edge(const lab_t* R, lab_t* T, lab_t w, lab_t v, int or
     }
 }
 
+// ---- device-side convergence loop (CUDA graph with a conditional WHILE node)
+// Body per iteration: order-guarded k_sweep launches -> k_loop_control,
+// which reads and clears the ballot/OR flag, records (wrote, globaltimer),
+// and sets the WHILE condition.  No host round trip between sweeps.
+struct LoopState {
+    long long sweep;      // sweeps completed
+    int order;            // operator order of the next sweep
+    int converged;        // last sweep lowered nothing
+    int capped;           // sweep cap reached while still changing
+    int pad;
+    unsigned long long t0;
+};
+struct SweepRec {
+    int wrote;
+    int pad;
+    unsigned long long t;
+};
+constexpr int kMaxRec = 4096;
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+__device__ __forceinline__ int order_for_dev(const cc_schedule& s, long long sweep) {
+    switch (s.variant) {  // engine.py:61-74
+        case CC_VAR_C2:
+        case CC_VAR_CSYN: return 2;
+        case CC_VAR_C1: return 1;
+        case CC_VAR_CM: return s.high_order;
+        case CC_VAR_C11MM: return sweep <= s.warmup ? 1 : s.high_order;
+        default: return (sweep % 2 == 1) ? 1 : s.high_order;
+    }
+}
+
+__global__ void k_loop_init(LoopState* st, int* flags, cc_schedule s) {
+    st->sweep = 0;
+    st->order = order_for_dev(s, 1);
+    st->converged = 0;
+    st->capped = 0;
+    flags[kFlagWrote] = 0;
+    flags[kFlagCompress] = 0;
+    st->t0 = globaltimer();
+}
+
+__global__ void k_loop_control(LoopState* st, SweepRec* rec, int* flags, cc_schedule s,
+                               long long cap, cudaGraphConditionalHandle h) {
+    const int wrote = flags[kFlagWrote];
+    flags[kFlagWrote] = 0;
+    const long long k = ++st->sweep;
+    if (k <= kMaxRec) {
+        rec[k - 1].wrote = wrote;
+        rec[k - 1].t = globaltimer();
+    }
+    if (!wrote) {
+        st->converged = 1;
+        cudaGraphSetConditional(h, 0);
+    } else if (k >= cap) {
+        st->capped = 1;
+        cudaGraphSetConditional(h, 0);
+    } else {
+        st->order = order_for_dev(s, k + 1);
+        cudaGraphSetConditional(h, 1);
+    }
+}
+
 // RMAT rows [lo, hi) of the symmetrised list (rows >= M are (v,u) of row-M).
 __global__ void k_gen_rmat(ccgen::RmatParams rp, ccgen::Perm pm, int permute, int64_t M,
                            int symmetrize, int64_t lo, int64_t hi, lab_t* src, lab_t* dst) {
@@ -245,6 +312,20 @@ struct cc_ctx {
     void* stage_buf[2] = {nullptr, nullptr};  // cached H2D staging buffers
     size_t stage_buf_bytes = 0;
     cudaEvent_t copied[2] = {nullptr, nullptr}, freed[2] = {nullptr, nullptr};
+    // graph-captured convergence loop (built lazily, rebuilt when its key changes)
+    cudaStream_t cap_stream = nullptr, body_stream = nullptr;
+    cudaGraph_t loop_graph = nullptr;
+    cudaGraphExec_t loop_exec = nullptr;
+    LoopState* dstate = nullptr;
+    SweepRec* drec = nullptr;
+    LoopState* hstate = nullptr;  // pinned
+    SweepRec* hrec = nullptr;     // pinned
+    struct {
+        const void *src, *dst, *labels;
+        int64_t m, n, cap;
+        cc_schedule s;
+        int sm;
+    } loop_key = {};
     std::mutex mu;
 };
 
@@ -271,8 +352,15 @@ int grid_for(const cc_ctx* c, int64_t work, int per_sm = 8) {
     return (int)b;
 }
 
+// Launch context of one sweep: the stream, and for graph capture the
+// device word holding the order (nullptr: use the host value).
+struct SweepLaunch {
+    cudaStream_t stream;
+    const int* d_order;
+};
+
 template <int OK, int SM, int NV>
-int launch_sweep_t(cc_ctx* c, const lab_t* R, lab_t* T, int order) {
+int launch_sweep_t(cc_ctx* c, const lab_t* R, lab_t* T, int order, SweepLaunch sl) {
     static int occ = 0;
     if (occ == 0) {
         int o = 0;
@@ -281,29 +369,31 @@ int launch_sweep_t(cc_ctx* c, const lab_t* R, lab_t* T, int order) {
     }
     const int64_t units = (c->m + 4 * NV - 1) / (4 * NV);
     const int blocks = grid_for(c, units, occ);
-    cck::k_sweep<OK, SM, NV><<<blocks, kThreads, 0, c->stream>>>(c->src, c->dst, c->m, R, T,
-                                                                  order, c->dflags + kFlagWrote);
+    cck::k_sweep<OK, SM, NV><<<blocks, kThreads, 0, sl.stream>>>(
+        c->src, c->dst, c->m, R, T, order, c->dflags + kFlagWrote, sl.d_order);
     CUDA_TRY(cudaGetLastError());
     return CC_OK;
 }
 
 template <int OK, int NV>
-int launch_store_mode(cc_ctx* c, const lab_t* R, lab_t* T, int order, int sm) {
+int launch_store_mode(cc_ctx* c, const lab_t* R, lab_t* T, int order, int sm, SweepLaunch sl) {
     switch (sm) {
-        case cck::kStorePlain: return launch_sweep_t<OK, cck::kStorePlain, NV>(c, R, T, order);
-        case cck::kStoreRed: return launch_sweep_t<OK, cck::kStoreRed, NV>(c, R, T, order);
+        case cck::kStorePlain:
+            return launch_sweep_t<OK, cck::kStorePlain, NV>(c, R, T, order, sl);
+        case cck::kStoreRed: return launch_sweep_t<OK, cck::kStoreRed, NV>(c, R, T, order, sl);
         case cck::kStoreCheckPlain:
-            return launch_sweep_t<OK, cck::kStoreCheckPlain, NV>(c, R, T, order);
-        default: return launch_sweep_t<OK, cck::kStoreCheckRed, NV>(c, R, T, order);
+            return launch_sweep_t<OK, cck::kStoreCheckPlain, NV>(c, R, T, order, sl);
+        default: return launch_sweep_t<OK, cck::kStoreCheckRed, NV>(c, R, T, order, sl);
     }
 }
 
 // Order-specialised sweep: order 1 and 2 get unrolled batch kernels, any
 // other order the buffered chain walker.
 int launch_order(cc_ctx* c, const lab_t* R, lab_t* T, int order, int sm) {
-    if (order == 1) return launch_store_mode<1, 2>(c, R, T, order, sm);
-    if (order == 2) return launch_store_mode<2, 2>(c, R, T, order, sm);
-    return launch_store_mode<0, 1>(c, R, T, order, sm);
+    const SweepLaunch sl{c->stream, nullptr};
+    if (order == 1) return launch_store_mode<1, 2>(c, R, T, order, sm, sl);
+    if (order == 2) return launch_store_mode<2, 2>(c, R, T, order, sm, sl);
+    return launch_store_mode<0, 1>(c, R, T, order, sm, sl);
 }
 
 int ensure_aux(cc_ctx* c, bool need_shadow, bool need_before) {
@@ -472,6 +562,134 @@ int compress(cc_ctx* c, int* rounds) {
     return CC_OK;
 }
 
+// Capture one order-guarded sweep launch per order kind the schedule can
+// use (order 1, order 2, generic); at run time only the launch matching the
+// device-side order does any work.
+int launch_guarded(cc_ctx* c, const cc_schedule* s, int sm, cudaStream_t st) {
+    bool need1 = false, need2 = false, needh = false;
+    auto mark = [&](int order) {
+        if (order == 1) need1 = true;
+        else if (order == 2) need2 = true;
+        else needh = true;
+    };
+    switch (s->variant) {
+        case CC_VAR_C2:
+        case CC_VAR_CSYN: mark(2); break;
+        case CC_VAR_C1: mark(1); break;
+        case CC_VAR_CM: mark(s->high_order); break;
+        default: mark(1); mark(s->high_order); break;
+    }
+    const SweepLaunch sl{st, &c->dstate->order};
+    lab_t* L = c->labels;
+    if (need2) CC_TRY((launch_store_mode<2, 2>(c, L, L, 2, sm, sl)));
+    if (need1) CC_TRY((launch_store_mode<1, 2>(c, L, L, 1, sm, sl)));
+    if (needh) CC_TRY((launch_store_mode<0, 1>(c, L, L, s->high_order, sm, sl)));
+    return CC_OK;
+}
+
+bool same_schedule(const cc_schedule& a, const cc_schedule& b) {
+    return a.variant == b.variant && a.high_order == b.high_order && a.warmup == b.warmup &&
+           a.sync == b.sync && a.atomic == b.atomic;
+}
+
+// Capture iota -> loop_init -> WHILE{ guarded sweeps -> loop_control } -> compress
+// into one executable graph.
+int build_loop(cc_ctx* c, const cc_schedule* s, int64_t cap, int sm) {
+    auto& k = c->loop_key;
+    if (c->loop_exec && k.src == c->src && k.dst == c->dst && k.labels == c->labels &&
+        k.m == c->m && k.n == c->n && k.cap == cap && same_schedule(k.s, *s) && k.sm == sm)
+        return CC_OK;
+    if (c->loop_exec) cudaGraphExecDestroy(c->loop_exec);
+    if (c->loop_graph) cudaGraphDestroy(c->loop_graph);
+    c->loop_exec = nullptr;
+    c->loop_graph = nullptr;
+    if (!c->dstate) {
+        CUDA_TRY(cudaMalloc(&c->dstate, sizeof(LoopState)));
+        CUDA_TRY(cudaMalloc(&c->drec, sizeof(SweepRec) * kMaxRec));
+        CUDA_TRY(cudaHostAlloc(&c->hstate, sizeof(LoopState), cudaHostAllocDefault));
+        CUDA_TRY(cudaHostAlloc(&c->hrec, sizeof(SweepRec) * kMaxRec, cudaHostAllocDefault));
+    }
+    cudaStream_t cs = c->cap_stream;
+    CUDA_TRY(cudaStreamBeginCapture(cs, cudaStreamCaptureModeRelaxed));
+    k_iota<<<grid_for(c, c->n), kThreads, 0, cs>>>(c->labels, c->n);
+    k_loop_init<<<1, 1, 0, cs>>>(c->dstate, c->dflags, *s);
+    cudaStreamCaptureStatus status;
+    cudaGraph_t g = nullptr;
+    const cudaGraphNode_t* deps = nullptr;
+    size_t nd = 0;
+    CUDA_TRY(cudaStreamGetCaptureInfo(cs, &status, nullptr, &g, &deps, &nd));
+    cudaGraphConditionalHandle h;
+    CUDA_TRY(cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault));
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = h;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t cn;
+    CUDA_TRY(cudaGraphAddNode(&cn, g, deps, nd, &cp));
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    CUDA_TRY(cudaStreamUpdateCaptureDependencies(cs, &cn, 1, cudaStreamSetCaptureDependencies));
+    CUDA_TRY(cudaStreamBeginCaptureToGraph(c->body_stream, body, nullptr, nullptr, 0,
+                                           cudaStreamCaptureModeRelaxed));
+    CC_TRY(launch_guarded(c, s, sm, c->body_stream));
+    k_loop_control<<<1, 1, 0, c->body_stream>>>(c->dstate, c->drec, c->dflags, *s, cap, h);
+    CUDA_TRY(cudaGetLastError());
+    cudaGraph_t body_out = nullptr;
+    CUDA_TRY(cudaStreamEndCapture(c->body_stream, &body_out));
+    k_compress<<<grid_for(c, c->n), kThreads, 0, cs>>>(c->labels, c->n, c->dflags);
+    CUDA_TRY(cudaStreamEndCapture(cs, &c->loop_graph));
+    CUDA_TRY(cudaGraphInstantiate(&c->loop_exec, c->loop_graph, 0));
+    k = {c->src, c->dst, c->labels, c->m, c->n, cap, *s, sm};
+    return CC_OK;
+}
+
+int copy_out(cc_ctx* c, void* out, int eb);
+
+// The fast path of cc_run: async sweeps, no per-sweep counting or early
+// check -- the whole convergence loop is one graph launch.
+int run_graph(cc_ctx* c, const cc_schedule* s, int64_t cap, void* labels_out, int out_eb,
+              cc_stats* st) {
+    const int sm = s->atomic ? c->store_mode_atomic : c->store_mode_plain;
+    CC_TRY(build_loop(c, s, cap, sm));
+    CUDA_TRY(cudaEventRecord(c->evs, c->stream));
+    CUDA_TRY(cudaGraphLaunch(c->loop_exec, c->stream));
+    CUDA_TRY(cudaEventRecord(c->eve, c->stream));
+    CUDA_TRY(cudaMemcpyAsync(c->hstate, c->dstate, sizeof(LoopState), cudaMemcpyDeviceToHost,
+                             c->stream));
+    CC_TRY(read_flags(c));
+    const long long k = c->hstate->sweep;
+    if (c->hstate->capped)
+        return fail(CC_ECAP, "no convergence after %lld sweeps on n=%lld, m=%lld",
+                    (long long)cap, (long long)c->n, (long long)c->m);
+    const long long nrec = std::min<long long>(k, kMaxRec);
+    if (st && (st->changed_per_sweep || st->sweep_seconds) && nrec > 0) {
+        CUDA_TRY(cudaMemcpyAsync(c->hrec, c->drec, sizeof(SweepRec) * nrec,
+                                 cudaMemcpyDeviceToHost, c->stream));
+        CUDA_TRY(cudaStreamSynchronize(c->stream));
+        unsigned long long prev = c->hstate->t0;
+        for (long long i = 0; i < nrec && i < st->capacity; ++i) {
+            if (st->changed_per_sweep) st->changed_per_sweep[i] = c->hrec[i].wrote ? -1 : 0;
+            if (st->sweep_seconds) st->sweep_seconds[i] = (c->hrec[i].t - prev) * 1e-9;
+            prev = c->hrec[i].t;
+        }
+    }
+    int rounds = 0;
+    if (c->hflags[kFlagCompress]) {  // cannot happen after a no-write sweep; be safe
+        CC_TRY(compress(c, &rounds));
+        ++rounds;
+    }
+    float total_ms = 0.f;
+    cudaEventElapsedTime(&total_ms, c->evs, c->eve);
+    if (st) {
+        st->sweeps_executed = k;
+        st->sweeps_until_stable = k - 1;
+        st->converged_by = 0;
+        st->compress_rounds = rounds;
+        st->converge_seconds = total_ms * 1e-3;
+    }
+    return copy_out(c, labels_out, out_eb);
+}
+
 int copy_out(cc_ctx* c, void* out, int eb) {
     if (c->n == 0 || !out) return CC_OK;
     if (eb == 4) {
@@ -622,6 +840,8 @@ int cc_create(int device, void* stream, cc_ctx** out) {
         CUDA_TRY(cudaEventCreateWithFlags(&c->copied[b], cudaEventDisableTiming));
         CUDA_TRY(cudaEventCreateWithFlags(&c->freed[b], cudaEventDisableTiming));
     }
+    CUDA_TRY(cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
+    CUDA_TRY(cudaStreamCreateWithFlags(&c->body_stream, cudaStreamNonBlocking));
     *out = c;
     return CC_OK;
 }
@@ -650,6 +870,14 @@ void cc_destroy(cc_ctx* c) {
     cudaFree(c->sort_ks);
     cudaFree(c->sort_vs);
     cudaFree(c->sort_tmp);
+    if (c->loop_exec) cudaGraphExecDestroy(c->loop_exec);
+    if (c->loop_graph) cudaGraphDestroy(c->loop_graph);
+    cudaFree(c->dstate);
+    cudaFree(c->drec);
+    cudaFreeHost(c->hstate);
+    cudaFreeHost(c->hrec);
+    cudaStreamDestroy(c->cap_stream);
+    cudaStreamDestroy(c->body_stream);
     cudaStreamDestroy(c->copy_stream);
     if (c->own_stream) cudaStreamDestroy(c->stream);
     delete c;
@@ -775,6 +1003,9 @@ int cc_run(cc_ctx* c, const cc_schedule* s, int flags, int64_t cap, void* labels
     const bool count = (flags & CC_RUN_COUNT_CHANGES) != 0;
     const bool check = (flags & CC_RUN_EARLY_CHECK) != 0;
     const bool times = (flags & CC_RUN_SWEEP_TIMES) != 0;
+    const bool first_scatter = (flags & CC_RUN_FIRST_SCATTER) != 0;
+    if (!sync && !count && !check && !first_scatter && !(flags & CC_RUN_HOST_LOOP) && c->n > 0)
+        return run_graph(c, s, cap, labels_out, out_eb, st);
     CUDA_TRY(cudaEventRecord(c->evs, c->stream));
     CC_TRY(enqueue_init(c, sync));
     int64_t sweep = 0, until_stable = 0;
@@ -786,8 +1017,7 @@ int cc_run(cc_ctx* c, const cc_schedule* s, int flags, int64_t cap, void* labels
                         (long long)cap, (long long)c->n, (long long)c->m);
         const int order = order_for(s, sweep);
         if (times) CUDA_TRY(cudaEventRecord(c->ev0, c->stream));
-        CC_TRY(enqueue_sweep(c, order, sync, s->atomic, count,
-                             sweep == 1 && !(flags & CC_RUN_NO_FIRST_SCATTER)));
+        CC_TRY(enqueue_sweep(c, order, sync, s->atomic, count, sweep == 1 && first_scatter));
         if (times) CUDA_TRY(cudaEventRecord(c->ev1, c->stream));
         CC_TRY(read_flags(c));
         const bool wrote = c->hflags[kFlagWrote] != 0;

@@ -180,11 +180,19 @@ __device__ __forceinline__ bool batch(const lab_t* R, lab_t* T, const lab_t (&u)
 // OK: 1, 2 or 0 (generic order).  Sync sweeps pass R = labels, T = shadow
 // with SM = kStoreRed; async sweeps R == T (in place).  SM: store mode.  NV: uint4 vectors per
 // array per thread per iteration (4*NV edges in flight per thread).
+// d_order != nullptr (graph-captured loop): the order of this sweep is read
+// from device memory and the launch is a no-op unless it matches OK, so a
+// captured body holds one launch per order kind the schedule can use.
 template <int OK, int SM, int NV>
 __global__ void __launch_bounds__(kThreads) k_sweep(const lab_t* __restrict__ src,
                                                     const lab_t* __restrict__ dst, int64_t m,
                                                     const lab_t* R, lab_t* T, int order,
-                                                    int* __restrict__ flag) {
+                                                    int* __restrict__ flag,
+                                                    const int* __restrict__ d_order) {
+    if (d_order) {
+        order = *d_order;
+        if ((OK == 1) != (order == 1) || (OK == 2) != (order == 2)) return;
+    }
     const int64_t nvec = m >> 2;
     const uint4* __restrict__ s4 = reinterpret_cast<const uint4*>(src);
     const uint4* __restrict__ d4 = reinterpret_cast<const uint4*>(dst);

@@ -189,8 +189,13 @@ def stage_graph(ctx: _lib.Context, n: int, edges, layout: str = "auto") -> None:
 
 def run_staged(ctx: _lib.Context, schedule: Schedule, *, count_changes: bool = True,
                early_check: bool = True, sweep_times: bool = True, cap: Optional[int] = None,
-               labels_out: Optional[np.ndarray] = None, first_scatter: bool = True):
-    """cc_run on already-staged edges; returns (labels or None, IterationStats)."""
+               labels_out: Optional[np.ndarray] = None, first_scatter: bool = False,
+               host_loop: bool = False):
+    """cc_run on already-staged edges; returns (labels or None, IterationStats).
+
+    Async runs without ``count_changes``/``early_check``/``first_scatter``
+    execute the whole convergence loop as one CUDA-graph launch unless
+    ``host_loop`` forces the per-sweep host loop."""
     n = ctx.n
     cap = n + 2 if cap is None else int(cap)  # engine.py:275
     capacity = max(1, min(cap, 1 << 16))
@@ -203,7 +208,8 @@ def run_staged(ctx: _lib.Context, schedule: Schedule, *, count_changes: bool = T
     flags = ((_lib.CC_RUN_EARLY_CHECK if early_check else 0)
              | (_lib.CC_RUN_COUNT_CHANGES if count_changes else 0)
              | (_lib.CC_RUN_SWEEP_TIMES if sweep_times else 0)
-             | (0 if first_scatter else _lib.CC_RUN_NO_FIRST_SCATTER))
+             | (_lib.CC_RUN_FIRST_SCATTER if first_scatter else 0)
+             | (_lib.CC_RUN_HOST_LOOP if host_loop else 0))
     sched = _cc_schedule(schedule)
     out_ptr, eb = None, 8
     if labels_out is not None:
@@ -227,7 +233,8 @@ def run_staged(ctx: _lib.Context, schedule: Schedule, *, count_changes: bool = T
 def run_contour(g, schedule: Schedule, threads: int = 1, seed: Optional[int] = None, *,
                 device: int = 0, count_changes: bool = True, early_check: bool = True,
                 sweep_times: bool = True, layout: str = "auto",
-                first_scatter: bool = True) -> tuple[LabelArray, IterationStats]:
+                first_scatter: bool = False,
+                host_loop: bool = False) -> tuple[LabelArray, IterationStats]:
     """Run minimum-mapping sweeps to convergence on the GPU (engine.py:248-328).
 
     ``g`` is anything with ``.n`` and ``.edges`` ((m, 2) int32/int64 pairs,
@@ -246,7 +253,8 @@ def run_contour(g, schedule: Schedule, threads: int = 1, seed: Optional[int] = N
     stage_graph(ctx, n, edges, layout)
     labels = np.empty(n, dtype=np.int64)
     _, stats = run_staged(ctx, schedule, count_changes=count_changes, early_check=early_check,
-                          sweep_times=sweep_times, labels_out=labels, first_scatter=first_scatter)
+                          sweep_times=sweep_times, labels_out=labels, first_scatter=first_scatter,
+                          host_loop=host_loop)
     return labels, stats
 
 

@@ -332,6 +332,51 @@ def test_sharded_driver_two_shards_on_one_gpu(cadence):
         assert np.array_equal(results[r], exp)
 
 
+def test_graph_loop_matches_host_loop_all_variants(golden):
+    """The CUDA-graph convergence loop (device-side WHILE) against the host
+    loop and the oracle, for every variant incl. per-sweep order changes."""
+    cases = [(g["n"], np.asarray(g["edges"], dtype=np.int64).reshape(-1, 2), g["labels"])
+             for g in golden["graphs"][::3]]
+    n, e = graphgen.grid(200, 200, 0.55, 8)
+    cases.append((n, e, oracle.rem_union_find(n, e).tolist()))
+    n, e = graphgen.rmat(13, 16, 8)
+    cases.append((n, e, oracle.rem_union_find(n, e).tolist()))
+    for n, e, exp in cases:
+        for variant in ("C-1", "C-2", "C-m", "C-11mm", "C-1m1m"):
+            for atomic in (False, True):
+                sched = make_schedule(variant, 8, sync=False, atomic=atomic)
+                lg, sg = run_contour((n, e), sched, count_changes=False, early_check=False)
+                lh, sh = run_contour((n, e), sched, count_changes=False, early_check=False,
+                                     host_loop=True)
+                assert lg.tolist() == exp and lh.tolist() == exp, (variant, atomic)
+                for st in (sg, sh):
+                    check_invariants(lg, st)
+                    assert st.converged_by == "change-flag"
+                    assert st.changed_per_sweep[-1] == 0
+                    assert all(c == -1 for c in st.changed_per_sweep[:-1])
+
+
+def test_graph_loop_cap_and_rebuild():
+    ctx = _lib.Context(0)
+    e = np.array([[5, 4], [4, 3], [3, 2], [2, 1], [1, 0]])
+    engine.stage_graph(ctx, 6, e)
+    with pytest.raises(IterationCapExceeded):
+        engine.run_staged(ctx, make_schedule("c1"), count_changes=False, early_check=False,
+                          cap=1)
+    labels = np.empty(6, dtype=np.int64)
+    engine.run_staged(ctx, make_schedule("c1"), count_changes=False, early_check=False,
+                      labels_out=labels)
+    assert labels.tolist() == [0] * 6
+    # restaging a different graph must rebuild the captured loop
+    n, e2 = graphgen.rmat(11, 8, 2)
+    engine.stage_graph(ctx, n, e2)
+    labels = np.empty(n, dtype=np.int64)
+    engine.run_staged(ctx, make_schedule("c2"), count_changes=False, early_check=False,
+                      labels_out=labels)
+    assert np.array_equal(labels, oracle.rem_union_find(n, e2))
+    ctx.close()
+
+
 def test_staged_chunk_sort_from_host_matches_device_reorder():
     n, e = graphgen.rmat(16, 16, 2, elem_bytes=4)
     exp = oracle.rem_union_find(n, e)
