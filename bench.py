@@ -58,6 +58,10 @@ def parse():
                         "sorted by src on device while the next chunk is copied in)")
     p.add_argument("--first-scatter", action="store_true",
                    help="run sweep 1 as the load-free identity scatter")
+    p.add_argument("--host-loop", action="store_true",
+                   help="drive sweeps from the host instead of the CUDA-graph WHILE loop "
+                        "(same kernels; ncu cannot see kernels inside conditional nodes)")
+    p.add_argument("--no-e2e", action="store_true", help="skip the end-to-end leg")
     p.add_argument("--atomic", type=int, default=1,
                    help="Schedule.atomic (the reference default is True)")
     p.add_argument("--store-mode", type=int, default=None,
@@ -235,7 +239,10 @@ def run_single(args, device):
     from paper_2311_02811_b200.engine import make_schedule
 
     spec = config_spec(args.config)
-    stream = torch.cuda.current_stream()
+    # one dedicated stream: the library launches on it and the CUDA events
+    # that time the step are recorded on it
+    stream = torch.cuda.Stream(device)
+    torch.cuda.set_stream(stream)
     ctx = _lib.Context(device, stream.cuda_stream)
     if args.store_mode is not None:
         ctx.set_option(_lib.CC_OPT_STORE_MODE_ATOMIC if args.atomic else
@@ -252,7 +259,7 @@ def run_single(args, device):
         m = host_edges.shape[0]
     sched = make_schedule("c2", atomic=bool(args.atomic))
     kw = dict(count_changes=False, early_check=args.early_check,
-              first_scatter=args.first_scatter)
+              first_scatter=args.first_scatter, host_loop=args.host_loop)
 
     for _ in range(args.warmup):
         engine.run_staged(ctx, sched, sweep_times=False, **kw)
@@ -281,33 +288,43 @@ def run_single(args, device):
     b_sweep = 8 * m + 4 * n  # edge stream + one label-array read
     achieved = b_sweep / t_sweep / 1e9
     peak, peak_src = peak_hbm()
-    traffic = load_traffic().get(args.config)
-    launches = sum(1 + s.sweeps_executed + 1 for s in stats)  # iota + sweeps + compress
+    traffic = (load_traffic().get(args.config) or {}).get("dram_bytes_per_launch")
+    if args.host_loop:  # iota + sweeps + compress
+        launches = sum(1 + s.sweeps_executed + 1 for s in stats)
+    else:  # iota + loop_init + (sweep + control) per sweep + compress, all in one graph
+        launches = sum(3 + 2 * s.sweeps_executed for s in stats)
 
     # ---- e2e through the C-ABI with HOST buffers (pinned), H2D + D2H timed
-    if host_edges is None:
+    need_host = not (args.no_e2e and args.no_cpu_baseline)
+    if need_host and host_edges is None:
         host_edges_t = torch.empty((m, 2), dtype=torch.int32, pin_memory=True)
         graphgen.rmat(spec["scale"], spec.get("edgefactor", 16), args.seed, elem_bytes=4,
                       out=host_edges_t.numpy())
         host_edges = host_edges_t.numpy()
-    else:
+    elif need_host:
         t = torch.empty((m, 2), dtype=torch.int32, pin_memory=True)
         t.numpy()[:] = host_edges
         host_edges = t.numpy()
-    labels_t = torch.empty(n, dtype=torch.int64, pin_memory=True)
-    labels_host = labels_t.numpy()
-    e2e_times = []
-    for i in range(args.warmup + args.steps):
-        torch.cuda.synchronize()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        engine.stage_graph(ctx, n, host_edges, args.layout)
-        engine.run_staged(ctx, sched, sweep_times=False, labels_out=labels_host, **kw)
-        b.record(stream)
-        torch.cuda.synchronize()
-        if i >= args.warmup:
-            e2e_times.append(a.elapsed_time(b) / 1e3)
-    e2e_s = sum(e2e_times) / len(e2e_times)
+    e2e = None
+    if not args.no_e2e:
+        labels_t = torch.empty(n, dtype=torch.int64, pin_memory=True)
+        labels_host = labels_t.numpy()
+        e2e_times = []
+        for i in range(args.warmup + args.steps):
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            engine.stage_graph(ctx, n, host_edges, args.layout)
+            engine.run_staged(ctx, sched, sweep_times=False, labels_out=labels_host, **kw)
+            b.record(stream)
+            torch.cuda.synchronize()
+            if i >= args.warmup:
+                e2e_times.append(a.elapsed_time(b) / 1e3)
+        e2e_s = sum(e2e_times) / len(e2e_times)
+        e2e = {"value": m / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(host_edges.nbytes),
+               "d2h_bytes_per_step": int(labels_host.nbytes), "seconds_per_step": e2e_s,
+               "path": "cc_stage_edges(pinned int32 (m,2), chunk-sorted while copying) + "
+                       "cc_run(labels -> pinned int64)"}
 
     # ---- CPU baseline: the reference path (oracle port) on the host cores
     cpu = None
@@ -338,13 +355,11 @@ def run_single(args, device):
         "reference_sweeps": ref_sweeps,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "kernel": "k_sweep<2,false,2> (order-2 async sweep)",
+                     "kernel": "cck::k_sweep<2, 3, 2> (order-2 async sweep, check+red stores)",
                      "bytes_per_launch": b_sweep, "avg_launch_s": t_sweep,
                      "peak_source": peak_src},
         "cpu_baseline": cpu,
-        "e2e": {"value": m / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(host_edges.nbytes),
-                "d2h_bytes_per_step": int(labels_host.nbytes), "seconds_per_step": e2e_s,
-                "path": "cc_stage_edges(pinned int32 (m,2)) + cc_run(labels -> pinned int64)"},
+        "e2e": e2e,
         "gpu_launches": launches,
         "clocks": clk,
     }

@@ -654,18 +654,26 @@ int run_graph(cc_ctx* c, const cc_schedule* s, int64_t cap, void* labels_out, in
     CUDA_TRY(cudaEventRecord(c->evs, c->stream));
     CUDA_TRY(cudaGraphLaunch(c->loop_exec, c->stream));
     CUDA_TRY(cudaEventRecord(c->eve, c->stream));
+    // one synchronisation: state, flags and the first records come back together
+    constexpr int kEagerRec = 64;
+    const bool want_rec = st && (st->changed_per_sweep || st->sweep_seconds);
     CUDA_TRY(cudaMemcpyAsync(c->hstate, c->dstate, sizeof(LoopState), cudaMemcpyDeviceToHost,
                              c->stream));
+    if (want_rec)
+        CUDA_TRY(cudaMemcpyAsync(c->hrec, c->drec, sizeof(SweepRec) * kEagerRec,
+                                 cudaMemcpyDeviceToHost, c->stream));
     CC_TRY(read_flags(c));
     const long long k = c->hstate->sweep;
     if (c->hstate->capped)
         return fail(CC_ECAP, "no convergence after %lld sweeps on n=%lld, m=%lld",
                     (long long)cap, (long long)c->n, (long long)c->m);
     const long long nrec = std::min<long long>(k, kMaxRec);
-    if (st && (st->changed_per_sweep || st->sweep_seconds) && nrec > 0) {
-        CUDA_TRY(cudaMemcpyAsync(c->hrec, c->drec, sizeof(SweepRec) * nrec,
-                                 cudaMemcpyDeviceToHost, c->stream));
-        CUDA_TRY(cudaStreamSynchronize(c->stream));
+    if (want_rec && nrec > 0) {
+        if (nrec > kEagerRec) {
+            CUDA_TRY(cudaMemcpyAsync(c->hrec, c->drec, sizeof(SweepRec) * nrec,
+                                     cudaMemcpyDeviceToHost, c->stream));
+            CUDA_TRY(cudaStreamSynchronize(c->stream));
+        }
         unsigned long long prev = c->hstate->t0;
         for (long long i = 0; i < nrec && i < st->capacity; ++i) {
             if (st->changed_per_sweep) st->changed_per_sweep[i] = c->hrec[i].wrote ? -1 : 0;

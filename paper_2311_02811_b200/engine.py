@@ -198,7 +198,7 @@ def run_staged(ctx: _lib.Context, schedule: Schedule, *, count_changes: bool = T
     ``host_loop`` forces the per-sweep host loop."""
     n = ctx.n
     cap = n + 2 if cap is None else int(cap)  # engine.py:275
-    capacity = max(1, min(cap, 1 << 16))
+    capacity = max(1, min(cap, 1 << 12 if not count_changes else 1 << 16))
     changed = np.zeros(capacity, dtype=np.int64)
     secs = np.zeros(capacity, dtype=np.float64)
     st = _lib.CCStats()
