@@ -53,7 +53,7 @@ def parse():
                    help="run the reference early check after each changing sweep")
     p.add_argument("--seed", type=int, default=1)
     p.add_argument("--layout", default="chunk_sorted",
-                   choices=["input", "src_sorted", "chunk_sorted"],
+                   choices=["input", "src_sorted", "chunk_sorted", "dst_bucketed"],
                    help="staging-time edge layout (chunk_sorted: each 2^23-row chunk radix-"
                         "sorted by src on device while the next chunk is copied in)")
     p.add_argument("--first-scatter", action="store_true",

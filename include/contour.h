@@ -115,7 +115,10 @@ int cc_sweep(cc_ctx* ctx, int order, int sync, int atomic, int first, int* wrote
  * Graph construction, graph.py:80,109-122): mode 0 keeps the input order,
  * mode 1 stably sorts all rows by src (radix sort on device, m < 2^31),
  * mode 2 sorts each consecutive chunk of CC_OPT_SORT_CHUNK rows by src, so
- * label gathers of consecutive rows coalesce. */
+ * label gathers of consecutive rows coalesce; mode 3 groups all rows by dst
+ * bucket (2^CC_OPT_BUCKET_SHIFT vertices) and sorts them by src inside each
+ * bucket (one device radix sort, m < 2^31): order-2 async sweeps then hold
+ * the bucket's labels in shared memory (the dst-bucketed sweep kernel). */
 int cc_reorder_edges(cc_ctx* ctx, int mode);
 
 /* Tuning knobs of a context.  Store modes for async sweeps:
@@ -124,6 +127,9 @@ int cc_reorder_edges(cc_ctx* ctx, int mode);
 #define CC_OPT_STORE_MODE_PLAIN 1  /* Schedule.atomic == False (default 0) */
 #define CC_OPT_STORE_MODE_ATOMIC 2 /* Schedule.atomic == True (default 3) */
 #define CC_OPT_SORT_CHUNK 3        /* rows per chunk of layout mode 2 (default 2^23) */
+#define CC_OPT_BUCKET_SHIFT 5      /* layout 3: 2^shift labels per dst bucket (8..15, default 15) */
+#define CC_OPT_ITEM_ROWS 6         /* layout 3: rows per work item (default 2^18) */
+#define CC_OPT_BUCKET_THREADS 7    /* layout 3: threads per CTA (256/512/1024, default 1024) */
 #define CC_OPT_STAGE_LAYOUT 4      /* layout applied while staging: 0 input order (default),
                                       2 chunk-sorted, each chunk sorted as soon as it lands,
                                       overlapped with the next chunk's host->device copy */

@@ -161,6 +161,39 @@ __global__ void k_stage(const T* __restrict__ aos, int64_t rows, int64_t n, lab_
     if (__syncthreads_or(bad) && threadIdx.x == 0) flags[kFlagBad] = 1;
 }
 
+// Layout 3 keys: (dst bucket << sbits) | src, sorted -> bucket-major, src-minor.
+template <typename K>
+__global__ void k_make_keys(const lab_t* __restrict__ src, const lab_t* __restrict__ dst,
+                            int64_t m, int bshift, int sbits, K* keys) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m;
+         i += (int64_t)gridDim.x * blockDim.x)
+        keys[i] = ((K)(dst[i] >> bshift) << sbits) | (K)src[i];
+}
+
+template <typename K>
+__global__ void k_unkey(const K* __restrict__ keys, int64_t m, K mask, lab_t* src) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m;
+         i += (int64_t)gridDim.x * blockDim.x)
+        src[i] = (lab_t)(keys[i] & mask);
+}
+
+// starts[b] = first row whose bucket >= b (lower bound on the sorted keys).
+template <typename K>
+__global__ void k_bucket_starts(const K* __restrict__ keys, int64_t m, int64_t nb, int sbits,
+                                int64_t* starts) {
+    for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nb;
+         b += (int64_t)gridDim.x * blockDim.x) {
+        const K target = (K)b << sbits;
+        int64_t lo = 0, hi = m;
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (keys[mid] < target) lo = mid + 1;
+            else hi = mid;
+        }
+        starts[b] = lo;
+    }
+}
+
 __global__ void k_widen(const lab_t* L, int64_t n, int64_t* out) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x)
@@ -303,6 +336,12 @@ struct cc_ctx {
     int store_mode_plain = cck::kStorePlain;  // async, Schedule.atomic == False
     int store_mode_atomic = cck::kStoreCheckRed;  // async, Schedule.atomic == True
     int64_t sort_chunk = (int64_t)1 << 23;    // rows per chunk (staging, layout mode 2)
+    int layout = 0;                           // current row order (cc_reorder_edges modes)
+    int bucket_shift = 15;                    // layout 3: B = 2^shift labels per bucket
+    int64_t item_rows = (int64_t)1 << 18;     // layout 3: rows per work item
+    int bucket_threads = 1024;
+    cck::BucketItem* items = nullptr;         // layout 3 work items (device)
+    int n_items = 0;
     int stage_layout = 0;                     // layout applied by cc_stage_edges*
     lab_t* sort_ks = nullptr;                 // cached radix-sort scratch
     lab_t* sort_vs = nullptr;
@@ -440,6 +479,8 @@ int set_graph(cc_ctx* c, int64_t m, int64_t n) {
     if (m > 0 && n == 0) return fail(CC_EINVAL, "edge endpoint out of range: n=0");
     c->n = n;
     c->m = m;
+    c->layout = 0;  // a new edge set: any bucketed work items are stale
+    c->n_items = 0;
     return ensure_labels(c);
 }
 
@@ -465,6 +506,42 @@ int order_for(const cc_schedule* s, int64_t sweep) {  // engine.py:61-74
 }
 
 // Enqueue one sweep; flag word (and count for sync) left on device.
+template <int SM, int U>
+int launch_bucketed_t(cc_ctx* c, SweepLaunch sl) {
+    const size_t smem = sizeof(lab_t) * ((size_t)1 << c->bucket_shift);
+    static size_t smem_set = 0;
+    if (smem_set != smem) {
+        CUDA_TRY(cudaFuncSetAttribute(cck::k_sweep_bucketed<SM, U>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        smem_set = smem;
+    }
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, cck::k_sweep_bucketed<SM, U>,
+                                                  c->bucket_threads, smem);
+    if (occ < 1) occ = 1;
+    const int blocks = std::min<int64_t>(c->n_items, (int64_t)c->sm_count * occ);
+    cck::k_sweep_bucketed<SM, U><<<std::max(blocks, 1), c->bucket_threads, smem, sl.stream>>>(
+        c->src, c->dst, c->labels, c->items, c->n_items, c->dflags + kFlagWrote, sl.d_order);
+    CUDA_TRY(cudaGetLastError());
+    return CC_OK;
+}
+
+template <int U>
+int launch_bucketed_u(cc_ctx* c, int sm, SweepLaunch sl) {
+    switch (sm) {
+        case cck::kStorePlain: return launch_bucketed_t<cck::kStorePlain, U>(c, sl);
+        case cck::kStoreRed: return launch_bucketed_t<cck::kStoreRed, U>(c, sl);
+        case cck::kStoreCheckPlain: return launch_bucketed_t<cck::kStoreCheckPlain, U>(c, sl);
+        default: return launch_bucketed_t<cck::kStoreCheckRed, U>(c, sl);
+    }
+}
+
+// U = 4 rows per thread at up to 1024 threads, or 8 at up to 512.
+int launch_bucketed(cc_ctx* c, int sm, SweepLaunch sl) {
+    return c->bucket_threads > 512 ? launch_bucketed_u<4>(c, sm, sl)
+                                   : launch_bucketed_u<8>(c, sm, sl);
+}
+
 int launch_first(cc_ctx* c, lab_t* T) {
     static int occ = 0;
     if (occ == 0) {
@@ -504,11 +581,14 @@ int enqueue_sweep(cc_ctx* c, int order, int sync, int atomic, bool count_changes
                                  cudaMemcpyDeviceToDevice, c->stream));
     }
     lab_t* L = c->labels;
+    const int sm = atomic ? c->store_mode_atomic : c->store_mode_plain;
     int rc;
     if (first) {
         rc = launch_first(c, L);
+    } else if (order == 2 && c->layout == 3 && c->items) {
+        rc = launch_bucketed(c, sm, SweepLaunch{c->stream, nullptr});
     } else {
-        rc = launch_order(c, L, L, order, atomic ? c->store_mode_atomic : c->store_mode_plain);
+        rc = launch_order(c, L, L, order, sm);
     }
     if (rc) return rc;
     if (count_changes) {
@@ -581,7 +661,8 @@ int launch_guarded(cc_ctx* c, const cc_schedule* s, int sm, cudaStream_t st) {
     }
     const SweepLaunch sl{st, &c->dstate->order};
     lab_t* L = c->labels;
-    if (need2) CC_TRY((launch_store_mode<2, 2>(c, L, L, 2, sm, sl)));
+    if (need2 && c->layout == 3 && c->items) CC_TRY(launch_bucketed(c, sm, sl));
+    else if (need2) CC_TRY((launch_store_mode<2, 2>(c, L, L, 2, sm, sl)));
     if (need1) CC_TRY((launch_store_mode<1, 2>(c, L, L, 1, sm, sl)));
     if (needh) CC_TRY((launch_store_mode<0, 1>(c, L, L, s->high_order, sm, sl)));
     return CC_OK;
@@ -878,6 +959,7 @@ void cc_destroy(cc_ctx* c) {
     cudaFree(c->sort_ks);
     cudaFree(c->sort_vs);
     cudaFree(c->sort_tmp);
+    cudaFree(c->items);
     if (c->loop_exec) cudaGraphExecDestroy(c->loop_exec);
     if (c->loop_graph) cudaGraphDestroy(c->loop_graph);
     cudaFree(c->dstate);
@@ -1088,17 +1170,115 @@ int cc_set_option(cc_ctx* c, int option, int64_t value) {
                 return fail(CC_EINVAL, "staging layout must be 0 (input) or 2 (chunk-sorted)");
             c->stage_layout = (int)value;
             return CC_OK;
+        case CC_OPT_BUCKET_SHIFT:
+            if (value < 8 || value > 15)
+                return fail(CC_EINVAL, "bucket shift must be in [8, 15] (<= 128 KB of labels)");
+            c->bucket_shift = (int)value;
+            return CC_OK;
+        case CC_OPT_ITEM_ROWS:
+            if (value < 1024) return fail(CC_EINVAL, "item rows must be >= 1024");
+            c->item_rows = value;
+            return CC_OK;
+        case CC_OPT_BUCKET_THREADS:
+            if (value != 256 && value != 512 && value != 1024)
+                return fail(CC_EINVAL, "bucket threads must be 256, 512 or 1024");
+            c->bucket_threads = (int)value;
+            return CC_OK;
     }
     return fail(CC_EINVAL, "unknown option %d", option);
 }
 
+}  // extern "C"
+
+namespace {
+
+template <typename K>
+int reorder_bucketed_t(cc_ctx* c, int sbits, int total_bits, int64_t nb) {
+    const int64_t m = c->m;
+    K *kin = nullptr, *kout = nullptr;
+    lab_t* vout = nullptr;
+    void* tmp = nullptr;
+    size_t tb = 0;
+    CUDA_TRY(cudaMalloc(&kin, sizeof(K) * m));
+    CUDA_TRY(cudaMalloc(&kout, sizeof(K) * m));
+    CUDA_TRY(cudaMalloc(&vout, sizeof(lab_t) * m));
+    k_make_keys<K><<<grid_for(c, m, 16), kThreads, 0, c->stream>>>(c->src, c->dst, m,
+                                                                    c->bucket_shift, sbits, kin);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, tb, kin, kout, c->dst, vout, (int)m, 0,
+                                             total_bits, c->stream));
+    CUDA_TRY(cudaMalloc(&tmp, tb));
+    CUDA_TRY(cub::DeviceRadixSort::SortPairs(tmp, tb, kin, kout, c->dst, vout, (int)m, 0,
+                                             total_bits, c->stream));
+    k_unkey<K><<<grid_for(c, m, 16), kThreads, 0, c->stream>>>(kout, m,
+                                                                (K)(((K)1 << sbits) - 1), c->src);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaMemcpyAsync(c->dst, vout, sizeof(lab_t) * m, cudaMemcpyDeviceToDevice,
+                             c->stream));
+    int64_t* dstarts = nullptr;
+    CUDA_TRY(cudaMalloc(&dstarts, sizeof(int64_t) * (nb + 1)));
+    k_bucket_starts<K><<<grid_for(c, nb), kThreads, 0, c->stream>>>(kout, m, nb, sbits, dstarts);
+    CUDA_TRY(cudaGetLastError());
+    std::vector<int64_t> starts(nb + 1);
+    CUDA_TRY(cudaMemcpyAsync(starts.data(), dstarts, sizeof(int64_t) * nb,
+                             cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    starts[nb] = m;
+    cudaFree(kin);
+    cudaFree(kout);
+    cudaFree(vout);
+    cudaFree(tmp);
+    cudaFree(dstarts);
+    // work items: each bucket's rows split into pieces of <= item_rows
+    std::vector<cck::BucketItem> items;
+    const int64_t B = (int64_t)1 << c->bucket_shift;
+    for (int64_t b = 0; b < nb; ++b) {
+        const uint32_t base = (uint32_t)(b * B);
+        const uint32_t len = (uint32_t)std::min<int64_t>(B, c->n - b * B);
+        for (int64_t s = starts[b]; s < starts[b + 1]; s += c->item_rows)
+            items.push_back({s, std::min<int64_t>(s + c->item_rows, starts[b + 1]), base, len});
+    }
+    // largest items first so the static round-robin ends balanced
+    std::stable_sort(items.begin(), items.end(), [](const cck::BucketItem& a,
+                                                    const cck::BucketItem& b) {
+        return (a.end - a.start) > (b.end - b.start);
+    });
+    cudaFree(c->items);
+    c->items = nullptr;
+    c->n_items = (int)items.size();
+    if (!items.empty()) {
+        CUDA_TRY(cudaMalloc(&c->items, sizeof(cck::BucketItem) * items.size()));
+        CUDA_TRY(cudaMemcpy(c->items, items.data(), sizeof(cck::BucketItem) * items.size(),
+                            cudaMemcpyHostToDevice));
+    }
+    c->layout = 3;
+    return CC_OK;
+}
+
+// Layout 3: rows grouped by dst bucket, src-sorted inside (one global sort).
+int reorder_bucketed(cc_ctx* c) {
+    if (c->m >= ((int64_t)1 << 31)) return fail(CC_EINVAL, "bucketed layout needs m < 2^31");
+    const int sbits = std::max<int>(1, (int)ccgen::perm_bits((uint64_t)c->n));
+    const int64_t B = (int64_t)1 << c->bucket_shift;
+    const int64_t nb = (c->n + B - 1) / B;
+    const int bbits = std::max<int>(1, (int)ccgen::perm_bits((uint64_t)nb));
+    if (sbits + bbits <= 32) return reorder_bucketed_t<uint32_t>(c, sbits, sbits + bbits, nb);
+    return reorder_bucketed_t<unsigned long long>(c, sbits, sbits + bbits, nb);
+}
+
+}  // namespace
+
+extern "C" {
+
 int cc_reorder_edges(cc_ctx* c, int mode) {
     if (!c) return fail(CC_EINVAL, "null context");
     if (mode == 0) return CC_OK;
-    if (mode != 1 && mode != 2) return fail(CC_EINVAL, "unknown edge layout mode %d", mode);
+    if (mode < 1 || mode > 3) return fail(CC_EINVAL, "unknown edge layout mode %d", mode);
     std::lock_guard<std::mutex> lk(c->mu);
     DeviceGuard g(c->device);
     if (c->m < 2) return CC_OK;
+    if (mode == 3) return reorder_bucketed(c);
+    c->layout = mode;
     // mode 1: one global sort by src; mode 2: independent sorts of
     // consecutive chunks of c->sort_chunk rows (each chunk's label gathers
     // coalesce almost as well, and chunks can be sorted while later chunks

@@ -18,6 +18,8 @@
 #include <stdint.h>
 #include <cuda_runtime.h>
 
+#include <type_traits>
+
 namespace cck {
 
 typedef uint32_t lab_t;
@@ -214,6 +216,97 @@ __global__ void __launch_bounds__(kThreads) k_sweep(const lab_t* __restrict__ sr
     for (int64_t e = (nvec << 2) + tid; e < m; e += stride) {
         lab_t u[1] = {src[e]}, v[1] = {dst[e]};
         wrote |= batch<OK, 1, SM>(R, T, u, v, order);
+    }
+    if (__syncthreads_or(wrote) && threadIdx.x == 0) *flag = 1;
+}
+
+// ---- dst-bucketed order-2 sweep ---------------------------------------------
+// Layout (cc_reorder_edges mode 3): rows grouped by dst bucket
+// [b*B, (b+1)*B) and sorted by src inside each bucket.  A work item is a
+// row range inside one bucket.  The CTA copies the bucket's B labels into
+// shared memory, so every L[dst] gather (the random one) becomes a shared-
+// memory load, and src-sorted rows make the L[src] gathers of a warp
+// coalesce.  Lowerings of cells inside the slice go to shared memory
+// (atomicMin) and are merged into global memory by red.min when the item
+// ends; other cells are lowered in global memory with store mode SM.
+// Reads of the slice may be stale w.r.t. other CTAs -- a legal asynchronous
+// interleaving, and a sweep that decides no lowering anywhere saw unchanged
+// labels everywhere, so the ballot/OR flag stays exact.
+struct BucketItem {
+    int64_t start, end;  // row range
+    uint32_t base, len;  // label slice [base, base+len)
+};
+
+// U rows per thread in flight; the next U rows' (src, dst) are prefetched
+// into registers while the current ones gather, hiding the HBM latency of
+// the edge stream behind the L2 latency of the label gathers.
+template <int SM, int U>
+__global__ void __launch_bounds__(U <= 4 ? 1024 : 512)
+    k_sweep_bucketed(const lab_t* __restrict__ src, const lab_t* __restrict__ dst, lab_t* L,
+                     const BucketItem* __restrict__ items, int n_items, int* __restrict__ flag,
+                     const int* __restrict__ d_order) {
+    extern __shared__ lab_t sl[];
+    if (d_order && *d_order != 2) return;
+    bool wrote = false;
+    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+        const BucketItem w = items[it];
+        const lab_t base = w.base, len = w.len;
+        for (lab_t i = threadIdx.x; i < len; i += blockDim.x) sl[i] = __ldcg(L + base + i);
+        __syncthreads();
+        auto rd = [&](lab_t x) -> lab_t { return (x - base < len) ? sl[x - base] : L[x]; };
+        auto low = [&](lab_t x, lab_t z, auto hot) {
+            if (x - base < len) atomicMin(sl + (x - base), z);
+            else lower<SM, decltype(hot)::value>(L, x, z);
+        };
+        const int64_t T = blockDim.x;
+        lab_t nu[U], nv[U];
+        auto fetch = [&](int64_t r0) {
+#pragma unroll
+            for (int j = 0; j < U; ++j) {
+                const int64_t r = r0 + j * T;
+                const bool in = r < w.end;
+                nu[j] = in ? __ldcs(src + r) : 0u;
+                nv[j] = in ? __ldcs(dst + r) : 0u;
+            }
+        };
+        fetch(w.start + threadIdx.x);
+        for (int64_t r0 = w.start + threadIdx.x; r0 < w.end; r0 += T * U) {
+            lab_t u[U], v[U], lu[U], lv[U], zu[U], zv[U];
+#pragma unroll
+            for (int j = 0; j < U; ++j) {
+                u[j] = nu[j];
+                v[j] = nv[j];
+            }
+            fetch(r0 + T * U);
+#pragma unroll
+            for (int j = 0; j < U; ++j) {
+                const bool live = u[j] != v[j];
+                lv[j] = live ? sl[v[j] - base] : v[j];
+                lu[j] = live ? rd(u[j]) : u[j];
+            }
+#pragma unroll
+            for (int j = 0; j < U; ++j) {
+                zu[j] = (lu[j] != u[j]) ? rd(lu[j]) : lu[j];
+                zv[j] = (lv[j] != v[j]) ? rd(lv[j]) : lv[j];
+            }
+#pragma unroll
+            for (int j = 0; j < U; ++j) {
+                if (u[j] == v[j]) continue;
+                const lab_t z = min(zu[j], zv[j]);
+                using F = std::integral_constant<bool, false>;
+                using H = std::integral_constant<bool, true>;
+                if (lu[j] > z) { low(u[j], z, F{}); wrote = true; }
+                if (lu[j] != u[j] && zu[j] > z) { low(lu[j], z, H{}); wrote = true; }
+                if (lv[j] > z) { atomicMin(sl + (v[j] - base), z); wrote = true; }
+                if (lv[j] != v[j] && zv[j] > z) { low(lv[j], z, H{}); wrote = true; }
+            }
+        }
+        __syncthreads();
+        for (lab_t i = threadIdx.x; i < len; i += blockDim.x) {
+            const lab_t s = sl[i];
+            if (s < __ldcg(L + base + i)) atomicMin(L + base + i, s);
+        }
+        __syncthreads();
     }
     if (__syncthreads_or(wrote) && threadIdx.x == 0) *flag = 1;
 }

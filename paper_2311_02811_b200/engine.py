@@ -134,7 +134,7 @@ def _unpack_graph(g):
     return int(n), edges
 
 
-LAYOUTS = {"input": 0, "src_sorted": 1, "chunk_sorted": 2}
+LAYOUTS = {"input": 0, "src_sorted": 1, "chunk_sorted": 2, "dst_bucketed": 3}
 AUTO_SORT_MIN_ROWS = 1 << 20
 
 
@@ -183,7 +183,7 @@ def stage_graph(ctx: _lib.Context, n: int, edges, layout: str = "auto") -> None:
         _lib.check(lib.cc_stage_edges(ctx.handle, ctypes.c_void_p(e.ctypes.data),
                                       e.dtype.itemsize, m, n))
     ctx.n, ctx.m = n, m
-    if layout == "src_sorted":
+    if layout in ("src_sorted", "dst_bucketed"):
         _lib.check(lib.cc_reorder_edges(ctx.handle, LAYOUTS[layout]))
 
 

@@ -377,6 +377,34 @@ def test_graph_loop_cap_and_rebuild():
     ctx.close()
 
 
+@pytest.mark.parametrize("bshift,item_rows,threads", [(8, 1024, 256), (12, 5000, 512),
+                                                      (15, 1 << 18, 1024)])
+def test_dst_bucketed_layout_exact(bshift, item_rows, threads):
+    """Layout 3 + the shared-memory bucketed order-2 sweep, host and graph loops,
+    plain and atomic schedules, on RMAT / grid / forest / ragged inputs."""
+    graphs = [graphgen.rmat(14, 16, 5), graphgen.grid(150, 170, 0.55, 3),
+              graphgen.forest(30, 2), spec.erdos_renyi(3001, 7777, 4)]
+    ctx = _lib.Context(0)
+    ctx.set_option(_lib.CC_OPT_BUCKET_SHIFT, bshift)
+    ctx.set_option(_lib.CC_OPT_ITEM_ROWS, item_rows)
+    ctx.set_option(_lib.CC_OPT_BUCKET_THREADS, threads)
+    for n, e in graphs:
+        exp = oracle.rem_union_find(n, e)
+        engine.stage_graph(ctx, n, e, "dst_bucketed")
+        for sched in (make_schedule("c2"), make_schedule("c2", atomic=False),
+                      make_schedule("c1m1m", 8)):
+            for host_loop in (False, True):
+                labels = np.empty(n, dtype=np.int64)
+                _, st = engine.run_staged(ctx, sched, labels_out=labels, count_changes=False,
+                                          early_check=False, host_loop=host_loop)
+                assert np.array_equal(labels, exp), (n, sched, host_loop)
+                check_invariants(labels, st)
+        labels = np.empty(n, dtype=np.int64)
+        engine.run_staged(ctx, make_schedule("c2", sync=True), labels_out=labels)
+        assert np.array_equal(labels, exp)
+    ctx.close()
+
+
 def test_staged_chunk_sort_from_host_matches_device_reorder():
     n, e = graphgen.rmat(16, 16, 2, elem_bytes=4)
     exp = oracle.rem_union_find(n, e)

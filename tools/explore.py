@@ -15,9 +15,12 @@ from paper_2311_02811_b200 import _lib, engine, graphgen  # noqa: E402
 from paper_2311_02811_b200.engine import make_schedule  # noqa: E402
 
 
-def prepare(cfg, layout, chunk):
+def prepare(cfg, layout, chunk, bshift=15, item_rows=1 << 18, bthreads=1024):
     ctx = _lib.Context(0, torch.cuda.current_stream().cuda_stream)
     ctx.set_option(_lib.CC_OPT_SORT_CHUNK, chunk)
+    ctx.set_option(_lib.CC_OPT_BUCKET_SHIFT, bshift)
+    ctx.set_option(_lib.CC_OPT_ITEM_ROWS, item_rows)
+    ctx.set_option(_lib.CC_OPT_BUCKET_THREADS, bthreads)
     spec = graphgen.CONFIGS[cfg]
     if spec["kind"] == "rmat":
         graphgen.rmat_device(ctx, spec["scale"], spec["edgefactor"], 1)
@@ -52,14 +55,18 @@ def main():
     ap.add_argument("--stores", default="1")
     ap.add_argument("--chunk", type=int, default=1 << 23)
     ap.add_argument("--atomic", type=int, default=1)
+    ap.add_argument("--bshift", type=int, default=15)
+    ap.add_argument("--item-rows", type=int, default=1 << 18)
+    ap.add_argument("--bthreads", type=int, default=1024)
+    ap.add_argument("--no-fs", action="store_true")
     a = ap.parse_args()
     for cfg in a.configs:
         for layout in a.layouts.split(","):
-            ctx, tr = prepare(cfg, layout, a.chunk)
+            ctx, tr = prepare(cfg, layout, a.chunk, a.bshift, a.item_rows, a.bthreads)
             for sm in map(int, a.stores.split(",")):
                 ctx.set_option(_lib.CC_OPT_STORE_MODE_ATOMIC if a.atomic else
                                _lib.CC_OPT_STORE_MODE_PLAIN, sm)
-                for fs in (False, True):
+                for fs in ((False,) if a.no_fs else (False, True)):
                     st = measure(ctx, make_schedule("c2", atomic=bool(a.atomic)),
                                  early_check=False, first_scatter=fs)
                     print(f"{cfg:9s} layout={layout:12s} reorder={tr*1e3:6.2f}ms store={sm} "
