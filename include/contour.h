@@ -141,6 +141,10 @@ int cc_fold_flag(cc_ctx* ctx, int first);
 int cc_compress(cc_ctx* ctx, int* rounds_out);
 /* early_convergence_check(g, labels) (engine.py:331-365) on device. */
 int cc_early_check(cc_ctx* ctx, int* ok_out);
+/* Size-independent certificate of the device labels: *result bit 0 = some
+ * edge has L[u] != L[v], bit 1 = some L[L[x]] != L[x], bit 2 = some
+ * L[x] > x; 0 means every component carries one root label <= its IDs. */
+int cc_verify(cc_ctx* ctx, int* result);
 int cc_read_labels(cc_ctx* ctx, void* out_host, int elem_bytes);
 int cc_synchronize(cc_ctx* ctx);
 

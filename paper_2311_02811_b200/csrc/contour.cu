@@ -124,6 +124,15 @@ __global__ void k_check_edges(const lab_t* __restrict__ src, const lab_t* __rest
     if (__syncthreads_or(bad) && threadIdx.x == 0) flags[kFlagBad] = 1;
 }
 
+// Forest invariant L[x] <= x -- part of cc_verify.
+__global__ void k_check_le(const lab_t* L, int64_t n, int* flags) {
+    bool bad = false;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        bad |= ((int64_t)L[i] > i);
+    if (__syncthreads_or(bad) && threadIdx.x == 0) flags[3] = 1;
+}
+
 // Pointer-jumping compress L[v] = L[L[v]] (north-star step 4; the semantic
 // model is normalize_labels, baselines.py:146-152).
 __global__ void k_compress(lab_t* L, int64_t n, int* flags) {
@@ -1063,6 +1072,36 @@ int cc_early_check(cc_ctx* c, int* ok) {
     std::lock_guard<std::mutex> lk(c->mu);
     DeviceGuard g(c->device);
     return early_check(c, ok);
+}
+
+// Size-independent certificate of a final labelling (used where the host
+// oracle cannot run): bit 0 some edge has L[u] != L[v], bit 1 some label is
+// not a root (L[L[x]] != L[x]), bit 2 some L[x] > x.  0 = every component
+// carries one root label <= all its vertex IDs.
+int cc_verify(cc_ctx* c, int* result) {
+    if (!c || !result) return fail(CC_EINVAL, "null argument");
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard g(c->device);
+    *result = 0;
+    if (c->n == 0) return CC_OK;
+    CUDA_TRY(cudaMemsetAsync(c->dflags + kFlagBad, 0, sizeof(int), c->stream));
+    CUDA_TRY(cudaMemsetAsync(c->dflags + 3, 0, sizeof(int), c->stream));
+    k_check_idem<<<grid_for(c, c->n), kThreads, 0, c->stream>>>(c->labels, c->n, c->dflags);
+    k_check_le<<<grid_for(c, c->n), kThreads, 0, c->stream>>>(c->labels, c->n, c->dflags);
+    CUDA_TRY(cudaGetLastError());
+    CC_TRY(read_flags(c));
+    const int idem_bad = c->hflags[kFlagBad], le_bad = c->hflags[3];
+    int edge_bad = 0;
+    if (c->m > 0) {
+        CUDA_TRY(cudaMemsetAsync(c->dflags + kFlagBad, 0, sizeof(int), c->stream));
+        k_check_edges<<<grid_for(c, c->m), kThreads, 0, c->stream>>>(c->src, c->dst, c->m,
+                                                                     c->labels, c->dflags);
+        CUDA_TRY(cudaGetLastError());
+        CC_TRY(read_flags(c));
+        edge_bad = c->hflags[kFlagBad];
+    }
+    *result = (edge_bad ? 1 : 0) | (idem_bad ? 2 : 0) | (le_bad ? 4 : 0);
+    return CC_OK;
 }
 
 int cc_read_labels(cc_ctx* c, void* out, int eb) {

@@ -230,6 +230,15 @@ def run_staged(ctx: _lib.Context, schedule: Schedule, *, count_changes: bool = T
     return labels_out, stats
 
 
+def verify_staged(ctx: _lib.Context) -> int:
+    """cc_verify on the device labels of the last run: 0 = valid final
+    labelling (per edge L[u]==L[v], L[L[x]]==L[x], L[x]<=x); else a bitmask
+    (1 edge disagreement, 2 non-root label, 4 label above its vertex)."""
+    r = ctypes.c_int(0)
+    _lib.check(ctx.lib.cc_verify(ctx.handle, ctypes.byref(r)))
+    return r.value
+
+
 def run_contour(g, schedule: Schedule, threads: int = 1, seed: Optional[int] = None, *,
                 device: int = 0, count_changes: bool = True, early_check: bool = True,
                 sweep_times: bool = True, layout: str = "auto",

@@ -107,6 +107,17 @@ def test_threaded_sync_atomic_is_order_independent():
         assert st.sweeps_executed == ref.sweeps_executed
 
 
+def test_parallel_checker_matches_sequential_oracle(golden):
+    for g in golden["graphs"][::4]:
+        e = np.asarray(g["edges"], dtype=np.int64).reshape(-1, 2)
+        assert oracle.parallel_components(g["n"], e, threads=3).tolist() == g["labels"]
+    for n, e in (gen.rmat(14, 16, 2), gen.grid(200, 200, 0.55, 1), gen.forest(25, 3)):
+        exp = oracle.rem_union_find(n, e)
+        for t in (1, 8):
+            assert np.array_equal(oracle.parallel_components(n, e, threads=t), exp)
+        assert np.array_equal(oracle.parallel_components(n, e.astype(np.int32), 4), exp)
+
+
 def test_normalize_and_stars():
     assert oracle.normalize_labels(np.array([0, 0, 1, 2])).tolist() == [0, 0, 0, 0]
     with pytest.raises(ValueError):

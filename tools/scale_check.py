@@ -1,0 +1,98 @@
+"""Full-size runs of the BASELINE configs on one B200: device time, sweeps,
+the device certificate (cc_verify) and -- where host RAM allows -- exact
+equality with a CPU checker.
+
+    python tools/scale_check.py forest rmat28 grid4096 [--no-oracle]
+
+Prints one JSON line per config.  The checker is the sequential oracle for
+grid4096 and the multi-threaded union-find checker (same output contract as
+rem_union_find) for forest / rmat28.
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+
+from paper_2311_02811_b200 import _lib, engine, graphgen  # noqa: E402
+from paper_2311_02811_b200.engine import make_schedule  # noqa: E402
+
+
+def run(cfg, args):
+    spec = graphgen.CONFIGS[cfg]
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    ctx = _lib.Context(0, stream.cuda_stream)
+    rec = {"config": cfg}
+    t0 = time.perf_counter()
+    host = None
+    if spec["kind"] == "rmat":
+        n, m = graphgen.rmat_device(ctx, spec["scale"], spec["edgefactor"], 1)
+        _lib.check(ctx.lib.cc_reorder_edges(ctx.handle, engine.LAYOUTS["chunk_sorted"]))
+    else:
+        n, host = graphgen.make(spec, 1, elem_bytes=8)
+        m = host.shape[0]
+        engine.stage_graph(ctx, n, host, "chunk_sorted")
+    torch.cuda.synchronize()
+    rec.update(n=int(n), m_input=int(m), prep_s=round(time.perf_counter() - t0, 2))
+    sched = make_schedule("c2")
+    runs = []
+    for _ in range(args.repeats):
+        _, st = engine.run_staged(ctx, sched, count_changes=False, early_check=False)
+        runs.append(st)
+    best = min(runs, key=lambda s: s.device_seconds)
+    rec.update(device_s=best.device_seconds, edges_per_s=m / best.device_seconds,
+               sweeps=[s.sweeps_executed for s in runs],
+               sweep_ms=[round(t * 1e3, 3) for t in best.sweep_seconds],
+               b_sweep_gbs=(8 * m + 4 * n) / (sum(best.sweep_seconds) /
+                                              len(best.sweep_seconds)) / 1e9)
+    rec["verify"] = engine.verify_staged(ctx)
+    if not args.no_oracle:
+        from oracle import oracle
+        labels = np.empty(n, dtype=np.int64)
+        _lib.check(ctx.lib.cc_read_labels(ctx.handle, ctypes_ptr(labels), 8))
+        ctx.close()
+        if host is None:
+            t1 = time.perf_counter()
+            _, host = graphgen.rmat(spec["scale"], spec["edgefactor"], 1, elem_bytes=4)
+            rec["host_gen_s"] = round(time.perf_counter() - t1, 1)
+        t1 = time.perf_counter()
+        if cfg == "grid4096":
+            exp = oracle.rem_union_find(n, host)
+            rec["checker"] = "sequential oracle (rem_union_find restatement)"
+        else:
+            exp = oracle.parallel_components(n, host)
+            rec["checker"] = "multi-threaded union-find (rem_union_find output contract)"
+        rec["checker_s"] = round(time.perf_counter() - t1, 1)
+        rec["exact"] = bool(np.array_equal(labels, exp))
+        rec["components"] = int(np.count_nonzero(exp == np.arange(n)))
+        del exp, labels
+    else:
+        ctx.close()
+    del host
+    print(json.dumps(rec), flush=True)
+
+
+def ctypes_ptr(a):
+    import ctypes
+    return ctypes.c_void_p(a.ctypes.data)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("configs", nargs="+")
+    ap.add_argument("--no-oracle", action="store_true")
+    ap.add_argument("--repeats", type=int, default=3)
+    args = ap.parse_args()
+    for cfg in args.configs:
+        run(cfg, args)
+
+
+if __name__ == "__main__":
+    main()
