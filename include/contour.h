@@ -118,7 +118,11 @@ int cc_sweep(cc_ctx* ctx, int order, int sync, int atomic, int first, int* wrote
  * label gathers of consecutive rows coalesce; mode 3 groups all rows by dst
  * bucket (2^CC_OPT_BUCKET_SHIFT vertices) and sorts them by src inside each
  * bucket (one device radix sort, m < 2^31): order-2 async sweeps then hold
- * the bucket's labels in shared memory (the dst-bucketed sweep kernel). */
+ * the bucket's labels in shared memory (the dst-bucketed sweep kernel);
+ * mode 4 partitions rows by dst into L2-sized windows of 2^CC_OPT_TILE_SHIFT
+ * vertices and sorts each window's rows by src (any m; 8m bytes scratch), so
+ * a grid-stride sweep gathers dst labels from one L2-resident window at a
+ * time -- for label arrays larger than L2 (RMAT-28: 1 GB). */
 int cc_reorder_edges(cc_ctx* ctx, int mode);
 
 /* Tuning knobs of a context.  Store modes for async sweeps:
@@ -130,6 +134,10 @@ int cc_reorder_edges(cc_ctx* ctx, int mode);
 #define CC_OPT_BUCKET_SHIFT 5      /* layout 3: 2^shift labels per dst bucket (8..15, default 15) */
 #define CC_OPT_ITEM_ROWS 6         /* layout 3: rows per work item (default 2^18) */
 #define CC_OPT_BUCKET_THREADS 7    /* layout 3: threads per CTA (256/512/1024, default 1024) */
+#define CC_OPT_TILE_SHIFT 8        /* layout 4: 2^shift labels per L2 window (default 24 = 64 MB) */
+#define CC_OPT_SHORTCUT 9          /* pointer-jumping passes L[v]=L[L[v]] after every async sweep
+                                      without exact counting (0..8, default 1) */
+#define CC_OPT_TILE_SPLIT 10       /* layout 4: independently src-sorted runs per window (default 4) */
 #define CC_OPT_STAGE_LAYOUT 4      /* layout applied while staging: 0 input order (default),
                                       2 chunk-sorted, each chunk sorted as soon as it lands,
                                       overlapped with the next chunk's host->device copy */

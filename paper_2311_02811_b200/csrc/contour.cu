@@ -203,6 +203,53 @@ __global__ void k_bucket_starts(const K* __restrict__ keys, int64_t m, int64_t n
     }
 }
 
+// Layout 4 partition: rows -> P = ceil(n / 2^shift) dst buckets (P <= 1024).
+constexpr int kMaxTiles = 1024;
+constexpr int64_t kPartRows = 1 << 16;  // rows per partition block
+
+__global__ void __launch_bounds__(kThreads) k_tile_hist(const lab_t* __restrict__ dst, int64_t m,
+                                                        int shift, int P,
+                                                        unsigned long long* counts) {
+    __shared__ unsigned int h[kMaxTiles];
+    for (int i = threadIdx.x; i < P; i += blockDim.x) h[i] = 0;
+    __syncthreads();
+    const int64_t lo = (int64_t)blockIdx.x * kPartRows;
+    const int64_t hi = min(lo + kPartRows, m);
+    for (int64_t e = lo + threadIdx.x; e < hi; e += blockDim.x) atomicAdd(&h[dst[e] >> shift], 1u);
+    __syncthreads();
+    for (int i = threadIdx.x; i < P; i += blockDim.x)
+        if (h[i]) atomicAdd(counts + i, (unsigned long long)h[i]);
+}
+
+// Each block reserves one slice per bucket (one global atomic per bucket),
+// then scatters its rows into the reservations.
+__global__ void __launch_bounds__(kThreads) k_tile_scatter(const lab_t* __restrict__ src,
+                                                           const lab_t* __restrict__ dst,
+                                                           int64_t m, int shift, int P,
+                                                           unsigned long long* cursor,
+                                                           lab_t* osrc, lab_t* odst) {
+    __shared__ unsigned int h[kMaxTiles];
+    __shared__ unsigned long long basep[kMaxTiles];
+    for (int i = threadIdx.x; i < P; i += blockDim.x) h[i] = 0;
+    __syncthreads();
+    const int64_t lo = (int64_t)blockIdx.x * kPartRows;
+    const int64_t hi = min(lo + kPartRows, m);
+    for (int64_t e = lo + threadIdx.x; e < hi; e += blockDim.x) atomicAdd(&h[dst[e] >> shift], 1u);
+    __syncthreads();
+    for (int i = threadIdx.x; i < P; i += blockDim.x) {
+        basep[i] = h[i] ? atomicAdd(cursor + i, (unsigned long long)h[i]) : 0ull;
+        h[i] = 0;
+    }
+    __syncthreads();
+    for (int64_t e = lo + threadIdx.x; e < hi; e += blockDim.x) {
+        const lab_t d = dst[e];
+        const int b = (int)(d >> shift);
+        const unsigned long long pos = basep[b] + atomicAdd(&h[b], 1u);
+        osrc[pos] = src[e];
+        odst[pos] = d;
+    }
+}
+
 __global__ void k_widen(const lab_t* L, int64_t n, int64_t* out) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x)
@@ -347,6 +394,9 @@ struct cc_ctx {
     int64_t sort_chunk = (int64_t)1 << 23;    // rows per chunk (staging, layout mode 2)
     int layout = 0;                           // current row order (cc_reorder_edges modes)
     int bucket_shift = 15;                    // layout 3: B = 2^shift labels per bucket
+    int tile_shift = 24;                      // layout 4: 2^shift labels (64 MB) per L2 window
+    int shortcut = 1;  // pointer-jumping passes after every async sweep (fast path)
+    int tile_split = 4;  // layout 4: independently sorted runs per L2 window
     int64_t item_rows = (int64_t)1 << 18;     // layout 3: rows per work item
     int bucket_threads = 1024;
     cck::BucketItem* items = nullptr;         // layout 3 work items (device)
@@ -373,6 +423,8 @@ struct cc_ctx {
         int64_t m, n, cap;
         cc_schedule s;
         int sm;
+        int shortcut;
+        int layout;
     } loop_key = {};
     std::mutex mu;
 };
@@ -490,6 +542,7 @@ int set_graph(cc_ctx* c, int64_t m, int64_t n) {
     c->m = m;
     c->layout = 0;  // a new edge set: any bucketed work items are stale
     c->n_items = 0;
+    c->loop_key.m = -1;
     return ensure_labels(c);
 }
 
@@ -687,7 +740,8 @@ bool same_schedule(const cc_schedule& a, const cc_schedule& b) {
 int build_loop(cc_ctx* c, const cc_schedule* s, int64_t cap, int sm) {
     auto& k = c->loop_key;
     if (c->loop_exec && k.src == c->src && k.dst == c->dst && k.labels == c->labels &&
-        k.m == c->m && k.n == c->n && k.cap == cap && same_schedule(k.s, *s) && k.sm == sm)
+        k.m == c->m && k.n == c->n && k.cap == cap && same_schedule(k.s, *s) && k.sm == sm &&
+        k.shortcut == c->shortcut && k.layout == c->layout)
         return CC_OK;
     if (c->loop_exec) cudaGraphExecDestroy(c->loop_exec);
     if (c->loop_graph) cudaGraphDestroy(c->loop_graph);
@@ -722,6 +776,8 @@ int build_loop(cc_ctx* c, const cc_schedule* s, int64_t cap, int sm) {
     CUDA_TRY(cudaStreamBeginCaptureToGraph(c->body_stream, body, nullptr, nullptr, 0,
                                            cudaStreamCaptureModeRelaxed));
     CC_TRY(launch_guarded(c, s, sm, c->body_stream));
+    for (int j = 0; j < c->shortcut; ++j)
+        k_compress<<<grid_for(c, c->n), kThreads, 0, c->body_stream>>>(c->labels, c->n, c->dflags);
     k_loop_control<<<1, 1, 0, c->body_stream>>>(c->dstate, c->drec, c->dflags, *s, cap, h);
     CUDA_TRY(cudaGetLastError());
     cudaGraph_t body_out = nullptr;
@@ -729,7 +785,7 @@ int build_loop(cc_ctx* c, const cc_schedule* s, int64_t cap, int sm) {
     k_compress<<<grid_for(c, c->n), kThreads, 0, cs>>>(c->labels, c->n, c->dflags);
     CUDA_TRY(cudaStreamEndCapture(cs, &c->loop_graph));
     CUDA_TRY(cudaGraphInstantiate(&c->loop_exec, c->loop_graph, 0));
-    k = {c->src, c->dst, c->labels, c->m, c->n, cap, *s, sm};
+    k = {c->src, c->dst, c->labels, c->m, c->n, cap, *s, sm, c->shortcut, c->layout};
     return CC_OK;
 }
 
@@ -1147,6 +1203,10 @@ int cc_run(cc_ctx* c, const cc_schedule* s, int flags, int64_t cap, void* labels
         const int order = order_for(s, sweep);
         if (times) CUDA_TRY(cudaEventRecord(c->ev0, c->stream));
         CC_TRY(enqueue_sweep(c, order, sync, s->atomic, count, sweep == 1 && first_scatter));
+        if (!sync && !count)
+            for (int j = 0; j < c->shortcut; ++j)
+                k_compress<<<grid_for(c, c->n), kThreads, 0, c->stream>>>(c->labels, c->n,
+                                                                          c->dflags);
         if (times) CUDA_TRY(cudaEventRecord(c->ev1, c->stream));
         CC_TRY(read_flags(c));
         const bool wrote = c->hflags[kFlagWrote] != 0;
@@ -1217,6 +1277,18 @@ int cc_set_option(cc_ctx* c, int option, int64_t value) {
         case CC_OPT_ITEM_ROWS:
             if (value < 1024) return fail(CC_EINVAL, "item rows must be >= 1024");
             c->item_rows = value;
+            return CC_OK;
+        case CC_OPT_SHORTCUT:
+            if (value < 0 || value > 8) return fail(CC_EINVAL, "shortcut passes must be 0..8");
+            c->shortcut = (int)value;
+            return CC_OK;
+        case CC_OPT_TILE_SPLIT:
+            if (value < 1 || value > 1024) return fail(CC_EINVAL, "tile split must be 1..1024");
+            c->tile_split = (int)value;
+            return CC_OK;
+        case CC_OPT_TILE_SHIFT:
+            if (value < 10 || value > 30) return fail(CC_EINVAL, "tile shift must be in [10, 30]");
+            c->tile_shift = (int)value;
             return CC_OK;
         case CC_OPT_BUCKET_THREADS:
             if (value != 256 && value != 512 && value != 1024)
@@ -1305,6 +1377,78 @@ int reorder_bucketed(cc_ctx* c) {
     return reorder_bucketed_t<unsigned long long>(c, sbits, sbits + bbits, nb);
 }
 
+// Layout 4: rows partitioned by dst into L2-window buckets of 2^tile_shift
+// vertices (default 2^23: 32 MB of labels), then sorted by src inside each
+// bucket.  A grid-stride sweep walks the buckets in order, so at any time
+// the gathered dst labels come from one 32 MB window that stays in L2 and
+// the src gathers of consecutive rows coalesce.  Scales past 2^31 rows
+// (partition kernels + per-bucket CUB sorts); needs 8m bytes of scratch.
+int reorder_l2tiles(cc_ctx* c) {
+    const int64_t m = c->m;
+    const int shift = c->tile_shift;
+    const int64_t P = (c->n + ((int64_t)1 << shift) - 1) >> shift;
+    if (P > kMaxTiles) return fail(CC_EINVAL, "too many L2 tiles (%lld); raise tile shift",
+                                   (long long)P);
+    unsigned long long* dcnt = nullptr;
+    CUDA_TRY(cudaMalloc(&dcnt, sizeof(unsigned long long) * P));
+    CUDA_TRY(cudaMemsetAsync(dcnt, 0, sizeof(unsigned long long) * P, c->stream));
+    const int64_t nblk = (m + kPartRows - 1) / kPartRows;
+    k_tile_hist<<<(unsigned)nblk, kThreads, 0, c->stream>>>(c->dst, m, shift, (int)P, dcnt);
+    CUDA_TRY(cudaGetLastError());
+    std::vector<unsigned long long> cnt(P), start(P + 1, 0);
+    CUDA_TRY(cudaMemcpyAsync(cnt.data(), dcnt, sizeof(unsigned long long) * P,
+                             cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    for (int64_t b = 0; b < P; ++b) start[b + 1] = start[b] + cnt[b];
+    CUDA_TRY(cudaMemcpyAsync(dcnt, start.data(), sizeof(unsigned long long) * P,
+                             cudaMemcpyHostToDevice, c->stream));
+    lab_t *os = nullptr, *od = nullptr;
+    CUDA_TRY(cudaMalloc(&os, sizeof(lab_t) * m));
+    CUDA_TRY(cudaMalloc(&od, sizeof(lab_t) * m));
+    k_tile_scatter<<<(unsigned)nblk, kThreads, 0, c->stream>>>(c->src, c->dst, m, shift, (int)P,
+                                                                dcnt, os, od);
+    CUDA_TRY(cudaGetLastError());
+    // per-bucket sort by src, out of the scratch copy straight back into src/dst
+    const int bits = std::max<int>(1, (int)ccgen::perm_bits((uint64_t)c->n));
+    int64_t maxb = 0;
+    for (int64_t b = 0; b < P; ++b) maxb = std::max<int64_t>(maxb, (int64_t)cnt[b]);
+    if (maxb >= ((int64_t)1 << 31)) {
+        cudaFree(os);
+        cudaFree(od);
+        cudaFree(dcnt);
+        return fail(CC_EINVAL, "an L2 tile holds >= 2^31 rows; lower the tile shift");
+    }
+    void* tmp = nullptr;
+    size_t tb = 0;
+    CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, tb, os, c->src, od, c->dst,
+                                             (int)std::max<int64_t>(maxb, 1), 0, bits,
+                                             c->stream));
+    CUDA_TRY(cudaMalloc(&tmp, tb));
+    // each window is sorted as tile_split independent runs: a sweep then
+    // crosses the src range tile_split times per window, which propagates
+    // labels further within one sweep (fewer sweeps) at a small cost in
+    // src-gather coalescing
+    for (int64_t b = 0; b < P; ++b) {
+        const int64_t off = (int64_t)start[b], len = (int64_t)cnt[b];
+        const int64_t k = std::max<int64_t>(1, std::min<int64_t>(c->tile_split, len));
+        for (int64_t r = 0; r < k; ++r) {
+            const int64_t lo = off + len * r / k, hi = off + len * (r + 1) / k;
+            if (hi <= lo) continue;
+            size_t t2 = tb;
+            CUDA_TRY(cub::DeviceRadixSort::SortPairs(tmp, t2, os + lo, c->src + lo, od + lo,
+                                                     c->dst + lo, (int)(hi - lo), 0, bits,
+                                                     c->stream));
+        }
+    }
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    cudaFree(tmp);
+    cudaFree(os);
+    cudaFree(od);
+    cudaFree(dcnt);
+    c->layout = 4;
+    return CC_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -1312,11 +1456,13 @@ extern "C" {
 int cc_reorder_edges(cc_ctx* c, int mode) {
     if (!c) return fail(CC_EINVAL, "null context");
     if (mode == 0) return CC_OK;
-    if (mode < 1 || mode > 3) return fail(CC_EINVAL, "unknown edge layout mode %d", mode);
+    if (mode < 1 || mode > 4) return fail(CC_EINVAL, "unknown edge layout mode %d", mode);
     std::lock_guard<std::mutex> lk(c->mu);
     DeviceGuard g(c->device);
     if (c->m < 2) return CC_OK;
+    c->loop_key.m = -1;  // the captured loop may reference the old layout's buffers
     if (mode == 3) return reorder_bucketed(c);
+    if (mode == 4) return reorder_l2tiles(c);
     c->layout = mode;
     // mode 1: one global sort by src; mode 2: independent sorts of
     // consecutive chunks of c->sort_chunk rows (each chunk's label gathers

@@ -29,12 +29,13 @@ from . import _lib, graphgen
 class CudaShard:
     """A rank's edge shard + label replica on its GPU (libcontour.so)."""
 
-    def __init__(self, ctx: _lib.Context, n: int):
+    def __init__(self, ctx: _lib.Context, n: int, atomic: bool = True):
         import torch
         if n >= 2 ** 31:
             raise ValueError("multi-GPU exchange uses int32 labels: n must be < 2^31")
         self.ctx = ctx
         self.n = n
+        self.atomic = atomic  # Schedule.atomic: red.min (with hot-cell re-check) vs plain stores
         self.labels = torch.empty(n + 1, dtype=torch.int32, device=f"cuda:{ctx.device}")
         _lib.check(ctx.lib.cc_attach_labels(ctx.handle, ctypes.c_void_p(self.labels.data_ptr())))
 
@@ -42,7 +43,8 @@ class CudaShard:
         _lib.check(self.ctx.lib.cc_init_labels(self.ctx.handle))
 
     def sweep(self, order: int, first: bool = False):
-        _lib.check(self.ctx.lib.cc_sweep(self.ctx.handle, order, 0, 0, int(first), None))
+        _lib.check(self.ctx.lib.cc_sweep(self.ctx.handle, order, 0, int(self.atomic), int(first),
+                                         None))
 
     def fold(self, first: bool):
         _lib.check(self.ctx.lib.cc_fold_flag(self.ctx.handle, int(first)))
@@ -82,17 +84,28 @@ class ShardedContour:
         self.cadence = max(1, int(cadence))
         self.allreduce = allreduce or nccl_allreduce_min(group)
         self.cap = n + 2 if cap is None else cap
+        self.layout = "input"
+        self.first_scatter = False  # load-free sweep 1 (exact, but adds a sweep on RMAT)
 
     @classmethod
     def from_rmat(cls, scale: int, edgefactor: int, seed: int, rank: int, world: int,
-                  device: int, **kw):
+                  device: int, layout: str = "auto", atomic: bool = True, **kw):
+        """Generate this rank's contiguous row shard of the symmetrised RMAT
+        list on its GPU and lay it out (engine.resolve_layout)."""
         import torch
+
+        from .engine import LAYOUTS, resolve_layout
         ctx = _lib.Context(device, torch.cuda.current_stream(device).cuda_stream)
         n = 1 << scale
         total = 2 * edgefactor * n
         lo, hi = shard_rows(total, rank, world)
         graphgen.rmat_device(ctx, scale, edgefactor, seed, row_lo=lo, row_hi=hi)
-        return cls(CudaShard(ctx, n), n, total, **kw)
+        layout = resolve_layout(layout, hi - lo, n)
+        if LAYOUTS[layout]:
+            _lib.check(ctx.lib.cc_reorder_edges(ctx.handle, LAYOUTS[layout]))
+        runner = cls(CudaShard(ctx, n, atomic), n, total, **kw)
+        runner.layout = layout
+        return runner
 
     def run(self) -> int:
         """Converge; returns the number of exchange rounds."""
@@ -105,7 +118,7 @@ class ShardedContour:
                 if sweep > self.cap:
                     from .errors import IterationCapExceeded
                     raise IterationCapExceeded(f"no convergence after {self.cap} sweeps")
-                self.shard.sweep(self.order_for(sweep), first=(sweep == 1))
+                self.shard.sweep(self.order_for(sweep), first=(sweep == 1 and self.first_scatter))
                 self.shard.fold(first=(k == 0))
             self.allreduce(self.shard.labels)
             if int(self.shard.labels[self.n].item()) == 1:

@@ -134,15 +134,21 @@ def _unpack_graph(g):
     return int(n), edges
 
 
-LAYOUTS = {"input": 0, "src_sorted": 1, "chunk_sorted": 2, "dst_bucketed": 3}
+LAYOUTS = {"input": 0, "src_sorted": 1, "chunk_sorted": 2, "dst_bucketed": 3, "l2_tiled": 4}
 AUTO_SORT_MIN_ROWS = 1 << 20
 
 
-def resolve_layout(layout: str, m: int) -> str:
-    """"auto": chunk-sorted staging for graphs with >= 2^20 rows (hides under
-    the host->device copy, ~2x faster sweeps), input order below that."""
+AUTO_L2_LABEL_BYTES = 96 << 20  # the 126 MB L2 holds the labels plus the edge stream's lines
+
+
+def resolve_layout(layout: str, m: int, n: int = 0) -> str:
+    """"auto": input order below 2^20 rows; chunk-sorted staging while the
+    label array fits comfortably in L2 (it hides under the host->device copy,
+    ~2x faster sweeps); L2-window tiles (layout 4) for larger label arrays."""
     if layout == "auto":
-        return "chunk_sorted" if m >= AUTO_SORT_MIN_ROWS else "input"
+        if m < AUTO_SORT_MIN_ROWS:
+            return "input"
+        return "chunk_sorted" if 4 * n <= AUTO_L2_LABEL_BYTES else "l2_tiled"
     if layout not in LAYOUTS:
         raise ValueError(f"unknown edge layout '{layout}'")
     return layout
@@ -159,7 +165,7 @@ def stage_graph(ctx: _lib.Context, n: int, edges, layout: str = "auto") -> None:
     "src_sorted" sorts all rows by src afterwards, "auto" picks."""
     m_rows = int(edges.shape[0]) if hasattr(edges, "shape") and len(edges.shape) == 2 \
         else len(edges)
-    layout = resolve_layout(layout, m_rows)
+    layout = resolve_layout(layout, m_rows, n)
     ctx.set_option(_lib.CC_OPT_STAGE_LAYOUT, 2 if layout == "chunk_sorted" else 0)
     lib = ctx.lib
     if hasattr(edges, "data_ptr") and getattr(edges, "is_cuda", False):
@@ -183,7 +189,7 @@ def stage_graph(ctx: _lib.Context, n: int, edges, layout: str = "auto") -> None:
         _lib.check(lib.cc_stage_edges(ctx.handle, ctypes.c_void_p(e.ctypes.data),
                                       e.dtype.itemsize, m, n))
     ctx.n, ctx.m = n, m
-    if layout in ("src_sorted", "dst_bucketed"):
+    if layout in ("src_sorted", "dst_bucketed", "l2_tiled"):
         _lib.check(lib.cc_reorder_edges(ctx.handle, LAYOUTS[layout]))
 
 

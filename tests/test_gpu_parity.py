@@ -405,6 +405,35 @@ def test_dst_bucketed_layout_exact(bshift, item_rows, threads):
     ctx.close()
 
 
+@pytest.mark.parametrize("tile_shift", [10, 14])
+def test_l2_tiled_layout_exact(tile_shift):
+    ctx = _lib.Context(0)
+    ctx.set_option(_lib.CC_OPT_TILE_SHIFT, tile_shift)
+    for n, e in (graphgen.rmat(16, 16, 6), graphgen.grid(400, 300, 0.55, 9),
+                 graphgen.forest(60, 7), spec.erdos_renyi(5000, 20001, 2)):
+        if (n + (1 << tile_shift) - 1) >> tile_shift > 1024:
+            continue
+        exp = oracle.rem_union_find(n, e)
+        engine.stage_graph(ctx, n, e, "l2_tiled")
+        for sched in (make_schedule("c2"), make_schedule("cm", 16), make_schedule("c2", sync=True)):
+            labels = np.empty(n, dtype=np.int64)
+            engine.run_staged(ctx, sched, labels_out=labels, count_changes=False,
+                              early_check=False)
+            assert np.array_equal(labels, exp), (n, sched)
+            assert engine.verify_staged(ctx) == 0
+    ctx.close()
+
+
+def test_verify_detects_bad_labels():
+    ctx = _lib.Context(0)
+    engine.stage_graph(ctx, 4, np.array([[0, 1], [2, 3]]))
+    engine.run_staged(ctx, make_schedule("c2"))
+    assert engine.verify_staged(ctx) == 0
+    _lib.check(ctx.lib.cc_init_labels(ctx.handle))  # identity labels: edges disagree
+    assert engine.verify_staged(ctx) & 1
+    ctx.close()
+
+
 def test_staged_chunk_sort_from_host_matches_device_reorder():
     n, e = graphgen.rmat(16, 16, 2, elem_bytes=4)
     exp = oracle.rem_union_find(n, e)

@@ -15,9 +15,12 @@ from paper_2311_02811_b200 import _lib, engine, graphgen  # noqa: E402
 from paper_2311_02811_b200.engine import make_schedule  # noqa: E402
 
 
-def prepare(cfg, layout, chunk, bshift=15, item_rows=1 << 18, bthreads=1024):
+def prepare(cfg, layout, chunk, bshift=15, item_rows=1 << 18, bthreads=1024, tshift=23,
+            tsplit=1):
     ctx = _lib.Context(0, torch.cuda.current_stream().cuda_stream)
     ctx.set_option(_lib.CC_OPT_SORT_CHUNK, chunk)
+    ctx.set_option(_lib.CC_OPT_TILE_SHIFT, tshift)
+    ctx.set_option(_lib.CC_OPT_TILE_SPLIT, tsplit)
     ctx.set_option(_lib.CC_OPT_BUCKET_SHIFT, bshift)
     ctx.set_option(_lib.CC_OPT_ITEM_ROWS, item_rows)
     ctx.set_option(_lib.CC_OPT_BUCKET_THREADS, bthreads)
@@ -37,14 +40,17 @@ def prepare(cfg, layout, chunk, bshift=15, item_rows=1 << 18, bthreads=1024):
     return ctx, min(ts)
 
 
-def measure(ctx, sched, **kw):
+def measure(ctx, sched, reps=3, **kw):
     for _ in range(2):
         engine.run_staged(ctx, sched, count_changes=False, sweep_times=False, **kw)
-    best = None
-    for _ in range(3):
+    best, runs = None, []
+    for _ in range(reps):
         _, st = engine.run_staged(ctx, sched, count_changes=False, **kw)
+        runs.append(st)
         if best is None or st.device_seconds < best.device_seconds:
             best = st
+    best.mean_ms = 1e3 * sum(s.device_seconds for s in runs) / len(runs)
+    best.sweep_hist = sorted(s.sweeps_executed for s in runs)
     return best
 
 
@@ -59,20 +65,32 @@ def main():
     ap.add_argument("--item-rows", type=int, default=1 << 18)
     ap.add_argument("--bthreads", type=int, default=1024)
     ap.add_argument("--no-fs", action="store_true")
+    ap.add_argument("--shortcut", default="0")
+    ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--tshift", type=int, default=23)
+    ap.add_argument("--tsplit", default="1")
     a = ap.parse_args()
     for cfg in a.configs:
-        for layout in a.layouts.split(","):
-            ctx, tr = prepare(cfg, layout, a.chunk, a.bshift, a.item_rows, a.bthreads)
+        for layout, tsplit in [(lay, int(t)) for lay in a.layouts.split(",")
+                               for t in a.tsplit.split(",")]:
+            ctx, tr = prepare(cfg, layout, a.chunk, a.bshift, a.item_rows, a.bthreads, a.tshift,
+                              tsplit)
+            print(f"# {cfg} layout={layout} tsplit={tsplit} tshift={a.tshift} chunk={a.chunk}",
+                  flush=True)
             for sm in map(int, a.stores.split(",")):
                 ctx.set_option(_lib.CC_OPT_STORE_MODE_ATOMIC if a.atomic else
                                _lib.CC_OPT_STORE_MODE_PLAIN, sm)
-                for fs in ((False,) if a.no_fs else (False, True)):
-                    st = measure(ctx, make_schedule("c2", atomic=bool(a.atomic)),
-                                 early_check=False, first_scatter=fs)
-                    print(f"{cfg:9s} layout={layout:12s} reorder={tr*1e3:6.2f}ms store={sm} "
-                          f"first_scatter={fs:d} total={st.device_seconds*1e3:8.3f}ms "
-                          f"sweeps={st.sweeps_executed} "
-                          f"sweep_ms={[round(t*1e3,3) for t in st.sweep_seconds]}", flush=True)
+                for sc in map(int, a.shortcut.split(",")):
+                    ctx.set_option(_lib.CC_OPT_SHORTCUT, sc)
+                    for fs in ((False,) if a.no_fs else (False, True)):
+                        st = measure(ctx, make_schedule("c2", atomic=bool(a.atomic)), a.reps,
+                                     early_check=False, first_scatter=fs)
+                        print(f"{cfg:9s} layout={layout:12s} reorder={tr*1e3:6.2f}ms store={sm} "
+                              f"shortcut={sc} first_scatter={fs:d} "
+                              f"best={st.device_seconds*1e3:8.3f}ms mean={st.mean_ms:8.3f}ms "
+                              f"sweeps={st.sweep_hist} "
+                              f"sweep_ms={[round(t*1e3,3) for t in st.sweep_seconds]}",
+                              flush=True)
             ctx.close()
 
 

@@ -34,13 +34,18 @@ def run(cfg, args):
     host = None
     if spec["kind"] == "rmat":
         n, m = graphgen.rmat_device(ctx, spec["scale"], spec["edgefactor"], 1)
-        _lib.check(ctx.lib.cc_reorder_edges(ctx.handle, engine.LAYOUTS["chunk_sorted"]))
+        lay = engine.resolve_layout(args.layout, m, n)
+        t1 = time.perf_counter()
+        _lib.check(ctx.lib.cc_reorder_edges(ctx.handle, engine.LAYOUTS[lay]))
     else:
         n, host = graphgen.make(spec, 1, elem_bytes=8)
         m = host.shape[0]
-        engine.stage_graph(ctx, n, host, "chunk_sorted")
+        lay = engine.resolve_layout(args.layout, m, n)
+        t1 = time.perf_counter()
+        engine.stage_graph(ctx, n, host, lay)
     torch.cuda.synchronize()
-    rec.update(n=int(n), m_input=int(m), prep_s=round(time.perf_counter() - t0, 2))
+    rec.update(n=int(n), m_input=int(m), layout=lay, layout_s=round(time.perf_counter() - t1, 3),
+               prep_s=round(time.perf_counter() - t0, 2))
     sched = make_schedule("c2")
     runs = []
     for _ in range(args.repeats):
@@ -89,6 +94,7 @@ def main():
     ap.add_argument("configs", nargs="+")
     ap.add_argument("--no-oracle", action="store_true")
     ap.add_argument("--repeats", type=int, default=3)
+    ap.add_argument("--layout", default="auto")
     args = ap.parse_args()
     for cfg in args.configs:
         run(cfg, args)
