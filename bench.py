@@ -68,6 +68,8 @@ def parse():
                    help="use the edge-sharded NCCL driver even with one rank (plumbing check)")
     p.add_argument("--cadence", type=int, default=1,
                    help="local sweeps per MIN exchange in the sharded driver")
+    p.add_argument("--clock-interval-ms", type=int, default=100,
+                   help="nvidia-smi sampling interval during the timed region")
     p.add_argument("--atomic", type=int, default=1,
                    help="Schedule.atomic (the reference default is True)")
     p.add_argument("--store-mode", type=int, default=None,
@@ -115,6 +117,8 @@ class ClockSampler:
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
+    interval_ms = 100
+
     def __init__(self, device: int):
         self.device = device
         self.proc = None
@@ -125,7 +129,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", str(self.interval_ms)],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -226,6 +230,7 @@ def load_traffic():
 
 def main():
     args = parse()
+    ClockSampler.interval_ms = max(20, args.clock_interval_ms)
     if args.impl == "reference":
         return run_reference_arm(args)
     rank, world, local = dist_env()

@@ -170,13 +170,17 @@ __global__ void k_stage(const T* __restrict__ aos, int64_t rows, int64_t n, lab_
     if (__syncthreads_or(bad) && threadIdx.x == 0) flags[kFlagBad] = 1;
 }
 
-// Layout 3 keys: (dst bucket << sbits) | src, sorted -> bucket-major, src-minor.
+// Layout 3 keys: ((dst bucket * runs + run) << sbits) | src, where run is
+// the row's original position in `runs` equal slices -> bucket-major, then
+// `runs` src-sorted runs per bucket.
 template <typename K>
 __global__ void k_make_keys(const lab_t* __restrict__ src, const lab_t* __restrict__ dst,
-                            int64_t m, int bshift, int sbits, K* keys) {
+                            int64_t m, int bshift, int sbits, int runs, K* keys) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m;
-         i += (int64_t)gridDim.x * blockDim.x)
-        keys[i] = ((K)(dst[i] >> bshift) << sbits) | (K)src[i];
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const K run = (K)((i * runs) / m);
+        keys[i] = (((K)(dst[i] >> bshift) * (K)runs + run) << sbits) | (K)src[i];
+    }
 }
 
 template <typename K>
@@ -189,10 +193,10 @@ __global__ void k_unkey(const K* __restrict__ keys, int64_t m, K mask, lab_t* sr
 // starts[b] = first row whose bucket >= b (lower bound on the sorted keys).
 template <typename K>
 __global__ void k_bucket_starts(const K* __restrict__ keys, int64_t m, int64_t nb, int sbits,
-                                int64_t* starts) {
+                                int runs, int64_t* starts) {
     for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nb;
          b += (int64_t)gridDim.x * blockDim.x) {
-        const K target = (K)b << sbits;
+        const K target = ((K)b * (K)runs) << sbits;
         int64_t lo = 0, hi = m;
         while (lo < hi) {
             const int64_t mid = (lo + hi) >> 1;
@@ -600,8 +604,8 @@ int launch_bucketed_u(cc_ctx* c, int sm, SweepLaunch sl) {
 
 // U = 4 rows per thread at up to 1024 threads, or 8 at up to 512.
 int launch_bucketed(cc_ctx* c, int sm, SweepLaunch sl) {
-    return c->bucket_threads > 512 ? launch_bucketed_u<4>(c, sm, sl)
-                                   : launch_bucketed_u<8>(c, sm, sl);
+    return c->bucket_threads > 512 ? launch_bucketed_u<1>(c, sm, sl)
+                                   : launch_bucketed_u<2>(c, sm, sl);
 }
 
 int launch_first(cc_ctx* c, lab_t* T) {
@@ -1304,7 +1308,7 @@ int cc_set_option(cc_ctx* c, int option, int64_t value) {
 namespace {
 
 template <typename K>
-int reorder_bucketed_t(cc_ctx* c, int sbits, int total_bits, int64_t nb) {
+int reorder_bucketed_t(cc_ctx* c, int sbits, int total_bits, int64_t nb, int runs) {
     const int64_t m = c->m;
     K *kin = nullptr, *kout = nullptr;
     lab_t* vout = nullptr;
@@ -1313,8 +1317,8 @@ int reorder_bucketed_t(cc_ctx* c, int sbits, int total_bits, int64_t nb) {
     CUDA_TRY(cudaMalloc(&kin, sizeof(K) * m));
     CUDA_TRY(cudaMalloc(&kout, sizeof(K) * m));
     CUDA_TRY(cudaMalloc(&vout, sizeof(lab_t) * m));
-    k_make_keys<K><<<grid_for(c, m, 16), kThreads, 0, c->stream>>>(c->src, c->dst, m,
-                                                                    c->bucket_shift, sbits, kin);
+    k_make_keys<K><<<grid_for(c, m, 16), kThreads, 0, c->stream>>>(
+        c->src, c->dst, m, c->bucket_shift, sbits, runs, kin);
     CUDA_TRY(cudaGetLastError());
     CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, tb, kin, kout, c->dst, vout, (int)m, 0,
                                              total_bits, c->stream));
@@ -1328,7 +1332,8 @@ int reorder_bucketed_t(cc_ctx* c, int sbits, int total_bits, int64_t nb) {
                              c->stream));
     int64_t* dstarts = nullptr;
     CUDA_TRY(cudaMalloc(&dstarts, sizeof(int64_t) * (nb + 1)));
-    k_bucket_starts<K><<<grid_for(c, nb), kThreads, 0, c->stream>>>(kout, m, nb, sbits, dstarts);
+    k_bucket_starts<K><<<grid_for(c, nb), kThreads, 0, c->stream>>>(kout, m, nb, sbits, runs,
+                                                                     dstarts);
     CUDA_TRY(cudaGetLastError());
     std::vector<int64_t> starts(nb + 1);
     CUDA_TRY(cudaMemcpyAsync(starts.data(), dstarts, sizeof(int64_t) * nb,
@@ -1340,20 +1345,35 @@ int reorder_bucketed_t(cc_ctx* c, int sbits, int total_bits, int64_t nb) {
     cudaFree(vout);
     cudaFree(tmp);
     cudaFree(dstarts);
-    // work items: each bucket's rows split into pieces of <= item_rows
-    std::vector<cck::BucketItem> items;
+    // work items: each bucket's (src-sorted) rows cut into `seg` equal
+    // segments, each segment into pieces of <= item_rows; ordered
+    // segment-major so the CTAs running at the same time cover the same src
+    // range of every bucket -- the whole GPU then walks the src range in
+    // increasing order, as the grid-stride sweep does on chunk-sorted rows
+    // (the order that propagates the smallest labels furthest per sweep).
+    struct Keyed {
+        int64_t seg, b;
+        cck::BucketItem it;
+    };
+    std::vector<Keyed> keyed;
     const int64_t B = (int64_t)1 << c->bucket_shift;
+    const int64_t seg = std::max(1, c->tile_split);
     for (int64_t b = 0; b < nb; ++b) {
         const uint32_t base = (uint32_t)(b * B);
         const uint32_t len = (uint32_t)std::min<int64_t>(B, c->n - b * B);
-        for (int64_t s = starts[b]; s < starts[b + 1]; s += c->item_rows)
-            items.push_back({s, std::min<int64_t>(s + c->item_rows, starts[b + 1]), base, len});
+        const int64_t rows = starts[b + 1] - starts[b];
+        for (int64_t s = 0; s < seg; ++s) {
+            const int64_t lo = starts[b] + rows * s / seg, hi = starts[b] + rows * (s + 1) / seg;
+            for (int64_t r = lo; r < hi; r += c->item_rows)
+                keyed.push_back({s, b, {r, std::min<int64_t>(r + c->item_rows, hi), base, len}});
+        }
     }
-    // largest items first so the static round-robin ends balanced
-    std::stable_sort(items.begin(), items.end(), [](const cck::BucketItem& a,
-                                                    const cck::BucketItem& b) {
-        return (a.end - a.start) > (b.end - b.start);
+    std::stable_sort(keyed.begin(), keyed.end(), [](const Keyed& a, const Keyed& b) {
+        return a.seg != b.seg ? a.seg < b.seg : a.b < b.b;
     });
+    std::vector<cck::BucketItem> items;
+    items.reserve(keyed.size());
+    for (auto& k : keyed) items.push_back(k.it);
     cudaFree(c->items);
     c->items = nullptr;
     c->n_items = (int)items.size();
@@ -1372,9 +1392,11 @@ int reorder_bucketed(cc_ctx* c) {
     const int sbits = std::max<int>(1, (int)ccgen::perm_bits((uint64_t)c->n));
     const int64_t B = (int64_t)1 << c->bucket_shift;
     const int64_t nb = (c->n + B - 1) / B;
-    const int bbits = std::max<int>(1, (int)ccgen::perm_bits((uint64_t)nb));
-    if (sbits + bbits <= 32) return reorder_bucketed_t<uint32_t>(c, sbits, sbits + bbits, nb);
-    return reorder_bucketed_t<unsigned long long>(c, sbits, sbits + bbits, nb);
+    const int runs = 1;  // key runs kept for experiments; segments order the items instead
+    const int bbits = std::max<int>(1, (int)ccgen::perm_bits((uint64_t)(nb * runs)));
+    if (sbits + bbits <= 32)
+        return reorder_bucketed_t<uint32_t>(c, sbits, sbits + bbits, nb, runs);
+    return reorder_bucketed_t<unsigned long long>(c, sbits, sbits + bbits, nb, runs);
 }
 
 // Layout 4: rows partitioned by dst into L2-window buckets of 2^tile_shift

@@ -224,89 +224,100 @@ __global__ void __launch_bounds__(kThreads) k_sweep(const lab_t* __restrict__ sr
 // Layout (cc_reorder_edges mode 3): rows grouped by dst bucket
 // [b*B, (b+1)*B) and sorted by src inside each bucket.  A work item is a
 // row range inside one bucket.  The CTA copies the bucket's B labels into
-// shared memory, so every L[dst] gather (the random one) becomes a shared-
-// memory load, and src-sorted rows make the L[src] gathers of a warp
-// coalesce.  Lowerings of cells inside the slice go to shared memory
-// (atomicMin) and are merged into global memory by red.min when the item
-// ends; other cells are lowered in global memory with store mode SM.
-// Reads of the slice may be stale w.r.t. other CTAs -- a legal asynchronous
-// interleaving, and a sweep that decides no lowering anywhere saw unchanged
-// labels everywhere, so the ballot/OR flag stays exact.
+// shared memory, so the random L[dst] gather becomes a shared-memory load
+// (no L1->L2 request), and src-sorted rows make the L[src] gathers of a warp
+// coalesce.  A lowering of the dst cell goes to shared memory (so later rows
+// of the item see it) AND through to global memory with store mode SM, so
+// other CTAs see it as early as with the plain kernel; every other cell is
+// read and lowered in global memory.  Slice reads may be stale w.r.t. other
+// CTAs -- a legal asynchronous interleaving; a sweep that decides no
+// lowering anywhere saw unchanged labels everywhere, so the ballot/OR flag
+// stays exact.
 struct BucketItem {
     int64_t start, end;  // row range
     uint32_t base, len;  // label slice [base, base+len)
 };
 
-// U rows per thread in flight; the next U rows' (src, dst) are prefetched
-// into registers while the current ones gather, hiding the HBM latency of
-// the edge stream behind the L2 latency of the label gathers.
-template <int SM, int U>
-__global__ void __launch_bounds__(U <= 4 ? 1024 : 512)
+template <int SM, int NE>
+__device__ __forceinline__ bool bucket_rows(lab_t* L, const lab_t* sl, lab_t base, lab_t len,
+                                            const lab_t (&u)[NE], const lab_t (&v)[NE]) {
+    lab_t lu[NE], lv[NE], zu[NE], zv[NE];
+#pragma unroll
+    for (int k = 0; k < NE; ++k) {
+        const bool live = u[k] != v[k];
+        lv[k] = live ? sl[v[k] - base] : v[k];
+        lu[k] = live ? L[u[k]] : u[k];
+    }
+#pragma unroll
+    for (int k = 0; k < NE; ++k) {
+        zu[k] = (lu[k] != u[k]) ? L[lu[k]] : lu[k];
+        zv[k] = (lv[k] != v[k]) ? ((lv[k] - base < len) ? sl[lv[k] - base] : L[lv[k]]) : lv[k];
+    }
+    bool wrote = false;
+#pragma unroll
+    for (int k = 0; k < NE; ++k) {
+        if (u[k] == v[k]) continue;
+        const lab_t z = min(zu[k], zv[k]);
+        if (lu[k] > z) { lower<SM, false>(L, u[k], z); wrote = true; }
+        if (lu[k] != u[k] && zu[k] > z) { lower<SM, true>(L, lu[k], z); wrote = true; }
+        if (lv[k] > z) {
+            atomicMin((lab_t*)sl + (v[k] - base), z);
+            lower<SM, false>(L, v[k], z);
+            wrote = true;
+        }
+        if (lv[k] != v[k] && zv[k] > z) {
+            if (lv[k] - base < len) atomicMin((lab_t*)sl + (lv[k] - base), z);
+            lower<SM, true>(L, lv[k], z);
+            wrote = true;
+        }
+    }
+    return wrote;
+}
+
+// NV uint4 vectors (4 rows each) per array per thread per iteration.
+template <int SM, int NV>
+__global__ void __launch_bounds__(1024)
     k_sweep_bucketed(const lab_t* __restrict__ src, const lab_t* __restrict__ dst, lab_t* L,
                      const BucketItem* __restrict__ items, int n_items, int* __restrict__ flag,
                      const int* __restrict__ d_order) {
     extern __shared__ lab_t sl[];
     if (d_order && *d_order != 2) return;
     bool wrote = false;
+    const int T = blockDim.x;
     for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
         const BucketItem w = items[it];
         const lab_t base = w.base, len = w.len;
-        for (lab_t i = threadIdx.x; i < len; i += blockDim.x) sl[i] = __ldcg(L + base + i);
+        for (lab_t i = threadIdx.x; i < len; i += T) sl[i] = __ldcg(L + base + i);
         __syncthreads();
-        auto rd = [&](lab_t x) -> lab_t { return (x - base < len) ? sl[x - base] : L[x]; };
-        auto low = [&](lab_t x, lab_t z, auto hot) {
-            if (x - base < len) atomicMin(sl + (x - base), z);
-            else lower<SM, decltype(hot)::value>(L, x, z);
-        };
-        const int64_t T = blockDim.x;
-        lab_t nu[U], nv[U];
-        auto fetch = [&](int64_t r0) {
-#pragma unroll
-            for (int j = 0; j < U; ++j) {
-                const int64_t r = r0 + j * T;
-                const bool in = r < w.end;
-                nu[j] = in ? __ldcs(src + r) : 0u;
-                nv[j] = in ? __ldcs(dst + r) : 0u;
-            }
-        };
-        fetch(w.start + threadIdx.x);
-        for (int64_t r0 = w.start + threadIdx.x; r0 < w.end; r0 += T * U) {
-            lab_t u[U], v[U], lu[U], lv[U], zu[U], zv[U];
-#pragma unroll
-            for (int j = 0; j < U; ++j) {
-                u[j] = nu[j];
-                v[j] = nv[j];
-            }
-            fetch(r0 + T * U);
-#pragma unroll
-            for (int j = 0; j < U; ++j) {
-                const bool live = u[j] != v[j];
-                lv[j] = live ? sl[v[j] - base] : v[j];
-                lu[j] = live ? rd(u[j]) : u[j];
-            }
-#pragma unroll
-            for (int j = 0; j < U; ++j) {
-                zu[j] = (lu[j] != u[j]) ? rd(lu[j]) : lu[j];
-                zv[j] = (lv[j] != v[j]) ? rd(lv[j]) : lv[j];
-            }
-#pragma unroll
-            for (int j = 0; j < U; ++j) {
-                if (u[j] == v[j]) continue;
-                const lab_t z = min(zu[j], zv[j]);
-                using F = std::integral_constant<bool, false>;
-                using H = std::integral_constant<bool, true>;
-                if (lu[j] > z) { low(u[j], z, F{}); wrote = true; }
-                if (lu[j] != u[j] && zu[j] > z) { low(lu[j], z, H{}); wrote = true; }
-                if (lv[j] > z) { atomicMin(sl + (v[j] - base), z); wrote = true; }
-                if (lv[j] != v[j] && zv[j] > z) { low(lv[j], z, H{}); wrote = true; }
-            }
+        // [start, a0) scalar head, [a0, a1) uint4 body, [a1, end) scalar tail
+        const int64_t a0 = min((w.start + 3) & ~(int64_t)3, w.end);
+        const int64_t a1 = max(a0, w.end & ~(int64_t)3);
+        for (int64_t r = w.start + threadIdx.x; r < a0; r += T) {
+            lab_t u[1] = {src[r]}, v[1] = {dst[r]};
+            wrote |= bucket_rows<SM, 1>(L, sl, base, len, u, v);
         }
-        __syncthreads();
-        for (lab_t i = threadIdx.x; i < len; i += blockDim.x) {
-            const lab_t s = sl[i];
-            if (s < __ldcg(L + base + i)) atomicMin(L + base + i, s);
+        const uint4* s4 = reinterpret_cast<const uint4*>(src + a0);
+        const uint4* d4 = reinterpret_cast<const uint4*>(dst + a0);
+        const int64_t nvec = (a1 - a0) >> 2;
+        for (int64_t q0 = threadIdx.x; q0 < nvec; q0 += (int64_t)T * NV) {
+            lab_t u[4 * NV], v[4 * NV];
+#pragma unroll
+            for (int q = 0; q < NV; ++q) {
+                const int64_t i = q0 + (int64_t)q * T;
+                uint4 a = make_uint4(0, 0, 0, 0), b = make_uint4(0, 0, 0, 0);
+                if (i < nvec) { a = __ldcs(s4 + i); b = __ldcs(d4 + i); }
+                u[4 * q + 0] = a.x; u[4 * q + 1] = a.y; u[4 * q + 2] = a.z; u[4 * q + 3] = a.w;
+                v[4 * q + 0] = b.x; v[4 * q + 1] = b.y; v[4 * q + 2] = b.z; v[4 * q + 3] = b.w;
+            }
+            // padding rows (i >= nvec) are u == v == 0: inert, and 0 is never
+            // read from the slice because live rows only are looked up
+            wrote |= bucket_rows<SM, 4 * NV>(L, sl, base, len, u, v);
         }
-        __syncthreads();
+        for (int64_t r = a1 + threadIdx.x; r < w.end; r += T) {
+            lab_t u[1] = {src[r]}, v[1] = {dst[r]};
+            wrote |= bucket_rows<SM, 1>(L, sl, base, len, u, v);
+        }
+        __syncthreads();  // the next item overwrites the slice
     }
     if (__syncthreads_or(wrote) && threadIdx.x == 0) *flag = 1;
 }
