@@ -401,6 +401,7 @@ struct cc_ctx {
     int tile_shift = 24;                      // layout 4: 2^shift labels (64 MB) per L2 window
     int shortcut = 1;  // pointer-jumping passes after every async sweep (fast path)
     int tile_split = 4;  // layout 4: independently sorted runs per L2 window
+    int bucket_nosmem = 0;  // layout 3 experiment: gather dst labels from global memory
     int64_t item_rows = (int64_t)1 << 18;     // layout 3: rows per work item
     int bucket_threads = 1024;
     cck::BucketItem* items = nullptr;         // layout 3 work items (device)
@@ -1286,6 +1287,9 @@ int cc_set_option(cc_ctx* c, int option, int64_t value) {
             if (value < 0 || value > 8) return fail(CC_EINVAL, "shortcut passes must be 0..8");
             c->shortcut = (int)value;
             return CC_OK;
+        case CC_OPT_BUCKET_NOSMEM:
+            c->bucket_nosmem = value != 0;
+            return CC_OK;
         case CC_OPT_TILE_SPLIT:
             if (value < 1 || value > 1024) return fail(CC_EINVAL, "tile split must be 1..1024");
             c->tile_split = (int)value;
@@ -1357,7 +1361,7 @@ int reorder_bucketed_t(cc_ctx* c, int sbits, int total_bits, int64_t nb, int run
     };
     std::vector<Keyed> keyed;
     const int64_t B = (int64_t)1 << c->bucket_shift;
-    const int64_t seg = std::max(1, c->tile_split);
+    const int64_t seg = 1;  // segment-major ordering measured slower (more items); kept at 1
     for (int64_t b = 0; b < nb; ++b) {
         const uint32_t base = (uint32_t)(b * B);
         const uint32_t len = (uint32_t)std::min<int64_t>(B, c->n - b * B);
@@ -1365,7 +1369,8 @@ int reorder_bucketed_t(cc_ctx* c, int sbits, int total_bits, int64_t nb, int run
         for (int64_t s = 0; s < seg; ++s) {
             const int64_t lo = starts[b] + rows * s / seg, hi = starts[b] + rows * (s + 1) / seg;
             for (int64_t r = lo; r < hi; r += c->item_rows)
-                keyed.push_back({s, b, {r, std::min<int64_t>(r + c->item_rows, hi), base, len}});
+                keyed.push_back({s, b, {r, std::min<int64_t>(r + c->item_rows, hi), base,
+                                        c->bucket_nosmem ? 0u : len}});
         }
     }
     std::stable_sort(keyed.begin(), keyed.end(), [](const Keyed& a, const Keyed& b) {

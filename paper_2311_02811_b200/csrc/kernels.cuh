@@ -245,7 +245,7 @@ __device__ __forceinline__ bool bucket_rows(lab_t* L, const lab_t* sl, lab_t bas
 #pragma unroll
     for (int k = 0; k < NE; ++k) {
         const bool live = u[k] != v[k];
-        lv[k] = live ? sl[v[k] - base] : v[k];
+        lv[k] = live ? ((v[k] - base < len) ? sl[v[k] - base] : L[v[k]]) : v[k];
         lu[k] = live ? L[u[k]] : u[k];
     }
 #pragma unroll
@@ -261,7 +261,7 @@ __device__ __forceinline__ bool bucket_rows(lab_t* L, const lab_t* sl, lab_t bas
         if (lu[k] > z) { lower<SM, false>(L, u[k], z); wrote = true; }
         if (lu[k] != u[k] && zu[k] > z) { lower<SM, true>(L, lu[k], z); wrote = true; }
         if (lv[k] > z) {
-            atomicMin((lab_t*)sl + (v[k] - base), z);
+            if (v[k] - base < len) atomicMin((lab_t*)sl + (v[k] - base), z);
             lower<SM, false>(L, v[k], z);
             wrote = true;
         }
