@@ -139,6 +139,8 @@ int cc_reorder_edges(cc_ctx* ctx, int mode);
                                       without exact counting (0..8, default 1) */
 #define CC_OPT_TILE_SPLIT 10       /* layout 4: independently src-sorted runs per window (default 4) */
 #define CC_OPT_BUCKET_NOSMEM 11    /* layout 3: 1 = gather dst labels from global memory (experiment) */
+#define CC_OPT_SWEEP_VARIANT 12    /* order-2 kernel: 0 8 rows/thread, 1 4 rows, 2 8 rows <=64 regs,
+                                      3 16 rows, 4 4 rows <=40 regs, 5 4 rows <=32 regs (default 1) */
 #define CC_OPT_STAGE_LAYOUT 4      /* layout applied while staging: 0 input order (default),
                                       2 chunk-sorted, each chunk sorted as soon as it lands,
                                       overlapped with the next chunk's host->device copy */

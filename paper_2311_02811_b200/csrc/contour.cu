@@ -402,6 +402,7 @@ struct cc_ctx {
     int shortcut = 1;  // pointer-jumping passes after every async sweep (fast path)
     int tile_split = 4;  // layout 4: independently sorted runs per L2 window
     int bucket_nosmem = 0;  // layout 3 experiment: gather dst labels from global memory
+    int sweep_variant = 1;  // order-2 kernel tuning variant (launch_o2): 4 rows/thread, 48 regs
     int64_t item_rows = (int64_t)1 << 18;     // layout 3: rows per work item
     int bucket_threads = 1024;
     cck::BucketItem* items = nullptr;         // layout 3 work items (device)
@@ -464,31 +465,47 @@ struct SweepLaunch {
     const int* d_order;
 };
 
-template <int OK, int SM, int NV>
+template <int OK, int SM, int NV, int MINB = 1>
 int launch_sweep_t(cc_ctx* c, const lab_t* R, lab_t* T, int order, SweepLaunch sl) {
     static int occ = 0;
     if (occ == 0) {
         int o = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, cck::k_sweep<OK, SM, NV>, kThreads, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, cck::k_sweep<OK, SM, NV, MINB>,
+                                                      kThreads, 0);
         occ = o > 0 ? o : 1;
     }
     const int64_t units = (c->m + 4 * NV - 1) / (4 * NV);
     const int blocks = grid_for(c, units, occ);
-    cck::k_sweep<OK, SM, NV><<<blocks, kThreads, 0, sl.stream>>>(
+    cck::k_sweep<OK, SM, NV, MINB><<<blocks, kThreads, 0, sl.stream>>>(
         c->src, c->dst, c->m, R, T, order, c->dflags + kFlagWrote, sl.d_order);
     CUDA_TRY(cudaGetLastError());
     return CC_OK;
 }
 
-template <int OK, int NV>
+template <int OK, int NV, int MINB = 1>
 int launch_store_mode(cc_ctx* c, const lab_t* R, lab_t* T, int order, int sm, SweepLaunch sl) {
     switch (sm) {
         case cck::kStorePlain:
-            return launch_sweep_t<OK, cck::kStorePlain, NV>(c, R, T, order, sl);
-        case cck::kStoreRed: return launch_sweep_t<OK, cck::kStoreRed, NV>(c, R, T, order, sl);
+            return launch_sweep_t<OK, cck::kStorePlain, NV, MINB>(c, R, T, order, sl);
+        case cck::kStoreRed:
+            return launch_sweep_t<OK, cck::kStoreRed, NV, MINB>(c, R, T, order, sl);
         case cck::kStoreCheckPlain:
-            return launch_sweep_t<OK, cck::kStoreCheckPlain, NV>(c, R, T, order, sl);
-        default: return launch_sweep_t<OK, cck::kStoreCheckRed, NV>(c, R, T, order, sl);
+            return launch_sweep_t<OK, cck::kStoreCheckPlain, NV, MINB>(c, R, T, order, sl);
+        default: return launch_sweep_t<OK, cck::kStoreCheckRed, NV, MINB>(c, R, T, order, sl);
+    }
+}
+
+// The order-2 sweep in one of its tuning variants (CC_OPT_SWEEP_VARIANT):
+// 0 = 8 rows/thread (default), 1 = 4 rows/thread, 2 = 8 rows/thread capped
+// at 64 registers (4 blocks/SM), 3 = 16 rows/thread.
+int launch_o2(cc_ctx* c, const lab_t* R, lab_t* T, int sm, SweepLaunch sl) {
+    switch (c->sweep_variant) {
+        case 1: return launch_store_mode<2, 1>(c, R, T, 2, sm, sl);
+        case 2: return launch_store_mode<2, 2, 4>(c, R, T, 2, sm, sl);
+        case 3: return launch_store_mode<2, 4>(c, R, T, 2, sm, sl);
+        case 4: return launch_store_mode<2, 1, 6>(c, R, T, 2, sm, sl);
+        case 5: return launch_store_mode<2, 1, 8>(c, R, T, 2, sm, sl);
+        default: return launch_store_mode<2, 2>(c, R, T, 2, sm, sl);
     }
 }
 
@@ -497,7 +514,7 @@ int launch_store_mode(cc_ctx* c, const lab_t* R, lab_t* T, int order, int sm, Sw
 int launch_order(cc_ctx* c, const lab_t* R, lab_t* T, int order, int sm) {
     const SweepLaunch sl{c->stream, nullptr};
     if (order == 1) return launch_store_mode<1, 2>(c, R, T, order, sm, sl);
-    if (order == 2) return launch_store_mode<2, 2>(c, R, T, order, sm, sl);
+    if (order == 2) return launch_o2(c, R, T, sm, sl);
     return launch_store_mode<0, 1>(c, R, T, order, sm, sl);
 }
 
@@ -729,7 +746,7 @@ int launch_guarded(cc_ctx* c, const cc_schedule* s, int sm, cudaStream_t st) {
     const SweepLaunch sl{st, &c->dstate->order};
     lab_t* L = c->labels;
     if (need2 && c->layout == 3 && c->items) CC_TRY(launch_bucketed(c, sm, sl));
-    else if (need2) CC_TRY((launch_store_mode<2, 2>(c, L, L, 2, sm, sl)));
+    else if (need2) CC_TRY(launch_o2(c, L, L, sm, sl));
     if (need1) CC_TRY((launch_store_mode<1, 2>(c, L, L, 1, sm, sl)));
     if (needh) CC_TRY((launch_store_mode<0, 1>(c, L, L, s->high_order, sm, sl)));
     return CC_OK;
@@ -1286,6 +1303,11 @@ int cc_set_option(cc_ctx* c, int option, int64_t value) {
         case CC_OPT_SHORTCUT:
             if (value < 0 || value > 8) return fail(CC_EINVAL, "shortcut passes must be 0..8");
             c->shortcut = (int)value;
+            return CC_OK;
+        case CC_OPT_SWEEP_VARIANT:
+            if (value < 0 || value > 5) return fail(CC_EINVAL, "sweep variant must be 0..5");
+            c->sweep_variant = (int)value;
+            c->loop_key.m = -1;
             return CC_OK;
         case CC_OPT_BUCKET_NOSMEM:
             c->bucket_nosmem = value != 0;

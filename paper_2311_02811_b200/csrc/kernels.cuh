@@ -185,8 +185,8 @@ __device__ __forceinline__ bool batch(const lab_t* R, lab_t* T, const lab_t (&u)
 // d_order != nullptr (graph-captured loop): the order of this sweep is read
 // from device memory and the launch is a no-op unless it matches OK, so a
 // captured body holds one launch per order kind the schedule can use.
-template <int OK, int SM, int NV>
-__global__ void __launch_bounds__(kThreads) k_sweep(const lab_t* __restrict__ src,
+template <int OK, int SM, int NV, int MINB = 1>
+__global__ void __launch_bounds__(kThreads, MINB) k_sweep(const lab_t* __restrict__ src,
                                                     const lab_t* __restrict__ dst, int64_t m,
                                                     const lab_t* R, lab_t* T, int order,
                                                     int* __restrict__ flag,
