@@ -184,6 +184,24 @@ int cc_gen_er_host(int64_t n, int64_t pairs, uint64_t seed, void* out, int elem_
 int cc_gen_forest_host(const int64_t* sizes, int64_t components, int64_t n, uint64_t seed,
                        void* out, int elem_bytes, int64_t* m_out, int threads);
 
+/* ---- ingestion: multi-threaded text parsers ----
+ * Line semantics of load_edge_list (graph.py:149-197, mode 0: '#'/'%'
+ * comments, exactly two integer tokens >= 0) and of the Matrix Market entry
+ * lines (graph.py:203-274, mode 1: '%' comments, >= 2 tokens, first two
+ * integers).  Rows go to out as int64 pairs in file order (out may be NULL
+ * to count); on a malformed line returns CC_EINVAL with *err_line (1-based),
+ * *err_code (CC_PARSE_*), *err_tokens (token count of that line) and
+ * err_vals[0..1] (its two integers).  mode 1 with bound != 0 also rejects
+ * entries outside 1..bound (CC_PARSE_RANGE; bound < 0 rejects every entry),
+ * in file order with the other errors. */
+#define CC_PARSE_TOKENS (-1)
+#define CC_PARSE_NONINT (-2)
+#define CC_PARSE_NEGATIVE (-3)
+#define CC_PARSE_RANGE (-4)
+int cc_parse_edges(const char* buf, int64_t len, int mode, int64_t* out, int64_t cap,
+                   int64_t* m_out, int64_t* err_line, int* err_code, int* err_tokens,
+                   int threads, int64_t bound, int64_t* err_vals);
+
 #ifdef __cplusplus
 }
 #endif

@@ -153,10 +153,72 @@ def configs():
     return out
 
 
+EDGE_LIST_CASES = [
+    ("0 1\n1 2\n", {}),
+    ("# comment\n% also\n\n3 1\n1 3\n5 5\n", {}),
+    ("# comment\n% also\n\n3 1\n1 3\n5 5\n", {"remap": False}),
+    ("# comment\n% also\n\n3 1\n1 3\n5 5\n", {"dedupe": False}),
+    ("4 2\n2 4\n0 9\n", {"dedupe": False, "remap": False}),
+    ("0 1 2\n", {}),
+    ("a b\n", {}),
+    ("-1 2\n", {}),
+    ("#c\n0 1\n\n1\n", {}),
+    ("0 1\n2 x\n3\n", {}),
+    ("1_0 2\n", {}),
+    ("+3 4\n", {}),
+    ("", {}),
+    ("# only comments\n\n% x\n", {}),
+    ("  7\t8  \r\n9 7\r\n", {}),
+    ("10 20\n20 30\n40 50\n", {}),
+]
+
+MTX_CASES = [
+    "%%MatrixMarket matrix coordinate pattern general\n% c\n4 4 3\n1 2\n2 3\n4 4\n",
+    "%%MatrixMarket matrix coordinate real symmetric\n3 3 3\n2 1 0.5\n3 1 1.5\n3 3 2\n",
+    "%%MatrixMarket matrix coordinate integer general\n3 3 4\n1 2 7\n2 1 7\n% mid\n\n3 2 1\n2 3 1\n",
+    "",
+    "%%MatrixMarket matrix coordinate pattern\n2 2 1\n1 2\n",
+    "%%MatrixMarket matrix array real general\n2 2 1\n1 2\n",
+    "%%MatrixMarket matrix coordinate complex general\n2 2 1\n1 2\n",
+    "%%MatrixMarket matrix coordinate real hermitian\n2 2 1\n1 2\n",
+    "%%MatrixMarket matrix coordinate pattern general\n2 3 1\n1 2\n",
+    "%%MatrixMarket matrix coordinate pattern general\n2 2\n1 2\n",
+    "%%MatrixMarket matrix coordinate pattern general\n2 2 x\n1 2\n",
+    "%%MatrixMarket matrix coordinate pattern general\n2 2 1\n1\n",
+    "%%MatrixMarket matrix coordinate pattern general\n2 2 1\n1 y\n",
+    "%%MatrixMarket matrix coordinate pattern general\n2 2 2\n1 2\n0 1\n",
+    "%%MatrixMarket matrix coordinate pattern general\n2 2 2\n1 2\n",
+    "%%MatrixMarket matrix coordinate pattern general\n% only comments\n",
+    "%%MatrixMarket matrix coordinate pattern general\n3 3 2\n1 3\n3 4\n",
+    "%%MatrixMarket matrix coordinate pattern general\n0 0 0\n",
+]
+
+
+def ingest_cases():
+    import io
+    out = []
+
+    def record(kind, text, kwargs, fn):
+        try:
+            g = fn()
+            res = {"n": g.n, "edges": g.edges.tolist(),
+                   "id_map": None if g.id_map is None else g.id_map.tolist()}
+        except Exception as exc:  # noqa: BLE001 - recording the reference's error
+            res = {"error": type(exc).__name__, "message": str(exc)}
+        out.append({"kind": kind, "text": text, "kwargs": kwargs, "result": res})
+
+    for text, kw in EDGE_LIST_CASES:
+        record("edgelist", text, kw, lambda: ref.load_edge_list(io.StringIO(text), **kw))
+    for text in MTX_CASES:
+        record("mtx", text, {}, lambda: ref.load_matrix_market(io.StringIO(text)))
+    return out
+
+
 def main():
     rng = np.random.default_rng(20261020)
     data = {"generator": "tests/golden/make_golden.py", "reference": "minmapcc " + ref.__version__,
-            "mm_order": mm_cases(rng), "graphs": small_graphs(rng), "configs": configs()}
+            "mm_order": mm_cases(rng), "graphs": small_graphs(rng), "configs": configs(),
+            "ingest": ingest_cases()}
     with open(os.path.join(HERE, "golden.json"), "w") as fh:
         json.dump(data, fh, separators=(",", ":"))
 
