@@ -64,6 +64,7 @@ def parse():
                    help="drive sweeps from the host instead of the CUDA-graph WHILE loop "
                         "(same kernels; ncu cannot see kernels inside conditional nodes)")
     p.add_argument("--no-e2e", action="store_true", help="skip the end-to-end leg")
+    p.add_argument("--no-fastsv", action="store_true", help="skip the GPU FastSV comparison")
     p.add_argument("--sharded", action="store_true",
                    help="use the edge-sharded NCCL driver even with one rank (plumbing check)")
     p.add_argument("--cadence", type=int, default=1,
@@ -310,6 +311,26 @@ def run_single(args, device):
     else:  # iota + loop_init + (sweep + control) per sweep + compress, all in one graph
         launches = sum(3 + 2 * s.sweeps_executed for s in stats)
 
+    # ---- the paper's comparison baseline on the same device and staged edges:
+    # GPU FastSV (baselines.py:81-131), not part of `value`
+    fsv = None
+    if not args.no_fastsv:
+        from paper_2311_02811_b200.baselines import fastsv_staged
+        fastsv_staged(ctx, sweep_times=False)
+        torch.cuda.synchronize()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        fst = None
+        for _ in range(args.steps):
+            _, fst = fastsv_staged(ctx, sweep_times=False)
+        f1.record(stream)
+        torch.cuda.synchronize()
+        fms = f0.elapsed_time(f1) / args.steps
+        fsv = {"value": m / (fms / 1e3), "unit": UNIT, "ms_per_step": fms,
+               "iterations": fst.sweeps_executed, "contour_speedup": fms / ms,
+               "what": "GPU FastSV (synchronous hooking + shortcutting, baselines.py:81-131) "
+                       "on the same staged edges; the paper's comparison baseline"}
+
     # ---- e2e through the C-ABI with HOST buffers (pinned), H2D + D2H timed
     need_host = not (args.no_e2e and args.no_cpu_baseline)
     if need_host and host_edges is None:
@@ -377,6 +398,7 @@ def run_single(args, device):
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": launches,
+        "fastsv_baseline": fsv,
         "clocks": clk,
     }
     print(json.dumps(line), flush=True)

@@ -184,6 +184,13 @@ int cc_gen_er_host(int64_t n, int64_t pairs, uint64_t seed, void* out, int elem_
 int cc_gen_forest_host(const int64_t* sizes, int64_t components, int64_t n, uint64_t seed,
                        void* out, int elem_bytes, int64_t* m_out, int threads);
 
+/* ---- FastSV baseline: fastsv(g) (baselines.py:81-131) on
+ * the staged edges.  Synchronous hooking + shortcutting with atomic-min
+ * proposals, so every iteration equals the reference's; stats as cc_run with
+ * converged_by = 2 ("grandparent-stable"); flags: CC_RUN_SWEEP_TIMES. */
+int cc_fastsv(cc_ctx* ctx, int64_t cap, void* labels_out, int out_elem_bytes, cc_stats* stats,
+              int flags);
+
 /* ---- ingestion: multi-threaded text parsers ----
  * Line semantics of load_edge_list (graph.py:149-197, mode 0: '#'/'%'
  * comments, exactly two integer tokens >= 0) and of the Matrix Market entry

@@ -87,6 +87,8 @@ SIGNATURES = {
                                       ctypes.c_void_p, ctypes.c_int, _I64P]),
     "cc_gen_forest_host": (ctypes.c_int, [_I64P, ctypes.c_int64, ctypes.c_int64, ctypes.c_uint64,
                                           ctypes.c_void_p, ctypes.c_int, _I64P, ctypes.c_int]),
+    "cc_fastsv": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int,
+                                 ctypes.POINTER(CCStats), ctypes.c_int]),
     "cc_parse_edges": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_int64, ctypes.c_int, _I64P,
                                       ctypes.c_int64, _I64P, _I64P, ctypes.POINTER(ctypes.c_int),
                                       ctypes.POINTER(ctypes.c_int), ctypes.c_int, ctypes.c_int64,

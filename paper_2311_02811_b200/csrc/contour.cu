@@ -254,6 +254,59 @@ __global__ void __launch_bounds__(kThreads) k_tile_scatter(const lab_t* __restri
     }
 }
 
+// ---- FastSV baseline (baselines.py:81-131) ------------
+// One synchronous iteration = hooking proposals from every edge into a copy
+// of the parent array by atomic min (order-independent, so per-iteration
+// results equal the reference's numpy np.minimum.at exactly), then
+// shortcutting against the grandparents.
+__global__ void __launch_bounds__(kThreads) k_fastsv_hook(const lab_t* __restrict__ src,
+                                                          const lab_t* __restrict__ dst,
+                                                          int64_t m, const lab_t* P,
+                                                          const lab_t* G, lab_t* N) {
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const lab_t w = __ldcs(src + e), v = __ldcs(dst + e);
+        const lab_t gw = G[w], gv = G[v], pw = P[w], pv = P[v];
+        // N starts as a copy of P and only decreases, so a proposal that is
+        // not below the target's P value is a no-op; G = P[P] gives P[pw] = gw
+        // and P[pv] = gv for free.  Skipping provable no-ops keeps the result
+        // (the min over all proposals) exact and keeps every edge from
+        // serialising on the hot root cells.
+        if (gv < gw) atomicMin(N + pw, gv);  // stochastic hooking (baselines.py:109-110)
+        if (gw < gv) atomicMin(N + pv, gw);
+        if (gv < pw) atomicMin(N + w, gv);   // aggressive hooking (baselines.py:111-112)
+        if (gw < pv) atomicMin(N + v, gw);
+    }
+}
+
+// N = min(N, G) (shortcutting, :113); count N != P (:114).
+__global__ void __launch_bounds__(kThreads) k_fastsv_shortcut(lab_t* N, const lab_t* G,
+                                                              const lab_t* P, int64_t n,
+                                                              unsigned long long* count) {
+    unsigned long long c = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const lab_t x = min(N[i], G[i]);
+        N[i] = x;
+        c += (x != P[i]);
+    }
+    c = block_sum(c);
+    if (threadIdx.x == 0 && c) atomicAdd(count, c);
+}
+
+// G2 = P[P] (:116); flag if G2 != G (:121).
+__global__ void __launch_bounds__(kThreads) k_fastsv_grand(const lab_t* P, const lab_t* G,
+                                                           lab_t* G2, int64_t n, int* flags) {
+    bool diff = false;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const lab_t g = P[P[i]];
+        G2[i] = g;
+        diff |= (g != G[i]);
+    }
+    if (__syncthreads_or(diff) && threadIdx.x == 0) flags[kFlagBad] = 1;
+}
+
 __global__ void k_widen(const lab_t* L, int64_t n, int64_t* out) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x)
@@ -1258,6 +1311,90 @@ int cc_run(cc_ctx* c, const cc_schedule* s, int flags, int64_t cap, void* labels
         st->sweeps_executed = sweep;
         st->sweeps_until_stable = until_stable;
         st->converged_by = converged_by;
+        st->compress_rounds = rounds;
+        st->converge_seconds = total_ms * 1e-3;
+    }
+    return copy_out(c, labels_out, out_eb);
+}
+
+// FastSV baseline (baselines.py:81-131) on the staged edges: synchronous
+// hooking + shortcutting until the grandparent array stops changing.
+// stats: changed_per_sweep = cells changed per iteration (exact, equal to the
+// reference's), converged_by = 2 ("grandparent-stable").
+int cc_fastsv(cc_ctx* c, int64_t cap, void* labels_out, int out_eb, cc_stats* st, int flags) {
+    if (!c) return fail(CC_EINVAL, "null context");
+    if (labels_out && out_eb != 4 && out_eb != 8)
+        return fail(CC_EINVAL, "label element size must be 4 or 8");
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard g(c->device);
+    const int64_t n = c->n;
+    const bool times = (flags & CC_RUN_SWEEP_TIMES) != 0;
+    CC_TRY(ensure_aux(c, true, false));
+    lab_t *G2 = nullptr, *N = nullptr;
+    CUDA_TRY(cudaMalloc(&G2, sizeof(lab_t) * (n + 1)));
+    CUDA_TRY(cudaMalloc(&N, sizeof(lab_t) * (n + 1)));
+    lab_t* const n_alloc = N;
+    lab_t* const g2_alloc = G2;
+    lab_t* P = c->labels;
+    lab_t* G = c->shadow;
+    CUDA_TRY(cudaEventRecord(c->evs, c->stream));
+    if (n > 0) {
+        k_iota<<<grid_for(c, n), kThreads, 0, c->stream>>>(P, n);
+        CUDA_TRY(cudaMemcpyAsync(G, P, sizeof(lab_t) * n, cudaMemcpyDeviceToDevice, c->stream));
+    }
+    int64_t it = 0, until = 0;
+    int rc = CC_OK;
+    while (true) {
+        ++it;
+        if (it > cap) {
+            rc = fail(CC_ECAP, "fastsv did not converge in %lld iterations", (long long)cap);
+            break;
+        }
+        if (times) CUDA_TRY(cudaEventRecord(c->ev0, c->stream));
+        CUDA_TRY(cudaMemsetAsync(c->dcount, 0, sizeof(unsigned long long), c->stream));
+        CUDA_TRY(cudaMemsetAsync(c->dflags + kFlagBad, 0, sizeof(int), c->stream));
+        if (n > 0) {
+            CUDA_TRY(cudaMemcpyAsync(N, P, sizeof(lab_t) * n, cudaMemcpyDeviceToDevice, c->stream));
+            if (c->m > 0)
+                k_fastsv_hook<<<grid_for(c, c->m, 16), kThreads, 0, c->stream>>>(c->src, c->dst,
+                                                                                 c->m, P, G, N);
+            k_fastsv_shortcut<<<grid_for(c, n), kThreads, 0, c->stream>>>(N, G, P, n, c->dcount);
+            std::swap(P, N);
+            k_fastsv_grand<<<grid_for(c, n), kThreads, 0, c->stream>>>(P, G, G2, n, c->dflags);
+            CUDA_TRY(cudaGetLastError());
+        }
+        if (times) CUDA_TRY(cudaEventRecord(c->ev1, c->stream));
+        CC_TRY(read_flags(c));
+        const int64_t changed = (int64_t)*c->hcount;
+        if (st && st->changed_per_sweep && it <= st->capacity) st->changed_per_sweep[it - 1] = changed;
+        if (st && st->sweep_seconds && it <= st->capacity) {
+            float ms = 0.f;
+            if (times) cudaEventElapsedTime(&ms, c->ev0, c->ev1);
+            st->sweep_seconds[it - 1] = ms * 1e-3;
+        }
+        if (changed) until = it;
+        if (!c->hflags[kFlagBad]) break;
+        std::swap(G, G2);
+    }
+    if (rc == CC_OK && n > 0 && P != c->labels)
+        CUDA_TRY(cudaMemcpyAsync(c->labels, P, sizeof(lab_t) * n, cudaMemcpyDeviceToDevice,
+                                 c->stream));
+    // the local pointers rotated; the two scratch allocations are freed by
+    // their original addresses (c->labels / c->shadow stay owned by the ctx)
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    cudaFree(n_alloc);
+    cudaFree(g2_alloc);
+    if (rc != CC_OK) return rc;
+    int rounds = 0;
+    CC_TRY(compress(c, &rounds));
+    CUDA_TRY(cudaEventRecord(c->eve, c->stream));
+    CUDA_TRY(cudaEventSynchronize(c->eve));
+    float total_ms = 0.f;
+    cudaEventElapsedTime(&total_ms, c->evs, c->eve);
+    if (st) {
+        st->sweeps_executed = it;
+        st->sweeps_until_stable = until;
+        st->converged_by = 2;
         st->compress_rounds = rounds;
         st->converge_seconds = total_ms * 1e-3;
     }

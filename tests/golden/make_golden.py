@@ -118,8 +118,10 @@ def small_graphs(rng):
                 lab, st = ref.run_contour(ns, ref.make_schedule(v, ho, sync=s), threads=1)
                 assert np.array_equal(lab, oracle)
                 runs[f"{v}|{'sync' if s else 'async'}|{ho}"] = stats_dict(st)
+        flab, fst = ref.fastsv(ns)
+        assert np.array_equal(flab, oracle)
         out.append({"name": name, "n": n, "edges": e.tolist(), "labels": oracle.tolist(),
-                    "runs": runs})
+                    "runs": runs, "fastsv": stats_dict(fst)})
     return out
 
 
@@ -144,10 +146,13 @@ def configs():
             lab, st = ref.run_contour(ns, ref.make_schedule(v, 1024, sync=s), threads=1)
             assert np.array_equal(lab, oracle)
             runs[f"{v}|{'sync' if s else 'async'}|1024"] = stats_dict(st)
+        flab, fst = ref.fastsv(ns)
+        assert np.array_equal(flab, oracle)
         out.append({"name": name, "params": params, "n": n, "m": int(e.shape[0]),
                     "edges_sha256": sha(e), "labels_sha256": sha(oracle),
                     "components": int(np.unique(oracle).size),
-                    "checksum": ref.label_checksum(oracle), "runs": runs})
+                    "checksum": ref.label_checksum(oracle), "runs": runs,
+                    "fastsv": stats_dict(fst)})
         print(name, n, e.shape[0], out[-1]["components"], runs["C-2|sync|1024"]["executed"],
               flush=True)
     return out

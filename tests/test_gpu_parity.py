@@ -434,6 +434,26 @@ def test_verify_detects_bad_labels():
     ctx.close()
 
 
+def test_fastsv_matches_reference_stats(golden):
+    """GPU FastSV (baselines.py:81-131): exact labels and the reference's
+    per-iteration counts (atomic-min hooking is order-independent)."""
+    from paper_2311_02811_b200.baselines import fastsv
+    for g in golden["graphs"]:
+        e = np.asarray(g["edges"], dtype=np.int64).reshape(-1, 2)
+        labels, st = fastsv((g["n"], e))
+        exp = g["fastsv"]
+        assert labels.tolist() == g["labels"], g["name"]
+        assert (st.sweeps_executed, st.sweeps_until_stable, st.changed_per_sweep) == \
+            (exp["executed"], exp["until_stable"], exp["changed"]), g["name"]
+        assert st.converged_by == exp["converged_by"] == "grandparent-stable"
+    for c in golden["configs"]:
+        n, e = _config_edges(c["params"])
+        labels, st = fastsv((n, e))
+        assert sha(labels) == c["labels_sha256"], c["name"]
+        assert (st.sweeps_executed, st.changed_per_sweep) == \
+            (c["fastsv"]["executed"], c["fastsv"]["changed"]), c["name"]
+
+
 def test_staged_chunk_sort_from_host_matches_device_reorder():
     n, e = graphgen.rmat(16, 16, 2, elem_bytes=4)
     exp = oracle.rem_union_find(n, e)
