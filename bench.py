@@ -69,6 +69,9 @@ def parse():
                    help="use the edge-sharded NCCL driver even with one rank (plumbing check)")
     p.add_argument("--cadence", type=int, default=1,
                    help="local sweeps per MIN exchange in the sharded driver")
+    p.add_argument("--exchange", default="peer", choices=["peer", "nccl"],
+                   help="multi-GPU label exchange: fused red.min into peer replicas (CUDA IPC) "
+                        "or an NCCL allreduce-min of the labels")
     p.add_argument("--clock-interval-ms", type=int, default=100,
                    help="nvidia-smi sampling interval during the timed region")
     p.add_argument("--atomic", type=int, default=1,
@@ -418,10 +421,20 @@ def run_multi(args, rank, world, device):
         raise SystemExit("multi-GPU bench supports the RMAT configs")
     stream = torch.cuda.Stream(device)
     torch.cuda.set_stream(stream)
-    runner = distributed.ShardedContour.from_rmat(spec["scale"], spec.get("edgefactor", 16),
-                                                  args.seed, rank, world, device,
-                                                  layout=args.layout, cadence=args.cadence,
-                                                  atomic=bool(args.atomic))
+    exchange = args.exchange
+    runner = None
+    if exchange == "peer":
+        try:  # fused sweep + red.min into the peers' replicas (CUDA IPC over NVLink)
+            runner = distributed.FusedShardedContour.from_rmat(
+                spec["scale"], spec.get("edgefactor", 16), args.seed, rank, world, device,
+                layout=args.layout, atomic=bool(args.atomic))
+        except RuntimeError as exc:  # no IPC peer mapping on this node: use NCCL, say so
+            exchange = f"nccl (peer IPC unavailable: {str(exc)[:80]})"
+    if runner is None:
+        runner = distributed.ShardedContour.from_rmat(spec["scale"], spec.get("edgefactor", 16),
+                                                      args.seed, rank, world, device,
+                                                      layout=args.layout, cadence=args.cadence,
+                                                      atomic=bool(args.atomic))
     n, m_total = runner.n, runner.m_total
     for _ in range(args.warmup):
         runner.run()
@@ -450,6 +463,16 @@ def run_multi(args, rank, world, device):
     bad = torch.tensor([engine.verify_staged(runner.shard.ctx)], dtype=torch.int32,
                        device="cuda")
     dist.all_reduce(bad, op=dist.ReduceOp.MAX)
+    fused = isinstance(runner, distributed.FusedShardedContour)
+    if fused:
+        sched = (f"C-2 async atomic={bool(args.atomic)}, fused sweep + red.min into the peer "
+                 f"replicas (CUDA IPC / NVLink), 1-word MAX all-reduce per round")
+        launches = sum(2 + r for r in rounds)  # init + fused sweep per round + compress
+    else:
+        sched = (f"C-2 async atomic={bool(args.atomic)}, NCCL allreduce-min every "
+                 f"{args.cadence} local sweep(s)")
+        # init + per sweep (sweep + fold + shortcut) + compress
+        launches = sum(2 + r * args.cadence * 3 for r in rounds)
     if rank == 0:
         line = {
             "metric": METRIC, "value": m_total / (ms / 1e3), "unit": UNIT, "n_gpus": world,
@@ -457,19 +480,19 @@ def run_multi(args, rank, world, device):
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32",
             "data": "synthetic",
             "config": {"workload": workload_name(args.config, n, m_total), "n": n,
-                       "m_input": m_total,
-                       "schedule": f"C-2 async atomic={bool(args.atomic)}, NCCL allreduce-min "
-                                   f"every {args.cadence} local sweep(s)",
+                       "m_input": m_total, "schedule": sched, "exchange": exchange,
                        "layout": runner.layout,
                        "parallelism": f"edge-sharded x{world}, labels replicated",
                        "l2": "inputs larger than L2"},
             "exchanges_per_run": rounds,
             "verified": int(bad.item()) == 0,
-            # init + per round (cadence x (sweep + fold)) + compress, per run
-            "gpu_launches": sum(2 + r * args.cadence * 2 for r in rounds),
+            "gpu_launches": launches,
             "clocks": clk,
         }
         print(json.dumps(line), flush=True)
+    if fused:
+        dist.barrier()
+        runner.shard.close()
     dist.destroy_process_group()
 
 

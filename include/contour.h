@@ -150,6 +150,9 @@ int cc_set_option(cc_ctx* ctx, int option, int64_t value);
  * labels[n] = min(labels[n], wrote ? 0 : 1).  Clears the flag. */
 int cc_fold_flag(cc_ctx* ctx, int first);
 int cc_compress(cc_ctx* ctx, int* rounds_out);
+/* `passes` pointer-jumping passes L[v] = L[L[v]] without reading back (the
+ * between-sweep shortcut of CC_OPT_SHORTCUT for drivers using cc_sweep). */
+int cc_shortcut(cc_ctx* ctx, int passes);
 /* early_convergence_check(g, labels) (engine.py:331-365) on device. */
 int cc_early_check(cc_ctx* ctx, int* ok_out);
 /* Size-independent certificate of the device labels: *result bit 0 = some
@@ -183,6 +186,20 @@ int cc_gen_er_host(int64_t n, int64_t pairs, uint64_t seed, void* out, int elem_
                    int64_t* m_out);
 int cc_gen_forest_host(const int64_t* sizes, int64_t components, int64_t n, uint64_t seed,
                        void* out, int elem_bytes, int64_t* m_out, int threads);
+
+/* ---- fused sweep + exchange for multi-GPU runs ----
+ * Instead of an allreduce-min of the n labels after every sweep, each
+ * order-2 sweep sends every lowering it makes, as red.global.min, to the
+ * label replicas of up to 7 peer GPUs (mapped with CUDA IPC, stores over
+ * NVLink).  After a host barrier all replicas hold the min over all ranks'
+ * lowerings; a round where no rank lowered anything is converged.
+ * cc_ipc_get_handle: 64-byte cudaIpcMemHandle_t of the context's own label
+ * buffer; cc_ipc_open/close: map/unmap a peer's handle; cc_set_peers: the
+ * peer label pointers (device addresses valid in this context). */
+int cc_ipc_get_handle(cc_ctx* ctx, void* handle_out);
+int cc_ipc_open(cc_ctx* ctx, const void* handle, uint64_t* ptr_out);
+int cc_ipc_close(cc_ctx* ctx, uint64_t ptr);
+int cc_set_peers(cc_ctx* ctx, const uint64_t* ptrs, int npeers);
 
 /* ---- FastSV baseline: fastsv(g) (baselines.py:81-131) on
  * the staged edges.  Synchronous hooking + shortcutting with atomic-min

@@ -65,6 +65,7 @@ SIGNATURES = {
     "cc_set_option": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int64]),
     "cc_fold_flag": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
     "cc_compress": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_int)]),
+    "cc_shortcut": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
     "cc_early_check": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_int)]),
     "cc_read_labels": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]),
     "cc_verify": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_int)]),
@@ -87,6 +88,12 @@ SIGNATURES = {
                                       ctypes.c_void_p, ctypes.c_int, _I64P]),
     "cc_gen_forest_host": (ctypes.c_int, [_I64P, ctypes.c_int64, ctypes.c_int64, ctypes.c_uint64,
                                           ctypes.c_void_p, ctypes.c_int, _I64P, ctypes.c_int]),
+    "cc_ipc_get_handle": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p]),
+    "cc_ipc_open": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p,
+                                   ctypes.POINTER(ctypes.c_uint64)]),
+    "cc_ipc_close": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_uint64]),
+    "cc_set_peers": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_uint64),
+                                    ctypes.c_int]),
     "cc_fastsv": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int,
                                  ctypes.POINTER(CCStats), ctypes.c_int]),
     "cc_parse_edges": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_int64, ctypes.c_int, _I64P,

@@ -456,6 +456,7 @@ struct cc_ctx {
     int tile_split = 4;  // layout 4: independently sorted runs per L2 window
     int bucket_nosmem = 0;  // layout 3 experiment: gather dst labels from global memory
     int sweep_variant = 1;  // order-2 kernel tuning variant (launch_o2): 4 rows/thread, 48 regs
+    cck::PeerSet peers = {};  // peer label replicas for the fused sweep + exchange
     int64_t item_rows = (int64_t)1 << 18;     // layout 3: rows per work item
     int bucket_threads = 1024;
     cck::BucketItem* items = nullptr;         // layout 3 work items (device)
@@ -551,7 +552,30 @@ int launch_store_mode(cc_ctx* c, const lab_t* R, lab_t* T, int order, int sm, Sw
 // The order-2 sweep in one of its tuning variants (CC_OPT_SWEEP_VARIANT):
 // 0 = 8 rows/thread (default), 1 = 4 rows/thread, 2 = 8 rows/thread capped
 // at 64 registers (4 blocks/SM), 3 = 16 rows/thread.
+template <int SM>
+int launch_o2_peers(cc_ctx* c, lab_t* L, SweepLaunch sl) {
+    static int occ = 0;
+    if (occ == 0) {
+        int o = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, cck::k_sweep_o2_peers<SM>, kThreads, 0);
+        occ = o > 0 ? o : 1;
+    }
+    const int blocks = grid_for(c, (c->m + 3) / 4, occ);
+    cck::k_sweep_o2_peers<SM><<<blocks, kThreads, 0, sl.stream>>>(c->src, c->dst, c->m, L,
+                                                                  c->peers, c->dflags + kFlagWrote);
+    CUDA_TRY(cudaGetLastError());
+    return CC_OK;
+}
+
 int launch_o2(cc_ctx* c, const lab_t* R, lab_t* T, int sm, SweepLaunch sl) {
+    if (c->peers.n > 0 && R == T && !sl.d_order) {  // fused sweep + peer exchange (async only)
+        switch (sm) {
+            case cck::kStorePlain: return launch_o2_peers<cck::kStorePlain>(c, T, sl);
+            case cck::kStoreRed: return launch_o2_peers<cck::kStoreRed>(c, T, sl);
+            case cck::kStoreCheckPlain: return launch_o2_peers<cck::kStoreCheckPlain>(c, T, sl);
+            default: return launch_o2_peers<cck::kStoreCheckRed>(c, T, sl);
+        }
+    }
     switch (c->sweep_variant) {
         case 1: return launch_store_mode<2, 1>(c, R, T, 2, sm, sl);
         case 2: return launch_store_mode<2, 2, 4>(c, R, T, 2, sm, sl);
@@ -1191,6 +1215,17 @@ int cc_fold_flag(cc_ctx* c, int first) {
     return CC_OK;
 }
 
+int cc_shortcut(cc_ctx* c, int passes) {
+    if (!c) return fail(CC_EINVAL, "null context");
+    if (passes < 0) return fail(CC_EINVAL, "passes must be >= 0");
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard g(c->device);
+    for (int j = 0; j < passes && c->n > 0; ++j)
+        k_compress<<<grid_for(c, c->n), kThreads, 0, c->stream>>>(c->labels, c->n, c->dflags);
+    CUDA_TRY(cudaGetLastError());
+    return CC_OK;
+}
+
 int cc_compress(cc_ctx* c, int* rounds) {
     if (!c) return fail(CC_EINVAL, "null context");
     std::lock_guard<std::mutex> lk(c->mu);
@@ -1264,7 +1299,8 @@ int cc_run(cc_ctx* c, const cc_schedule* s, int flags, int64_t cap, void* labels
     const bool check = (flags & CC_RUN_EARLY_CHECK) != 0;
     const bool times = (flags & CC_RUN_SWEEP_TIMES) != 0;
     const bool first_scatter = (flags & CC_RUN_FIRST_SCATTER) != 0;
-    if (!sync && !count && !check && !first_scatter && !(flags & CC_RUN_HOST_LOOP) && c->n > 0)
+    if (!sync && !count && !check && !first_scatter && !(flags & CC_RUN_HOST_LOOP) && c->n > 0 &&
+        c->peers.n == 0)
         return run_graph(c, s, cap, labels_out, out_eb, st);
     CUDA_TRY(cudaEventRecord(c->evs, c->stream));
     CC_TRY(enqueue_init(c, sync));
@@ -1315,6 +1351,47 @@ int cc_run(cc_ctx* c, const cc_schedule* s, int flags, int64_t cap, void* labels
         st->converge_seconds = total_ms * 1e-3;
     }
     return copy_out(c, labels_out, out_eb);
+}
+
+// ---- fused multi-GPU exchange: peer replicas over CUDA IPC -----------------
+int cc_ipc_get_handle(cc_ctx* c, void* handle_out) {
+    if (!c || !handle_out) return fail(CC_EINVAL, "null argument");
+    if (!c->own_labels || !c->labels)
+        return fail(CC_EINVAL, "IPC export needs the context's own label buffer");
+    DeviceGuard g(c->device);
+    cudaIpcMemHandle_t h;
+    CUDA_TRY(cudaIpcGetMemHandle(&h, c->labels));
+    memcpy(handle_out, &h, sizeof(h));
+    return CC_OK;
+}
+
+int cc_ipc_open(cc_ctx* c, const void* handle, uint64_t* ptr_out) {
+    if (!c || !handle || !ptr_out) return fail(CC_EINVAL, "null argument");
+    DeviceGuard g(c->device);
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle, sizeof(h));
+    void* p = nullptr;
+    CUDA_TRY(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+    *ptr_out = (uint64_t)(uintptr_t)p;
+    return CC_OK;
+}
+
+int cc_ipc_close(cc_ctx* c, uint64_t ptr) {
+    if (!c) return fail(CC_EINVAL, "null context");
+    DeviceGuard g(c->device);
+    CUDA_TRY(cudaIpcCloseMemHandle((void*)(uintptr_t)ptr));
+    return CC_OK;
+}
+
+int cc_set_peers(cc_ctx* c, const uint64_t* ptrs, int npeers) {
+    if (!c || (npeers > 0 && !ptrs)) return fail(CC_EINVAL, "null argument");
+    if (npeers < 0 || npeers > cck::kMaxPeers)
+        return fail(CC_EINVAL, "peer count must be 0..%d", cck::kMaxPeers);
+    std::lock_guard<std::mutex> lk(c->mu);
+    c->peers.n = npeers;
+    for (int i = 0; i < npeers; ++i) c->peers.p[i] = (lab_t*)(uintptr_t)ptrs[i];
+    c->loop_key.m = -1;
+    return CC_OK;
 }
 
 // FastSV baseline (baselines.py:81-131) on the staged edges: synchronous

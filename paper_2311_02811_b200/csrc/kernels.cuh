@@ -107,6 +107,64 @@ __device__ __forceinline__ bool batch_o2(const lab_t* R, lab_t* T, const lab_t (
     return wrote;
 }
 
+// ---- fused sweep + exchange (multi-GPU) ------------------------------------
+// Every lowering of the local replica is also sent, as a fire-and-forget
+// red.global.min, to the label replicas of the peer GPUs (their buffers
+// mapped into this process through CUDA IPC; stores to them travel over
+// NVLink / NVSwitch).  The exchange overlaps the sweep edge by edge and its
+// volume is the number of lowerings, not 4n bytes per sweep as with an
+// allreduce.  After a host barrier every replica holds the min over all
+// lowerings of all ranks, i.e. the replicas are identical again.
+constexpr int kMaxPeers = 7;
+struct PeerSet {
+    lab_t* p[kMaxPeers];
+    int n;
+};
+
+template <int SM, bool HOT>
+__device__ __forceinline__ void lower_bcast(lab_t* T, const PeerSet& ps, lab_t t, lab_t z) {
+    constexpr bool check = HOT && (SM == kStoreCheckPlain || SM == kStoreCheckRed);
+    // a local value already <= z came from a lowering that was broadcast too
+    if (check && __ldcg(T + t) <= z) return;
+    if (SM == kStoreRed || SM == kStoreCheckRed) atomicMin(T + t, z);
+    else T[t] = z;
+    for (int i = 0; i < ps.n; ++i) atomicMin(ps.p[i] + t, z);
+}
+
+template <int SM>
+__global__ void __launch_bounds__(kThreads) k_sweep_o2_peers(const lab_t* __restrict__ src,
+                                                             const lab_t* __restrict__ dst,
+                                                             int64_t m, lab_t* L, PeerSet ps,
+                                                             int* __restrict__ flag) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    bool wrote = false;
+    const int64_t nvec = m >> 2;
+    const uint4* __restrict__ s4 = reinterpret_cast<const uint4*>(src);
+    const uint4* __restrict__ d4 = reinterpret_cast<const uint4*>(dst);
+    auto edge = [&](lab_t u, lab_t v) {
+        if (u == v) return;
+        const lab_t lu = L[u], lv = L[v];
+        const lab_t zu = (lu != u) ? L[lu] : lu;
+        const lab_t zv = (lv != v) ? L[lv] : lv;
+        const lab_t z = min(zu, zv);
+        if (lu > z) { lower_bcast<SM, false>(L, ps, u, z); wrote = true; }
+        if (lu != u && zu > z) { lower_bcast<SM, true>(L, ps, lu, z); wrote = true; }
+        if (lv > z) { lower_bcast<SM, false>(L, ps, v, z); wrote = true; }
+        if (lv != v && zv > z) { lower_bcast<SM, true>(L, ps, lv, z); wrote = true; }
+    };
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nvec; i += stride) {
+        const uint4 a = __ldcs(s4 + i), b = __ldcs(d4 + i);
+        edge(a.x, b.x);
+        edge(a.y, b.y);
+        edge(a.z, b.z);
+        edge(a.w, b.w);
+    }
+    for (int64_t e = (nvec << 2) + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m;
+         e += stride)
+        edge(src[e], dst[e]);
+    if (__syncthreads_or(wrote) && threadIdx.x == 0) *flag = 1;
+}
+
 // ---- generic order h (C-m, C-11mm, C-1m1m high sweeps) --------------------
 // Walk both chains buffering up to kChainBuf (cell, value) pairs each, then
 // lower the buffered cells.  Cells beyond the buffer (chains longer than 16

@@ -49,10 +49,115 @@ class CudaShard:
     def fold(self, first: bool):
         _lib.check(self.ctx.lib.cc_fold_flag(self.ctx.handle, int(first)))
 
+    def shortcut(self, passes: int = 1):
+        # safe before the MIN exchange: a shortcut value is a valid label and
+        # the all-reduce makes the replicas identical again
+        _lib.check(self.ctx.lib.cc_shortcut(self.ctx.handle, passes))
+
     def compress(self) -> int:
         r = ctypes.c_int(0)
         _lib.check(self.ctx.lib.cc_compress(self.ctx.handle, ctypes.byref(r)))
         return r.value
+
+
+class PeerShard:
+    """A rank's shard whose order-2 sweeps write every lowering into all
+    replicas at once (fused sweep + exchange, `cc_set_peers`): the label
+    replicas of the other ranks are mapped through CUDA IPC, so no labels
+    are reduced between sweeps -- only a one-word "did anyone lower" flag.
+
+    Requires the context's own label buffer (not attached) and one process
+    per GPU of one node (or several processes sharing a GPU in tests)."""
+
+    def __init__(self, ctx: _lib.Context, n: int, atomic: bool = True, group=None):
+        import torch.distributed as dist
+        self.ctx = ctx
+        self.n = n
+        self.atomic = atomic
+        self.group = group
+        h = (ctypes.c_ubyte * 64)()
+        _lib.check(ctx.lib.cc_ipc_get_handle(ctx.handle, h))
+        handles = [None] * dist.get_world_size(group)
+        dist.all_gather_object(handles, bytes(h), group=group)
+        me = dist.get_rank(group)
+        self.peer_ptrs = []
+        for r, hb in enumerate(handles):
+            if r == me:
+                continue
+            ptr = ctypes.c_uint64(0)
+            buf = (ctypes.c_ubyte * 64).from_buffer_copy(hb)
+            _lib.check(ctx.lib.cc_ipc_open(ctx.handle, buf, ctypes.byref(ptr)))
+            self.peer_ptrs.append(ptr.value)
+        arr = (ctypes.c_uint64 * max(1, len(self.peer_ptrs)))(*self.peer_ptrs)
+        _lib.check(ctx.lib.cc_set_peers(ctx.handle, arr, len(self.peer_ptrs)))
+
+    def close(self):
+        _lib.check(self.ctx.lib.cc_set_peers(self.ctx.handle, None, 0))
+        for p in self.peer_ptrs:
+            self.ctx.lib.cc_ipc_close(self.ctx.handle, p)
+        self.peer_ptrs = []
+
+
+class FusedShardedContour:
+    """Per-rank driver of the fused exchange: init; barrier; then rounds of
+    one fused order-2 sweep + a MAX all-reduce of the local "wrote" bit until
+    no rank lowered anything (every replica then equals the min over all
+    lowerings of all ranks, and every shard is at a fixed point of it)."""
+
+    def __init__(self, shard: PeerShard, n: int, m_total: int, cap=None):
+        self.shard = shard
+        self.n = n
+        self.m_total = m_total
+        self.cap = n + 2 if cap is None else cap
+        self.layout = "input"
+
+    @classmethod
+    def from_rmat(cls, scale: int, edgefactor: int, seed: int, rank: int, world: int,
+                  device: int, layout: str = "auto", atomic: bool = True, group=None):
+        import torch
+
+        from .engine import LAYOUTS, resolve_layout
+        ctx = _lib.Context(device, torch.cuda.current_stream(device).cuda_stream)
+        n = 1 << scale
+        total = 2 * edgefactor * n
+        lo, hi = shard_rows(total, rank, world)
+        graphgen.rmat_device(ctx, scale, edgefactor, seed, row_lo=lo, row_hi=hi)
+        layout = resolve_layout(layout, hi - lo, n)
+        if LAYOUTS[layout]:
+            _lib.check(ctx.lib.cc_reorder_edges(ctx.handle, LAYOUTS[layout]))
+        runner = cls(PeerShard(ctx, n, atomic, group), n, total)
+        runner.layout = layout
+        return runner
+
+    def _flag_any(self, wrote: int) -> bool:
+        import torch
+        import torch.distributed as dist
+        dev = "cpu" if dist.get_backend(self.shard.group) == "gloo" else \
+            f"cuda:{self.shard.ctx.device}"
+        t = torch.tensor([wrote], dtype=torch.int32, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.shard.group)
+        return bool(t.item())
+
+    def run(self) -> int:
+        import torch.distributed as dist
+        ctx = self.shard.ctx
+        _lib.check(ctx.lib.cc_init_labels(ctx.handle))
+        _lib.check(ctx.lib.cc_synchronize(ctx.handle))
+        dist.barrier(group=self.shard.group)  # no peer lowers into a replica before its init
+        rounds = 0
+        while True:
+            rounds += 1
+            if rounds > self.cap:
+                from .errors import IterationCapExceeded
+                raise IterationCapExceeded(f"no convergence after {self.cap} sweeps")
+            wrote = ctypes.c_int(0)
+            _lib.check(ctx.lib.cc_sweep(ctx.handle, 2, 0, int(self.shard.atomic), 0,
+                                        ctypes.byref(wrote)))  # synchronises the device
+            if not self._flag_any(wrote.value):
+                break
+        r = ctypes.c_int(0)
+        _lib.check(ctx.lib.cc_compress(ctx.handle, ctypes.byref(r)))
+        return rounds
 
 
 def shard_rows(total: int, rank: int, world: int, align: int = 4) -> tuple[int, int]:
@@ -120,6 +225,8 @@ class ShardedContour:
                     raise IterationCapExceeded(f"no convergence after {self.cap} sweeps")
                 self.shard.sweep(self.order_for(sweep), first=(sweep == 1 and self.first_scatter))
                 self.shard.fold(first=(k == 0))
+                if hasattr(self.shard, "shortcut"):  # pointer jumping before the exchange
+                    self.shard.shortcut()
             self.allreduce(self.shard.labels)
             if int(self.shard.labels[self.n].item()) == 1:
                 break
