@@ -322,20 +322,17 @@ __global__ void k_from64(const int64_t* in, int64_t n, lab_t* L) {
 // Single-edge operator through the same device routines as the sweeps.
 __global__ void k_single_edge(const lab_t* R, lab_t* T, lab_t w, lab_t v, int order, int inplace,
                               int* changed) {
-    lab_t u1[1] = {w}, v1[1] = {v};
-    bool c;
+    constexpr int P = cck::kStorePlain, A = cck::kStoreRed;
     if (inplace) {
-        if (order == 1) c = cck::batch<1, 1, false>(T, T, u1, v1, order);
-        else if (order == 2) c = cck::batch<2, 1, false>(T, T, u1, v1, order);
-        else c = cck::batch<0, 1, false>(T, T, u1, v1, order);
+        bool c;
+        if (order == 1) c = cck::single_edge<1, P>(T, T, w, v, order);
+        else if (order == 2) c = cck::single_edge<2, P>(T, T, w, v, order);
+        else c = cck::single_edge<0, P>(T, T, w, v, order);
         *changed = c;
-    } else {
-        // sync form: lowering of a separate target; report whether it moved
-        lab_t before_w = T[w], before_v = T[v];
-        (void)before_w; (void)before_v;
-        if (order == 1) cck::batch<1, 1, true>(R, T, u1, v1, order);
-        else if (order == 2) cck::batch<2, 1, true>(R, T, u1, v1, order);
-        else cck::batch<0, 1, true>(R, T, u1, v1, order);
+    } else {  // sync form: atomic lowering of a separate target (host diffs it)
+        if (order == 1) cck::single_edge<1, A>(R, T, w, v, order);
+        else if (order == 2) cck::single_edge<2, A>(R, T, w, v, order);
+        else cck::single_edge<0, A>(R, T, w, v, order);
     }
 }
 
@@ -545,6 +542,8 @@ int launch_store_mode(cc_ctx* c, const lab_t* R, lab_t* T, int order, int sm, Sw
             return launch_sweep_t<OK, cck::kStoreRed, NV, MINB>(c, R, T, order, sl);
         case cck::kStoreCheckPlain:
             return launch_sweep_t<OK, cck::kStoreCheckPlain, NV, MINB>(c, R, T, order, sl);
+        case cck::kStoreCheckAllRed:
+            return launch_sweep_t<OK, cck::kStoreCheckAllRed, NV, MINB>(c, R, T, order, sl);
         default: return launch_sweep_t<OK, cck::kStoreCheckRed, NV, MINB>(c, R, T, order, sl);
     }
 }
@@ -728,7 +727,8 @@ int enqueue_sweep(cc_ctx* c, int order, int sync, int atomic, bool count_changes
         CC_TRY(ensure_aux(c, true, false));
         const lab_t* R = c->labels;
         lab_t* T = c->shadow;
-        int rc = first ? launch_first(c, T) : launch_order(c, R, T, order, cck::kStoreRed);
+        int rc = first ? launch_first(c, T)
+                       : launch_order(c, R, T, order, cck::kStoreCheckAllRed);
         if (rc) return rc;
         CUDA_TRY(cudaMemsetAsync(c->dflags + kFlagWrote, 0, sizeof(int), c->stream));
         k_commit<<<grid_for(c, c->n), kThreads, 0, c->stream>>>(c->labels, c->shadow, c->n,

@@ -36,15 +36,20 @@ constexpr int kChainBuf = 16;  // buffered chain cells per endpoint for order >=
 // Modes 2/3 trade one L2 load for skipping stores that a concurrent thread
 // already made redundant -- on hot cells those stores invalidate L1 lines
 // that every SM is reading.
-enum { kStorePlain = 0, kStoreRed = 1, kStoreCheckPlain = 2, kStoreCheckRed = 3 };
+//   4 re-check EVERY target cell, then red.min: synchronous sweeps, where the
+//     target is the shadow array that many edges lower at once (the result,
+//     the min over all proposals, is unchanged by skipping provable no-ops)
+enum { kStorePlain = 0, kStoreRed = 1, kStoreCheckPlain = 2, kStoreCheckRed = 3,
+       kStoreCheckAllRed = 4 };
 
 // HOT marks chain cells past the endpoint (L[w], L[v], ...): those are the
 // shared parents many edges lower at once; endpoint cells are random and
-// rarely contended, so the re-check modes only re-check HOT cells.
+// rarely contended, so the re-check modes 2/3 only re-check HOT cells.
 template <int SM, bool HOT>
 __device__ __forceinline__ void lower(lab_t* T, lab_t t, lab_t z) {
-    constexpr bool check = HOT && (SM == kStoreCheckPlain || SM == kStoreCheckRed);
-    constexpr bool red = SM == kStoreRed || SM == kStoreCheckRed;
+    constexpr bool check =
+        SM == kStoreCheckAllRed || (HOT && (SM == kStoreCheckPlain || SM == kStoreCheckRed));
+    constexpr bool red = SM == kStoreRed || SM == kStoreCheckRed || SM == kStoreCheckAllRed;
     if (check && __ldcg(T + t) <= z) return;
     if (red) {
         atomicMin(T + t, z);
@@ -225,15 +230,171 @@ __device__ __forceinline__ bool edge_oh(const lab_t* R, lab_t* T, lab_t w, lab_t
     return wrote;
 }
 
+// ---- generic order h, register chains (the bulk sweeps) --------------------
+// Same update as edge_oh, but the first kRegChain cells of each chain live in
+// registers (fully unrolled, no local memory) and the first hop of all NE
+// edges is loaded up front; chains that run longer (before a fixed point and
+// within `order` steps) are finished by walking/re-walking as in edge_oh.
+constexpr int kRegChain = 4;
+
+struct RegChain {
+    lab_t c[kRegChain], val[kRegChain];
+    int len;  // cells walked (may exceed kRegChain)
+    lab_t z;  // the order-fold value
+};
+
+__device__ __forceinline__ void walk_reg(const lab_t* R, lab_t x, lab_t lx, int order,
+                                         RegChain& ch) {
+    lab_t c = x, nxt = lx;
+    int j = 0;
+    bool done = false;
+#pragma unroll
+    for (int s = 0; s < kRegChain; ++s) {
+        if (!done) {
+            if (s > 0) nxt = R[c];
+            ch.c[s] = c;
+            ch.val[s] = nxt;
+            ++j;
+            if (nxt == c) {
+                done = true;
+            } else {
+                c = nxt;
+                if (j == order) done = true;
+            }
+        }
+    }
+    if (!done) {
+        for (;;) {
+            const lab_t n2 = R[c];
+            ++j;
+            if (n2 == c) break;
+            c = n2;
+            if (j == order) break;
+        }
+    }
+    ch.len = j;
+    ch.z = c;
+}
+
+template <int SM>
+__device__ __forceinline__ bool lower_reg(const lab_t* R, lab_t* T, const RegChain& ch, lab_t z) {
+    bool wrote = false;
+#pragma unroll
+    for (int s = 0; s < kRegChain; ++s) {
+        if (s < ch.len && ch.val[s] > z) {
+            if (s == 0) lower<SM, false>(T, ch.c[s], z);
+            else lower<SM, true>(T, ch.c[s], z);
+            wrote = true;
+        }
+    }
+    if (ch.len > kRegChain) {
+        lab_t x = ch.val[kRegChain - 1];
+        for (int j = kRegChain; j < ch.len; ++j) {
+            const lab_t nxt = R[x];
+            if (nxt > z) { lower<SM, true>(T, x, z); wrote = true; }
+            if (nxt == x) break;
+            x = nxt;
+        }
+    }
+    return wrote;
+}
+
+// Order >= 3.  The first three hops of every chain are loaded for all NE
+// edges at once (ILP 2*NE per hop, as in the order-2 batch); after a sweep or
+// two almost every chain reaches a fixed point within those hops (vertex ->
+// parent -> root), and such an edge is finished from registers.  Edges whose
+// chain is still moving after three hops (with order > 3) take the general
+// register-chain walk.
+template <int NE, int SM>
+__device__ __forceinline__ bool batch_oh(const lab_t* R, lab_t* T, const lab_t (&u)[NE],
+                                         const lab_t (&v)[NE], int order) {
+    lab_t lu[NE], lv[NE], zu[NE], zv[NE], gu[NE], gv[NE];
+#pragma unroll
+    for (int k = 0; k < NE; ++k) {
+        const bool live = u[k] != v[k];
+        lu[k] = live ? R[u[k]] : u[k];
+        lv[k] = live ? R[v[k]] : v[k];
+    }
+#pragma unroll
+    for (int k = 0; k < NE; ++k) {
+        zu[k] = (lu[k] != u[k]) ? R[lu[k]] : lu[k];
+        zv[k] = (lv[k] != v[k]) ? R[lv[k]] : lv[k];
+    }
+#pragma unroll
+    for (int k = 0; k < NE; ++k) {
+        gu[k] = (zu[k] != lu[k]) ? R[zu[k]] : zu[k];
+        gv[k] = (zv[k] != lv[k]) ? R[zv[k]] : zv[k];
+    }
+    bool wrote = false;
+#pragma unroll
+    for (int k = 0; k < NE; ++k) {
+        if (u[k] == v[k]) continue;
+        // chain ends within three cells: at a fixed point, or after exactly
+        // three steps when order == 3 (then the third successor is z)
+        const bool short_u = lu[k] == u[k] || zu[k] == lu[k] || gu[k] == zu[k] || order == 3;
+        const bool short_v = lv[k] == v[k] || zv[k] == lv[k] || gv[k] == zv[k] || order == 3;
+        if (short_u && short_v) {
+            const lab_t eu = lu[k] == u[k] ? u[k] : (zu[k] == lu[k] ? lu[k] : gu[k]);
+            const lab_t ev = lv[k] == v[k] ? v[k] : (zv[k] == lv[k] ? lv[k] : gv[k]);
+            const lab_t z = min(eu, ev);
+            if (lu[k] > z) { lower<SM, false>(T, u[k], z); wrote = true; }
+            if (lu[k] != u[k] && zu[k] > z) { lower<SM, true>(T, lu[k], z); wrote = true; }
+            if (lu[k] != u[k] && zu[k] != lu[k] && gu[k] > z) {
+                lower<SM, true>(T, zu[k], z);
+                wrote = true;
+            }
+            if (lv[k] > z) { lower<SM, false>(T, v[k], z); wrote = true; }
+            if (lv[k] != v[k] && zv[k] > z) { lower<SM, true>(T, lv[k], z); wrote = true; }
+            if (lv[k] != v[k] && zv[k] != lv[k] && gv[k] > z) {
+                lower<SM, true>(T, zv[k], z);
+                wrote = true;
+            }
+        } else {
+            RegChain cu, cv;
+            walk_reg(R, u[k], lu[k], order, cu);
+            walk_reg(R, v[k], lv[k], order, cv);
+            const lab_t z = min(cu.z, cv.z);
+            wrote |= lower_reg<SM>(R, T, cu, z);
+            wrote |= lower_reg<SM>(R, T, cv, z);
+        }
+    }
+    return wrote;
+}
+
 template <int OK, int NE, int SM>
 __device__ __forceinline__ bool batch(const lab_t* R, lab_t* T, const lab_t (&u)[NE],
                                       const lab_t (&v)[NE], int order) {
     if (OK == 1) return batch_o1<NE, SM>(R, T, u, v);
     if (OK == 2) return batch_o2<NE, SM>(R, T, u, v);
-    bool wrote = false;
+    if (SM == kStoreCheckAllRed) {
+        // synchronous sweeps (the only users of mode 4): labels do not move
+        // within the sweep, chains stay long, so walk each edge's chains
+        // directly instead of batching three hops first
+        bool wrote = false;
 #pragma unroll 1
-    for (int k = 0; k < NE; ++k) wrote |= edge_oh<SM>(R, T, u[k], v[k], order);
-    return wrote;
+        for (int k = 0; k < NE; ++k) {
+            if (u[k] == v[k]) continue;
+            RegChain cu, cv;
+            walk_reg(R, u[k], R[u[k]], order, cu);
+            walk_reg(R, v[k], R[v[k]], order, cv);
+            const lab_t z = min(cu.z, cv.z);
+            wrote |= lower_reg<SM>(R, T, cu, z);
+            wrote |= lower_reg<SM>(R, T, cv, z);
+        }
+        return wrote;
+    }
+    return batch_oh<NE, SM>(R, T, u, v, order);
+}
+
+// Exact single-edge form for cc_mm_order (16-cell buffers: every golden
+// chain is buffered before any store, as the reference does).
+template <int OK, int SM>
+__device__ __forceinline__ bool single_edge(const lab_t* R, lab_t* T, lab_t w, lab_t v,
+                                            int order) {
+    lab_t u1[1] = {w}, v1[1] = {v};
+    if (OK == 1) return batch_o1<1, SM>(R, T, u1, v1);
+    if (OK == 2) return batch_o2<1, SM>(R, T, u1, v1);
+    return edge_oh<SM>(R, T, w, v, order);
 }
 
 // One sweep over edges [0, m) of the SoA arrays (16-byte aligned).
