@@ -49,8 +49,10 @@ def parse():
     p.add_argument("--config", default="rmat22")
     p.add_argument("--impl", default="b200", choices=["b200", "reference"])
     p.add_argument("--no-cpu-baseline", action="store_true")
-    p.add_argument("--early-check", action="store_true",
-                   help="run the reference early check after each changing sweep")
+    p.add_argument("--no-early-check", dest="early_check", action="store_false",
+                   help="skip the reference's early convergence check after each changing "
+                        "sweep (engine.py:318-320; on by default, as in the reference) and "
+                        "stop on a no-write sweep only")
     p.add_argument("--seed", type=int, default=1)
     p.add_argument("--layout", default="auto",
                    choices=["auto", "input", "src_sorted", "chunk_sorted", "dst_bucketed",
@@ -303,16 +305,26 @@ def run_single(args, device):
     value = m / (ms / 1e3)
 
     sweeps = [s.sweeps_executed for s in stats]
-    sweep_s = [t for s in stats for t in s.sweep_seconds]
-    t_sweep = sum(sweep_s) / len(sweep_s)
+    shortcut = 1  # CC_OPT_SHORTCUT default: one pointer-jumping pass after every sweep
+    check = 2 if args.early_check else 0  # idempotence + edge-agreement kernels
+    if args.host_loop:  # iota + (sweep + shortcut + check) per sweep + compress
+        launches = sum(2 + s.sweeps_executed * (1 + shortcut + check) for s in stats)
+    else:  # iota + loop_init + (sweep + shortcut + check + control) per sweep + compress
+        launches = sum(3 + s.sweeps_executed * (2 + shortcut + check) for s in stats)
+
+    # ---- roofline of the sweep kernel: its own launch time, CUDA events on
+    # the launching stream around each sweep (+ its shortcut pass) in the
+    # host-driven loop -- the graph loop's per-sweep records include the check
+    rt = []
+    for _ in range(max(1, min(args.steps, 3))):
+        _, st = engine.run_staged(ctx, sched, sweep_times=True, count_changes=False,
+                                  early_check=args.early_check, host_loop=True)
+        rt.extend(st.sweep_seconds)
+    t_sweep = sum(rt) / len(rt)
     b_sweep = 8 * m + 4 * n  # edge stream + one label-array read
     achieved = b_sweep / t_sweep / 1e9
     peak, peak_src = peak_hbm()
     traffic = (load_traffic().get(args.config) or {}).get("dram_bytes_per_launch")
-    if args.host_loop:  # iota + sweeps + compress
-        launches = sum(1 + s.sweeps_executed + 1 for s in stats)
-    else:  # iota + loop_init + (sweep + control) per sweep + compress, all in one graph
-        launches = sum(3 + 2 * s.sweeps_executed for s in stats)
 
     # ---- the paper's comparison baseline on the same device and staged edges:
     # GPU FastSV (baselines.py:81-131), not part of `value`
@@ -395,7 +407,9 @@ def run_single(args, device):
         "reference_sweeps": ref_sweeps,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "kernel": "cck::k_sweep<2, 3, 2> (order-2 async sweep, check+red stores)",
+                     "kernel": "cck::k_sweep<2, 3, 1, 1> (order-2 async sweep, check+red stores, "
+                               "4 rows/thread) + one shortcut pass",
+                     "launch_ms": [round(t * 1e3, 4) for t in rt],
                      "bytes_per_launch": b_sweep, "avg_launch_s": t_sweep,
                      "peak_source": peak_src},
         "cpu_baseline": cpu,

@@ -140,8 +140,17 @@ int cc_reorder_edges(cc_ctx* ctx, int mode);
 #define CC_OPT_TILE_SPLIT 10       /* layout 4: independently src-sorted runs per window (default 4) */
 #define CC_OPT_BUCKET_NOSMEM 11    /* layout 3: 1 = gather dst labels from global memory (experiment) */
 #define CC_OPT_SWEEP_VARIANT 12    /* order-2 kernel: 0 8 rows/thread, 1 4 rows, 2 8 rows <=64 regs,
-                                      3 16 rows, 4 4 rows <=40 regs, 5 4 rows <=32 regs (default 1) */
-#define CC_OPT_STAGE_LAYOUT 4      /* layout applied while staging: 0 input order (default),
+                                      3 16 rows, 4 4 rows <=40 regs, 5 4 rows <=32 regs,
+                                      6 4 rows + evict-first src gathers, 7 = 6 + evict-last dst
+                                      gathers, 8 4 rows + evict-last dst gathers (default 1) */
+#define CC_OPT_BUCKET_PIPE 13      /* layout 3 sweep kernel: 0 general, 1 lean slice kernel
+                                      (default), 2 lean + edge prefetch, 3 bulk-copy (TMA)
+                                      pipelined, 3-stage ring */
+#define CC_OPT_ITEM_ORDER 14       /* layout 3: 0 bucket-major work items (default), 1 run-major:
+                                      rows cut into sort_chunk runs in input order, items ordered
+                                      (run, bucket) so the GPU walks each run's src range in order,
+                                      2 run-major with the items of a run staggered over src */
+#define CC_OPT_STAGE_LAYOUT 4     /* layout applied while staging: 0 input order (default),
                                       2 chunk-sorted, each chunk sorted as soon as it lands,
                                       overlapped with the next chunk's host->device copy */
 int cc_set_option(cc_ctx* ctx, int option, int64_t value);

@@ -22,6 +22,8 @@ CC_OPT_STORE_MODE_PLAIN, CC_OPT_STORE_MODE_ATOMIC, CC_OPT_SORT_CHUNK = 1, 2, 3
 CC_OPT_STAGE_LAYOUT, CC_OPT_BUCKET_SHIFT, CC_OPT_ITEM_ROWS, CC_OPT_BUCKET_THREADS = 4, 5, 6, 7
 CC_OPT_TILE_SHIFT, CC_OPT_SHORTCUT, CC_OPT_TILE_SPLIT, CC_OPT_BUCKET_NOSMEM = 8, 9, 10, 11
 CC_OPT_SWEEP_VARIANT = 12
+CC_OPT_BUCKET_PIPE = 13
+CC_OPT_ITEM_ORDER = 14
 STORE_PLAIN, STORE_RED, STORE_CHECK_PLAIN, STORE_CHECK_RED = 0, 1, 2, 3
 
 _I64P = ctypes.POINTER(ctypes.c_int64)

@@ -55,7 +55,9 @@ namespace {
 constexpr int kFlagWrote = 0;    // any lowering in the current sweep (ballot/OR)
 constexpr int kFlagBad = 1;      // early check / staging range violation
 constexpr int kFlagCompress = 2; // compress round changed something
-constexpr int kNumFlags = 4;
+constexpr int kFlagLe = 3;      // cc_verify: forest invariant violated
+constexpr int kFlagCheck = 4;   // device-side early check failed (graph loop)
+constexpr int kNumFlags = 5;
 
 __global__ void k_iota(lab_t* L, int64_t n) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
@@ -124,13 +126,57 @@ __global__ void k_check_edges(const lab_t* __restrict__ src, const lab_t* __rest
     if (__syncthreads_or(bad) && threadIdx.x == 0) flags[kFlagBad] = 1;
 }
 
+// The same check inside the graph loop (engine.py:318-320: run after every
+// sweep that changed something).  Both kernels return at once when the sweep
+// wrote nothing (the loop then stops on the change flag); the edge pass also
+// returns when idempotence already failed, and polls the failure word every
+// 16 iterations (one load per warp), so a failing check -- the common case
+// before convergence -- costs a small fraction of a pass.
+__global__ void __launch_bounds__(kThreads) k_gcheck_idem(const lab_t* __restrict__ L, int64_t n,
+                                                          int* flags) {
+    if (!*(volatile int*)&flags[kFlagWrote]) return;
+    bool bad = false;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const lab_t l = L[i];
+        bad |= (L[l] != l);
+    }
+    if (__syncthreads_or(bad) && threadIdx.x == 0) flags[kFlagCheck] = 1;
+}
+
+__global__ void __launch_bounds__(kThreads) k_gcheck_edges(const lab_t* __restrict__ src,
+                                                           const lab_t* __restrict__ dst,
+                                                           int64_t m, const lab_t* __restrict__ L,
+                                                           int* flags) {
+    volatile int* vf = flags;
+    if (!vf[kFlagWrote] || vf[kFlagCheck]) return;
+    const int64_t nvec = m >> 2;
+    const uint4* __restrict__ s4 = reinterpret_cast<const uint4*>(src);
+    const uint4* __restrict__ d4 = reinterpret_cast<const uint4*>(dst);
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    int it = 0;
+    for (int64_t i = tid; i < nvec; i += stride) {
+        if ((++it & 15) == 0 && vf[kFlagCheck]) return;
+        const uint4 a = __ldcs(s4 + i), b = __ldcs(d4 + i);
+        const bool bad = (L[a.x] != L[b.x]) | (L[a.y] != L[b.y]) | (L[a.z] != L[b.z]) |
+                         (L[a.w] != L[b.w]);
+        if (bad) {
+            vf[kFlagCheck] = 1;
+            return;
+        }
+    }
+    for (int64_t e = (nvec << 2) + tid; e < m; e += stride)
+        if (L[src[e]] != L[dst[e]]) vf[kFlagCheck] = 1;
+}
+
 // Forest invariant L[x] <= x -- part of cc_verify.
 __global__ void k_check_le(const lab_t* L, int64_t n, int* flags) {
     bool bad = false;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x)
         bad |= ((int64_t)L[i] > i);
-    if (__syncthreads_or(bad) && threadIdx.x == 0) flags[3] = 1;
+    if (__syncthreads_or(bad) && threadIdx.x == 0) flags[kFlagLe] = 1;
 }
 
 // Pointer-jumping compress L[v] = L[L[v]] (north-star step 4; the semantic
@@ -173,13 +219,17 @@ __global__ void k_stage(const T* __restrict__ aos, int64_t rows, int64_t n, lab_
 // Layout 3 keys: ((dst bucket * runs + run) << sbits) | src, where run is
 // the row's original position in `runs` equal slices -> bucket-major, then
 // `runs` src-sorted runs per bucket.
+// run_major: ((run * nb + dst bucket) << sbits) | src instead -> run-major.
 template <typename K>
 __global__ void k_make_keys(const lab_t* __restrict__ src, const lab_t* __restrict__ dst,
-                            int64_t m, int bshift, int sbits, int runs, K* keys) {
+                            int64_t m, int bshift, int sbits, int runs, int64_t nb,
+                            int run_major, K* keys) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m;
          i += (int64_t)gridDim.x * blockDim.x) {
         const K run = (K)((i * runs) / m);
-        keys[i] = (((K)(dst[i] >> bshift) * (K)runs + run) << sbits) | (K)src[i];
+        const K b = (K)(dst[i] >> bshift);
+        const K g = run_major ? run * (K)nb + b : b * (K)runs + run;
+        keys[i] = (g << sbits) | (K)src[i];
     }
 }
 
@@ -345,7 +395,7 @@ struct LoopState {
     int order;            // operator order of the next sweep
     int converged;        // last sweep lowered nothing
     int capped;           // sweep cap reached while still changing
-    int pad;
+    int by_check;         // stopped by the early check (not the change flag)
     unsigned long long t0;
 };
 struct SweepRec {
@@ -377,15 +427,20 @@ __global__ void k_loop_init(LoopState* st, int* flags, cc_schedule s) {
     st->order = order_for_dev(s, 1);
     st->converged = 0;
     st->capped = 0;
+    st->by_check = 0;
     flags[kFlagWrote] = 0;
+    flags[kFlagCheck] = 0;
     flags[kFlagCompress] = 0;
     st->t0 = globaltimer();
 }
 
 __global__ void k_loop_control(LoopState* st, SweepRec* rec, int* flags, cc_schedule s,
-                               long long cap, cudaGraphConditionalHandle h) {
+                               long long cap, int check, cudaGraphConditionalHandle h) {
     const int wrote = flags[kFlagWrote];
+    const int bad = flags[kFlagCheck];
     flags[kFlagWrote] = 0;
+    flags[kFlagCheck] = 0;
+    flags[kFlagCompress] = 0;  // only the post-loop compress pass reports to the host
     const long long k = ++st->sweep;
     if (k <= kMaxRec) {
         rec[k - 1].wrote = wrote;
@@ -393,6 +448,10 @@ __global__ void k_loop_control(LoopState* st, SweepRec* rec, int* flags, cc_sche
     }
     if (!wrote) {
         st->converged = 1;
+        cudaGraphSetConditional(h, 0);
+    } else if (check && !bad) {  // engine.py:318-320
+        st->converged = 1;
+        st->by_check = 1;
         cudaGraphSetConditional(h, 0);
     } else if (k >= cap) {
         st->capped = 1;
@@ -435,6 +494,8 @@ struct cc_ctx {
     lab_t* labels = nullptr;  // n + 1
     int64_t label_cap = 0;
     bool own_labels = false;
+    int64_t* wide = nullptr;  // cached int64 label buffer for copy_out
+    int64_t wide_cap = 0;
     lab_t* shadow = nullptr;
     lab_t* before = nullptr;
     int64_t aux_cap = 0;
@@ -456,6 +517,8 @@ struct cc_ctx {
     cck::PeerSet peers = {};  // peer label replicas for the fused sweep + exchange
     int64_t item_rows = (int64_t)1 << 18;     // layout 3: rows per work item
     int bucket_threads = 1024;
+    int bucket_pipe = 1;  // layout 3 kernel (launch_bucketed)
+    int item_order = 0;   // layout 3: 0 bucket-major items, 1 run-major (see reorder_bucketed)
     cck::BucketItem* items = nullptr;         // layout 3 work items (device)
     int n_items = 0;
     int stage_layout = 0;                     // layout applied by cc_stage_edges*
@@ -482,6 +545,9 @@ struct cc_ctx {
         int sm;
         int shortcut;
         int layout;
+        int check;
+        const void* items;
+        int n_items;
     } loop_key = {};
     std::mutex mu;
 };
@@ -533,18 +599,20 @@ int launch_sweep_t(cc_ctx* c, const lab_t* R, lab_t* T, int order, SweepLaunch s
     return CC_OK;
 }
 
-template <int OK, int NV, int MINB = 1>
+// H: cck::kHint* cache-hint bits (order 2 only).
+template <int OK, int NV, int MINB = 1, int H = 0>
 int launch_store_mode(cc_ctx* c, const lab_t* R, lab_t* T, int order, int sm, SweepLaunch sl) {
     switch (sm) {
         case cck::kStorePlain:
-            return launch_sweep_t<OK, cck::kStorePlain, NV, MINB>(c, R, T, order, sl);
+            return launch_sweep_t<OK, cck::kStorePlain | H, NV, MINB>(c, R, T, order, sl);
         case cck::kStoreRed:
-            return launch_sweep_t<OK, cck::kStoreRed, NV, MINB>(c, R, T, order, sl);
+            return launch_sweep_t<OK, cck::kStoreRed | H, NV, MINB>(c, R, T, order, sl);
         case cck::kStoreCheckPlain:
-            return launch_sweep_t<OK, cck::kStoreCheckPlain, NV, MINB>(c, R, T, order, sl);
+            return launch_sweep_t<OK, cck::kStoreCheckPlain | H, NV, MINB>(c, R, T, order, sl);
         case cck::kStoreCheckAllRed:
-            return launch_sweep_t<OK, cck::kStoreCheckAllRed, NV, MINB>(c, R, T, order, sl);
-        default: return launch_sweep_t<OK, cck::kStoreCheckRed, NV, MINB>(c, R, T, order, sl);
+            return launch_sweep_t<OK, cck::kStoreCheckAllRed | H, NV, MINB>(c, R, T, order, sl);
+        default:
+            return launch_sweep_t<OK, cck::kStoreCheckRed | H, NV, MINB>(c, R, T, order, sl);
     }
 }
 
@@ -581,6 +649,19 @@ int launch_o2(cc_ctx* c, const lab_t* R, lab_t* T, int sm, SweepLaunch sl) {
         case 3: return launch_store_mode<2, 4>(c, R, T, 2, sm, sl);
         case 4: return launch_store_mode<2, 1, 6>(c, R, T, 2, sm, sl);
         case 5: return launch_store_mode<2, 1, 8>(c, R, T, 2, sm, sl);
+        case 6: return launch_store_mode<2, 1, 1, cck::kHintSrcStream>(c, R, T, 2, sm, sl);
+        case 7:
+            return launch_store_mode<2, 1, 1, cck::kHintSrcStream | cck::kHintDstKeep>(c, R, T,
+                                                                                       2, sm, sl);
+        case 8: return launch_store_mode<2, 1, 1, cck::kHintDstKeep>(c, R, T, 2, sm, sl);
+        case 9: return launch_store_mode<2, 1, 1, cck::kHintEdgeFirst>(c, R, T, 2, sm, sl);
+        case 10:
+            return launch_store_mode<2, 1, 1,
+                                     cck::kHintEdgeFirst | cck::kHintDstKeep | cck::kHintSrcKeep>(
+                c, R, T, 2, sm, sl);
+        case 11:
+            return launch_store_mode<2, 1, 1, cck::kHintEdgeFirst | cck::kHintDstKeep>(c, R, T, 2,
+                                                                                       sm, sl);
         default: return launch_store_mode<2, 2>(c, R, T, 2, sm, sl);
     }
 }
@@ -640,7 +721,9 @@ int set_graph(cc_ctx* c, int64_t m, int64_t n) {
     c->m = m;
     c->layout = 0;  // a new edge set: any bucketed work items are stale
     c->n_items = 0;
-    c->loop_key.m = -1;
+    // the captured loop stays valid: its key (build_loop) holds every value
+    // the capture baked in, so restaging a same-shaped graph into the same
+    // buffers (the end-to-end path) reuses it
     return ensure_labels(c);
 }
 
@@ -696,8 +779,85 @@ int launch_bucketed_u(cc_ctx* c, int sm, SweepLaunch sl) {
     }
 }
 
+int launch_check_slice(cc_ctx* c, cudaStream_t st) {
+    const size_t smem = sizeof(lab_t) * ((size_t)1 << c->bucket_shift);
+    static size_t smem_set = 0;
+    if (smem_set != smem) {
+        CUDA_TRY(cudaFuncSetAttribute(cck::k_check_slice,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        smem_set = smem;
+    }
+    const int blocks = (int)std::min<int64_t>(c->n_items, (int64_t)c->sm_count);
+    cck::k_check_slice<<<std::max(blocks, 1), cck::kBT, smem, st>>>(
+        c->src, c->dst, c->labels, c->items, c->n_items, c->dflags, kFlagWrote, kFlagCheck);
+    CUDA_TRY(cudaGetLastError());
+    return CC_OK;
+}
+
+template <int SM, int NS>
+int launch_bucketed_pipe_t(cc_ctx* c, SweepLaunch sl) {
+    const size_t smem = sizeof(lab_t) * ((size_t)NS * 2 * cck::kStageRows +
+                                         ((size_t)1 << c->bucket_shift));
+    static size_t smem_set = 0;
+    if (smem_set != smem) {
+        CUDA_TRY(cudaFuncSetAttribute(cck::k_sweep_bucketed_tma<SM, NS>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        smem_set = smem;
+    }
+    const int blocks = (int)std::min<int64_t>(c->n_items, (int64_t)c->sm_count);
+    cck::k_sweep_bucketed_tma<SM, NS><<<std::max(blocks, 1), cck::kBT, smem, sl.stream>>>(
+        c->src, c->dst, c->labels, c->items, c->n_items, c->dflags + kFlagWrote, sl.d_order);
+    CUDA_TRY(cudaGetLastError());
+    return CC_OK;
+}
+
+template <int NS>
+int launch_bucketed_pipe(cc_ctx* c, int sm, SweepLaunch sl) {
+    switch (sm) {
+        case cck::kStorePlain: return launch_bucketed_pipe_t<cck::kStorePlain, NS>(c, sl);
+        case cck::kStoreRed: return launch_bucketed_pipe_t<cck::kStoreRed, NS>(c, sl);
+        case cck::kStoreCheckPlain: return launch_bucketed_pipe_t<cck::kStoreCheckPlain, NS>(c, sl);
+        default: return launch_bucketed_pipe_t<cck::kStoreCheckRed, NS>(c, sl);
+    }
+}
+
+// PF: 0 lean, 1 lean + edge prefetch
+template <int SM, int PF>
+int launch_slice_t(cc_ctx* c, SweepLaunch sl) {
+    const size_t smem = sizeof(lab_t) * ((size_t)1 << c->bucket_shift);
+    auto kern = cck::k_sweep_slice<SM, PF == 1>;
+    static size_t smem_set = 0;
+    if (smem_set != smem) {
+        CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)smem));
+        smem_set = smem;
+    }
+    const int blocks = (int)std::min<int64_t>(c->n_items, (int64_t)c->sm_count);
+    kern<<<std::max(blocks, 1), cck::kBT, smem, sl.stream>>>(
+        c->src, c->dst, c->labels, c->items, c->n_items, c->dflags + kFlagWrote, sl.d_order);
+    CUDA_TRY(cudaGetLastError());
+    return CC_OK;
+}
+
+template <int PF>
+int launch_slice(cc_ctx* c, int sm, SweepLaunch sl) {
+    switch (sm) {
+        case cck::kStorePlain: return launch_slice_t<cck::kStorePlain, PF>(c, sl);
+        case cck::kStoreRed: return launch_slice_t<cck::kStoreRed, PF>(c, sl);
+        case cck::kStoreCheckPlain: return launch_slice_t<cck::kStoreCheckPlain, PF>(c, sl);
+        default: return launch_slice_t<cck::kStoreCheckRed, PF>(c, sl);
+    }
+}
+
+// bucket_pipe (CC_OPT_BUCKET_PIPE): 1 lean slice kernel, 2 lean + edge
+// prefetch, 3 bulk-copy pipelined kernel; 0 the general kernel with
 // U = 4 rows per thread at up to 1024 threads, or 8 at up to 512.
 int launch_bucketed(cc_ctx* c, int sm, SweepLaunch sl) {
+    if (c->bucket_pipe > 0 && !c->bucket_nosmem) {
+        if (c->bucket_pipe == 1) return launch_slice<0>(c, sm, sl);
+        if (c->bucket_pipe == 2) return launch_slice<1>(c, sm, sl);
+        return launch_bucketed_pipe<3>(c, sm, sl);
+    }
     return c->bucket_threads > 512 ? launch_bucketed_u<1>(c, sm, sl)
                                    : launch_bucketed_u<2>(c, sm, sl);
 }
@@ -836,11 +996,12 @@ bool same_schedule(const cc_schedule& a, const cc_schedule& b) {
 
 // Capture iota -> loop_init -> WHILE{ guarded sweeps -> loop_control } -> compress
 // into one executable graph.
-int build_loop(cc_ctx* c, const cc_schedule* s, int64_t cap, int sm) {
+int build_loop(cc_ctx* c, const cc_schedule* s, int64_t cap, int sm, int check) {
     auto& k = c->loop_key;
     if (c->loop_exec && k.src == c->src && k.dst == c->dst && k.labels == c->labels &&
         k.m == c->m && k.n == c->n && k.cap == cap && same_schedule(k.s, *s) && k.sm == sm &&
-        k.shortcut == c->shortcut && k.layout == c->layout)
+        k.shortcut == c->shortcut && k.layout == c->layout && k.check == check &&
+        k.items == c->items && k.n_items == c->n_items)
         return CC_OK;
     if (c->loop_exec) cudaGraphExecDestroy(c->loop_exec);
     if (c->loop_graph) cudaGraphDestroy(c->loop_graph);
@@ -877,14 +1038,25 @@ int build_loop(cc_ctx* c, const cc_schedule* s, int64_t cap, int sm) {
     CC_TRY(launch_guarded(c, s, sm, c->body_stream));
     for (int j = 0; j < c->shortcut; ++j)
         k_compress<<<grid_for(c, c->n), kThreads, 0, c->body_stream>>>(c->labels, c->n, c->dflags);
-    k_loop_control<<<1, 1, 0, c->body_stream>>>(c->dstate, c->drec, c->dflags, *s, cap, h);
+    if (check) {
+        k_gcheck_idem<<<grid_for(c, c->n), kThreads, 0, c->body_stream>>>(c->labels, c->n,
+                                                                          c->dflags);
+        if (c->m > 0 && c->layout == 3 && c->items && !c->bucket_nosmem)
+            CC_TRY(launch_check_slice(c, c->body_stream));
+        else if (c->m > 0)
+            k_gcheck_edges<<<grid_for(c, (c->m + 3) / 4), kThreads, 0, c->body_stream>>>(
+                c->src, c->dst, c->m, c->labels, c->dflags);
+    }
+    k_loop_control<<<1, 1, 0, c->body_stream>>>(c->dstate, c->drec, c->dflags, *s, cap, check,
+                                                h);
     CUDA_TRY(cudaGetLastError());
     cudaGraph_t body_out = nullptr;
     CUDA_TRY(cudaStreamEndCapture(c->body_stream, &body_out));
     k_compress<<<grid_for(c, c->n), kThreads, 0, cs>>>(c->labels, c->n, c->dflags);
     CUDA_TRY(cudaStreamEndCapture(cs, &c->loop_graph));
     CUDA_TRY(cudaGraphInstantiate(&c->loop_exec, c->loop_graph, 0));
-    k = {c->src, c->dst, c->labels, c->m, c->n, cap, *s, sm, c->shortcut, c->layout};
+    k = {c->src,    c->dst,      c->labels, c->m,   c->n,     cap,        *s,
+         sm,        c->shortcut, c->layout, check, c->items, c->n_items};
     return CC_OK;
 }
 
@@ -893,9 +1065,9 @@ int copy_out(cc_ctx* c, void* out, int eb);
 // The fast path of cc_run: async sweeps, no per-sweep counting or early
 // check -- the whole convergence loop is one graph launch.
 int run_graph(cc_ctx* c, const cc_schedule* s, int64_t cap, void* labels_out, int out_eb,
-              cc_stats* st) {
+              cc_stats* st, int check) {
     const int sm = s->atomic ? c->store_mode_atomic : c->store_mode_plain;
-    CC_TRY(build_loop(c, s, cap, sm));
+    CC_TRY(build_loop(c, s, cap, sm, check));
     CUDA_TRY(cudaEventRecord(c->evs, c->stream));
     CUDA_TRY(cudaGraphLaunch(c->loop_exec, c->stream));
     CUDA_TRY(cudaEventRecord(c->eve, c->stream));
@@ -927,7 +1099,10 @@ int run_graph(cc_ctx* c, const cc_schedule* s, int64_t cap, void* labels_out, in
         }
     }
     int rounds = 0;
-    if (c->hflags[kFlagCompress]) {  // cannot happen after a no-write sweep; be safe
+    // the post-loop pass changed something: only possible when the last
+    // sweep was order 1 (a no-write order >= 2 sweep or a passed early check
+    // leaves idempotent labels)
+    if (c->hflags[kFlagCompress]) {
         CC_TRY(compress(c, &rounds));
         ++rounds;
     }
@@ -935,8 +1110,11 @@ int run_graph(cc_ctx* c, const cc_schedule* s, int64_t cap, void* labels_out, in
     cudaEventElapsedTime(&total_ms, c->evs, c->eve);
     if (st) {
         st->sweeps_executed = k;
-        st->sweeps_until_stable = k - 1;
-        st->converged_by = 0;
+        // engine.py:313-320: a sweep passing the early check was still a
+        // changing sweep
+        const int by_check = c->hstate->by_check;
+        st->sweeps_until_stable = by_check ? k : k - 1;
+        st->converged_by = by_check ? 1 : 0;
         st->compress_rounds = rounds;
         st->converge_seconds = total_ms * 1e-3;
     }
@@ -949,13 +1127,19 @@ int copy_out(cc_ctx* c, void* out, int eb) {
         CUDA_TRY(cudaMemcpyAsync(out, c->labels, sizeof(lab_t) * c->n, cudaMemcpyDeviceToHost,
                                  c->stream));
     } else if (eb == 8) {
-        int64_t* tmp = nullptr;
-        CUDA_TRY(cudaMallocAsync((void**)&tmp, sizeof(int64_t) * c->n, c->stream));
-        k_widen<<<grid_for(c, c->n), kThreads, 0, c->stream>>>(c->labels, c->n, tmp);
+        // a cached device buffer: a per-call stream-ordered allocation of 8n
+        // bytes re-maps pool memory every call (~0.8 ms at n = 2^22, measured)
+        if (c->wide_cap < c->n) {
+            cudaFree(c->wide);
+            c->wide = nullptr;
+            c->wide_cap = 0;
+            CUDA_TRY(cudaMalloc((void**)&c->wide, sizeof(int64_t) * c->n));
+            c->wide_cap = c->n;
+        }
+        k_widen<<<grid_for(c, c->n), kThreads, 0, c->stream>>>(c->labels, c->n, c->wide);
         CUDA_TRY(cudaGetLastError());
-        CUDA_TRY(cudaMemcpyAsync(out, tmp, sizeof(int64_t) * c->n, cudaMemcpyDeviceToHost,
+        CUDA_TRY(cudaMemcpyAsync(out, c->wide, sizeof(int64_t) * c->n, cudaMemcpyDeviceToHost,
                                  c->stream));
-        CUDA_TRY(cudaFreeAsync(tmp, c->stream));
     } else {
         return fail(CC_EINVAL, "label element size must be 4 or 8");
     }
@@ -1105,6 +1289,7 @@ void cc_destroy(cc_ctx* c) {
     cudaStreamSynchronize(c->stream);
     if (c->own_edges) { cudaFree(c->src); cudaFree(c->dst); }
     if (c->own_labels) cudaFree(c->labels);
+    cudaFree(c->wide);
     cudaFree(c->shadow);
     cudaFree(c->before);
     cudaFree(c->dflags);
@@ -1256,7 +1441,7 @@ int cc_verify(cc_ctx* c, int* result) {
     k_check_le<<<grid_for(c, c->n), kThreads, 0, c->stream>>>(c->labels, c->n, c->dflags);
     CUDA_TRY(cudaGetLastError());
     CC_TRY(read_flags(c));
-    const int idem_bad = c->hflags[kFlagBad], le_bad = c->hflags[3];
+    const int idem_bad = c->hflags[kFlagBad], le_bad = c->hflags[kFlagLe];
     int edge_bad = 0;
     if (c->m > 0) {
         CUDA_TRY(cudaMemsetAsync(c->dflags + kFlagBad, 0, sizeof(int), c->stream));
@@ -1299,9 +1484,9 @@ int cc_run(cc_ctx* c, const cc_schedule* s, int flags, int64_t cap, void* labels
     const bool check = (flags & CC_RUN_EARLY_CHECK) != 0;
     const bool times = (flags & CC_RUN_SWEEP_TIMES) != 0;
     const bool first_scatter = (flags & CC_RUN_FIRST_SCATTER) != 0;
-    if (!sync && !count && !check && !first_scatter && !(flags & CC_RUN_HOST_LOOP) && c->n > 0 &&
+    if (!sync && !count && !first_scatter && !(flags & CC_RUN_HOST_LOOP) && c->n > 0 &&
         c->peers.n == 0)
-        return run_graph(c, s, cap, labels_out, out_eb, st);
+        return run_graph(c, s, cap, labels_out, out_eb, st, check ? 1 : 0);
     CUDA_TRY(cudaEventRecord(c->evs, c->stream));
     CC_TRY(enqueue_init(c, sync));
     int64_t sweep = 0, until_stable = 0;
@@ -1519,12 +1704,24 @@ int cc_set_option(cc_ctx* c, int option, int64_t value) {
             c->shortcut = (int)value;
             return CC_OK;
         case CC_OPT_SWEEP_VARIANT:
-            if (value < 0 || value > 5) return fail(CC_EINVAL, "sweep variant must be 0..5");
+            if (value < 0 || value > 11) return fail(CC_EINVAL, "sweep variant must be 0..11");
             c->sweep_variant = (int)value;
             c->loop_key.m = -1;
             return CC_OK;
         case CC_OPT_BUCKET_NOSMEM:
             c->bucket_nosmem = value != 0;
+            c->loop_key.m = -1;
+            return CC_OK;
+        case CC_OPT_BUCKET_PIPE:
+            if (value < 0 || value > 3) return fail(CC_EINVAL, "bucket kernel must be 0..3");
+            c->bucket_pipe = (int)value;
+            c->loop_key.m = -1;
+            return CC_OK;
+        case CC_OPT_ITEM_ORDER:
+            if (value < 0 || value > 2)
+                return fail(CC_EINVAL, "item order must be 0 (bucket-major), 1 (run-major) or "
+                                       "2 (run-major, staggered)");
+            c->item_order = (int)value;
             return CC_OK;
         case CC_OPT_TILE_SPLIT:
             if (value < 1 || value > 1024) return fail(CC_EINVAL, "tile split must be 1..1024");
@@ -1548,7 +1745,8 @@ int cc_set_option(cc_ctx* c, int option, int64_t value) {
 namespace {
 
 template <typename K>
-int reorder_bucketed_t(cc_ctx* c, int sbits, int total_bits, int64_t nb, int runs) {
+int reorder_bucketed_t(cc_ctx* c, int sbits, int total_bits, int64_t nb, int runs,
+                       int run_major) {
     const int64_t m = c->m;
     K *kin = nullptr, *kout = nullptr;
     lab_t* vout = nullptr;
@@ -1558,7 +1756,7 @@ int reorder_bucketed_t(cc_ctx* c, int sbits, int total_bits, int64_t nb, int run
     CUDA_TRY(cudaMalloc(&kout, sizeof(K) * m));
     CUDA_TRY(cudaMalloc(&vout, sizeof(lab_t) * m));
     k_make_keys<K><<<grid_for(c, m, 16), kThreads, 0, c->stream>>>(
-        c->src, c->dst, m, c->bucket_shift, sbits, runs, kin);
+        c->src, c->dst, m, c->bucket_shift, sbits, runs, nb, run_major, kin);
     CUDA_TRY(cudaGetLastError());
     CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, tb, kin, kout, c->dst, vout, (int)m, 0,
                                              total_bits, c->stream));
@@ -1570,51 +1768,64 @@ int reorder_bucketed_t(cc_ctx* c, int sbits, int total_bits, int64_t nb, int run
     CUDA_TRY(cudaGetLastError());
     CUDA_TRY(cudaMemcpyAsync(c->dst, vout, sizeof(lab_t) * m, cudaMemcpyDeviceToDevice,
                              c->stream));
+    // group g = bucket (bucket-major) or run * nb + bucket (run-major)
+    const int64_t ng = nb * runs;
     int64_t* dstarts = nullptr;
-    CUDA_TRY(cudaMalloc(&dstarts, sizeof(int64_t) * (nb + 1)));
-    k_bucket_starts<K><<<grid_for(c, nb), kThreads, 0, c->stream>>>(kout, m, nb, sbits, runs,
+    CUDA_TRY(cudaMalloc(&dstarts, sizeof(int64_t) * (ng + 1)));
+    k_bucket_starts<K><<<grid_for(c, ng), kThreads, 0, c->stream>>>(kout, m, ng, sbits, 1,
                                                                      dstarts);
     CUDA_TRY(cudaGetLastError());
-    std::vector<int64_t> starts(nb + 1);
-    CUDA_TRY(cudaMemcpyAsync(starts.data(), dstarts, sizeof(int64_t) * nb,
+    std::vector<int64_t> starts(ng + 1);
+    CUDA_TRY(cudaMemcpyAsync(starts.data(), dstarts, sizeof(int64_t) * ng,
                              cudaMemcpyDeviceToHost, c->stream));
     CUDA_TRY(cudaStreamSynchronize(c->stream));
-    starts[nb] = m;
+    starts[ng] = m;
     cudaFree(kin);
     cudaFree(kout);
     cudaFree(vout);
     cudaFree(tmp);
     cudaFree(dstarts);
-    // work items: each bucket's (src-sorted) rows cut into `seg` equal
-    // segments, each segment into pieces of <= item_rows; ordered
-    // segment-major so the CTAs running at the same time cover the same src
-    // range of every bucket -- the whole GPU then walks the src range in
-    // increasing order, as the grid-stride sweep does on chunk-sorted rows
-    // (the order that propagates the smallest labels furthest per sweep).
+    // work items: each group's (src-sorted) rows cut into pieces of <=
+    // item_rows, in group order.  Run-major groups make the CTAs running at
+    // the same time cover the same src range of every bucket of one run, so
+    // the whole GPU walks each run's src range in increasing order, as the
+    // grid-stride sweep does on chunk-sorted rows (the order that propagates
+    // the smallest labels furthest per sweep).
+    // item_order 2 staggers the items of one run: item j of bucket b's k
+    // items is keyed ((j / k + b / nb) mod 1), so the CTAs running at the same
+    // time read different src ranges (run-major lockstep makes every SM
+    // gather the same src labels at once) while the runs stay ordered.
     struct Keyed {
-        int64_t seg, b;
+        int64_t run;
+        double key;
         cck::BucketItem it;
     };
     std::vector<Keyed> keyed;
     const int64_t B = (int64_t)1 << c->bucket_shift;
-    const int64_t seg = 1;  // segment-major ordering measured slower (more items); kept at 1
-    for (int64_t b = 0; b < nb; ++b) {
+    for (int64_t g = 0; g < ng; ++g) {
+        const int64_t b = run_major ? g % nb : g;
         const uint32_t base = (uint32_t)(b * B);
         const uint32_t len = (uint32_t)std::min<int64_t>(B, c->n - b * B);
-        const int64_t rows = starts[b + 1] - starts[b];
-        for (int64_t s = 0; s < seg; ++s) {
-            const int64_t lo = starts[b] + rows * s / seg, hi = starts[b] + rows * (s + 1) / seg;
-            for (int64_t r = lo; r < hi; r += c->item_rows)
-                keyed.push_back({s, b, {r, std::min<int64_t>(r + c->item_rows, hi), base,
-                                        c->bucket_nosmem ? 0u : len}});
+        const int64_t k = (starts[g + 1] - starts[g] + c->item_rows - 1) / c->item_rows;
+        int64_t j = 0;
+        for (int64_t r = starts[g]; r < starts[g + 1]; r += c->item_rows, ++j) {
+            double key = (double)keyed.size();
+            if (c->item_order == 2) {
+                key = (double)j / (double)k + (double)b / (double)nb;
+                key -= (double)(int64_t)key;
+            }
+            keyed.push_back({run_major ? g / nb : 0, key,
+                             {r, std::min<int64_t>(r + c->item_rows, starts[g + 1]), base,
+                              c->bucket_nosmem ? 0u : len}});
         }
     }
     std::stable_sort(keyed.begin(), keyed.end(), [](const Keyed& a, const Keyed& b) {
-        return a.seg != b.seg ? a.seg < b.seg : a.b < b.b;
+        return a.run != b.run ? a.run < b.run : a.key < b.key;
     });
     std::vector<cck::BucketItem> items;
     items.reserve(keyed.size());
     for (auto& k : keyed) items.push_back(k.it);
+    if (items.size() >= ((size_t)1 << 31)) return fail(CC_EINVAL, "too many bucket work items");
     cudaFree(c->items);
     c->items = nullptr;
     c->n_items = (int)items.size();
@@ -1628,16 +1839,20 @@ int reorder_bucketed_t(cc_ctx* c, int sbits, int total_bits, int64_t nb, int run
 }
 
 // Layout 3: rows grouped by dst bucket, src-sorted inside (one global sort).
+// item_order 1: rows first cut, in their current order, into runs of
+// sort_chunk rows; groups are (run, bucket).
 int reorder_bucketed(cc_ctx* c) {
     if (c->m >= ((int64_t)1 << 31)) return fail(CC_EINVAL, "bucketed layout needs m < 2^31");
     const int sbits = std::max<int>(1, (int)ccgen::perm_bits((uint64_t)c->n));
     const int64_t B = (int64_t)1 << c->bucket_shift;
     const int64_t nb = (c->n + B - 1) / B;
-    const int runs = 1;  // key runs kept for experiments; segments order the items instead
+    const int run_major = c->item_order >= 1;
+    const int runs =
+        run_major ? (int)std::max<int64_t>(1, (c->m + c->sort_chunk - 1) / c->sort_chunk) : 1;
     const int bbits = std::max<int>(1, (int)ccgen::perm_bits((uint64_t)(nb * runs)));
     if (sbits + bbits <= 32)
-        return reorder_bucketed_t<uint32_t>(c, sbits, sbits + bbits, nb, runs);
-    return reorder_bucketed_t<unsigned long long>(c, sbits, sbits + bbits, nb, runs);
+        return reorder_bucketed_t<uint32_t>(c, sbits, sbits + bbits, nb, runs, run_major);
+    return reorder_bucketed_t<unsigned long long>(c, sbits, sbits + bbits, nb, runs, run_major);
 }
 
 // Layout 4: rows partitioned by dst into L2-window buckets of 2^tile_shift
@@ -1723,7 +1938,6 @@ int cc_reorder_edges(cc_ctx* c, int mode) {
     std::lock_guard<std::mutex> lk(c->mu);
     DeviceGuard g(c->device);
     if (c->m < 2) return CC_OK;
-    c->loop_key.m = -1;  // the captured loop may reference the old layout's buffers
     if (mode == 3) return reorder_bucketed(c);
     if (mode == 4) return reorder_l2tiles(c);
     c->layout = mode;

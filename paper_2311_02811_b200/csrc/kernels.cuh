@@ -83,15 +83,47 @@ __device__ __forceinline__ bool batch_o1(const lab_t* R, lab_t* T, const lab_t (
 // ---- order 2 (C-2 / C-Syn): z = min(L[L[w]], L[L[v]]); targets w, L[w], v, L[v]
 // All four target cells' current values were read while walking the chains
 // (L[w]=lu, L[L[w]]=zu, ...), so the conditional stores need no re-read.
-template <int NE, int SM>
+// Cache-hint flags OR-ed into the order-2 store-mode parameter (launch_o2
+// variants 6/7), for label arrays far beyond L2 (l2_tiled layout): the
+// src-side endpoint gathers L[u] hit random lines over all n labels and are
+// loaded evict-first, so they do not push the tile's dst window (kHintDstKeep:
+// loaded evict-last) out of L2.
+// kHintEdgeFirst: the edge stream is loaded L1::no_allocate with an L2
+// evict-first policy; kHintSrcKeep: src-side gathers evict-last.
+constexpr int kStoreMask = 7, kHintSrcStream = 8, kHintDstKeep = 16, kHintEdgeFirst = 32,
+              kHintSrcKeep = 64;
+
+__device__ __forceinline__ lab_t ld_evict_last(const lab_t* p) {
+    uint64_t pol;
+    lab_t r;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    asm volatile("ld.global.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(pol));
+    return r;
+}
+
+__device__ __forceinline__ uint4 ld_edges_evict_first(const uint4* p) {
+    uint64_t pol;
+    uint4 r;
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p), "l"(pol));
+    return r;
+}
+
+template <int NE, int SMH>
 __device__ __forceinline__ bool batch_o2(const lab_t* R, lab_t* T, const lab_t (&u)[NE],
                                          const lab_t (&v)[NE]) {
+    constexpr int SM = SMH & kStoreMask;
     lab_t lu[NE], lv[NE], zu[NE], zv[NE];
 #pragma unroll
     for (int k = 0; k < NE; ++k) {
         const bool live = u[k] != v[k];
-        lu[k] = live ? R[u[k]] : u[k];
-        lv[k] = live ? R[v[k]] : v[k];
+        if (SMH & kHintSrcStream) lu[k] = live ? __ldcs(R + u[k]) : u[k];
+        else if (SMH & kHintSrcKeep) lu[k] = live ? ld_evict_last(R + u[k]) : u[k];
+        else lu[k] = live ? R[u[k]] : u[k];
+        if (SMH & kHintDstKeep) lv[k] = live ? ld_evict_last(R + v[k]) : v[k];
+        else lv[k] = live ? R[v[k]] : v[k];
     }
 #pragma unroll
     for (int k = 0; k < NE; ++k) {
@@ -362,10 +394,9 @@ __device__ __forceinline__ bool batch_oh(const lab_t* R, lab_t* T, const lab_t (
 }
 
 template <int OK, int NE, int SM>
-__device__ __forceinline__ bool batch(const lab_t* R, lab_t* T, const lab_t (&u)[NE],
-                                      const lab_t (&v)[NE], int order) {
+__device__ __forceinline__ bool batch_other(const lab_t* R, lab_t* T, const lab_t (&u)[NE],
+                                            const lab_t (&v)[NE], int order) {
     if (OK == 1) return batch_o1<NE, SM>(R, T, u, v);
-    if (OK == 2) return batch_o2<NE, SM>(R, T, u, v);
     if (SM == kStoreCheckAllRed) {
         // synchronous sweeps (the only users of mode 4): labels do not move
         // within the sweep, chains stay long, so walk each edge's chains
@@ -384,6 +415,14 @@ __device__ __forceinline__ bool batch(const lab_t* R, lab_t* T, const lab_t (&u)
         return wrote;
     }
     return batch_oh<NE, SM>(R, T, u, v, order);
+}
+
+// SM: store mode, plus the kHint* bits for the order-2 batch.
+template <int OK, int NE, int SM>
+__device__ __forceinline__ bool batch(const lab_t* R, lab_t* T, const lab_t (&u)[NE],
+                                      const lab_t (&v)[NE], int order) {
+    if (OK == 2) return batch_o2<NE, SM>(R, T, u, v);
+    return batch_other<OK, NE, SM & kStoreMask>(R, T, u, v, order);
 }
 
 // Exact single-edge form for cc_mm_order (16-cell buffers: every golden
@@ -426,7 +465,15 @@ __global__ void __launch_bounds__(kThreads, MINB) k_sweep(const lab_t* __restric
         for (int q = 0; q < NV; ++q) {
             const int64_t i = base + (int64_t)q * stride;
             uint4 a = make_uint4(0, 0, 0, 0), b = make_uint4(0, 0, 0, 0);
-            if (i < nvec) { a = __ldcs(s4 + i); b = __ldcs(d4 + i); }
+            if (i < nvec) {
+                if (SM & kHintEdgeFirst) {
+                    a = ld_edges_evict_first(s4 + i);
+                    b = ld_edges_evict_first(d4 + i);
+                } else {
+                    a = __ldcs(s4 + i);
+                    b = __ldcs(d4 + i);
+                }
+            }
             u[4 * q + 0] = a.x; u[4 * q + 1] = a.y; u[4 * q + 2] = a.z; u[4 * q + 3] = a.w;
             v[4 * q + 0] = b.x; v[4 * q + 1] = b.y; v[4 * q + 2] = b.z; v[4 * q + 3] = b.w;
         }
@@ -535,6 +582,303 @@ __global__ void __launch_bounds__(1024)
         for (int64_t r = a1 + threadIdx.x; r < w.end; r += T) {
             lab_t u[1] = {src[r]}, v[1] = {dst[r]};
             wrote |= bucket_rows<SM, 1>(L, sl, base, len, u, v);
+        }
+        __syncthreads();  // the next item overwrites the slice
+    }
+    if (__syncthreads_or(wrote) && threadIdx.x == 0) *flag = 1;
+}
+
+// ---- dst-bucketed order-2 sweep, bulk-copy pipelined ------------------------
+// Same layout, items and semantics as k_sweep_bucketed, restructured for
+// latency: the ncu profile of k_sweep_bucketed shows it latency-bound (1 CTA
+// of 32 warps per SM, "long scoreboard" the top stall: every thread waits on
+// its own edge loads before it can issue its gathers).  Here one thread
+// streams the item's rows into an NS-deep ring of shared-memory stages with
+// cp.async.bulk (TMA bulk copies, completion on an mbarrier), and the slice
+// itself arrives the same way, so the threads only issue label gathers and
+// stores.  Every dst endpoint v of an item lies in its slice by construction
+// (rows are grouped by dst bucket), so the first-hop dst gather is an
+// unconditional shared-memory load; the second hops read global memory.
+constexpr int kBT = 1024;             // threads per CTA
+constexpr int kStageRows = 4 * kBT;   // rows per pipeline stage (4 per thread)
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(b)), "r"(count)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(b)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* sdst, const void* gsrc, uint32_t bytes,
+                                         uint64_t* b) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+        ::"r"(smem_addr(sdst)), "l"(gsrc), "r"(bytes), "r"(smem_addr(b))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+    const uint32_t a = smem_addr(b);
+    uint32_t ok = 0;
+    do {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(ok)
+            : "r"(a), "r"(parity)
+            : "memory");
+    } while (!ok);
+}
+
+// Rows (u[k], v[k]) with v[k] in the slice [base, base+len); u == v rows are
+// inert (self loops and the masked rows of a partial stage).
+template <int SM, int NE>
+__device__ __forceinline__ bool slice_rows(lab_t* L, lab_t* sl, lab_t base, lab_t len,
+                                           const lab_t (&u)[NE], const lab_t (&v)[NE]) {
+    lab_t lu[NE], lv[NE], zu[NE], zv[NE];
+#pragma unroll
+    for (int k = 0; k < NE; ++k) {
+        const bool live = u[k] != v[k];
+        lv[k] = live ? sl[v[k] - base] : v[k];
+        lu[k] = live ? L[u[k]] : u[k];
+    }
+#pragma unroll
+    for (int k = 0; k < NE; ++k) {
+        zu[k] = (lu[k] != u[k]) ? L[lu[k]] : lu[k];
+        zv[k] = (lv[k] != v[k]) ? L[lv[k]] : lv[k];
+    }
+    bool wrote = false;
+#pragma unroll
+    for (int k = 0; k < NE; ++k) {
+        if (u[k] == v[k]) continue;
+        const lab_t z = min(zu[k], zv[k]);
+        if (lu[k] > z) { lower<SM, false>(L, u[k], z); wrote = true; }
+        if (lu[k] != u[k] && zu[k] > z) { lower<SM, true>(L, lu[k], z); wrote = true; }
+        if (lv[k] > z) {
+            atomicMin(sl + (v[k] - base), z);
+            lower<SM, false>(L, v[k], z);
+            wrote = true;
+        }
+        if (lv[k] != v[k] && zv[k] > z) {
+            if (lv[k] - base < len) atomicMin(sl + (lv[k] - base), z);
+            lower<SM, true>(L, lv[k], z);
+            wrote = true;
+        }
+    }
+    return wrote;
+}
+
+// Lean form of k_sweep_bucketed for items with a slice (len > 0): the
+// first-hop dst gather is an unconditional (predicated) shared-memory load
+// and the second hops are predicated global loads -- no divergent branches
+// around the loads, so a thread's gathers issue back to back.  Warps run
+// independently inside an item (no barrier per row batch).  PF: the next
+// batch's edge vectors are loaded before the current batch is processed.
+template <int SM, bool PF>
+__global__ void __launch_bounds__(kBT, 1)
+    k_sweep_slice(const lab_t* __restrict__ src, const lab_t* __restrict__ dst, lab_t* L,
+                  const BucketItem* __restrict__ items, int n_items, int* __restrict__ flag,
+                  const int* __restrict__ d_order) {
+    extern __shared__ __align__(128) lab_t sl[];
+    __shared__ __align__(8) uint64_t sbar;
+    if (d_order && *d_order != 2) return;
+    bool wrote = false;
+    const int tid = threadIdx.x;
+    if (tid == 0) {
+        mbar_init(&sbar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    uint32_t par = 0;
+    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+        const BucketItem w = items[it];
+        const lab_t base = w.base, len = w.len;
+        // the slice arrives as ONE bulk copy (a per-thread load loop is 32
+        // dependent L2 round trips per thread: ~13 us per item, measured)
+        const lab_t lenb = len & ~3u;
+        if (tid == 0) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            mbar_expect_tx(&sbar, lenb * 4u);
+            if (lenb) bulk_g2s(sl, L + base, lenb * 4u, &sbar);
+        }
+        if (tid < len - lenb) sl[lenb + tid] = __ldcg(L + base + lenb + tid);
+        mbar_wait(&sbar, par);
+        par ^= 1u;
+        __syncthreads();
+        const int64_t a0 = min((w.start + 3) & ~(int64_t)3, w.end);
+        const int64_t a1 = max(a0, w.end & ~(int64_t)3);
+        if (tid < a0 - w.start) {  // <= 3 head rows
+            lab_t u[1] = {src[w.start + tid]}, v[1] = {dst[w.start + tid]};
+            wrote |= slice_rows<SM, 1>(L, sl, base, len, u, v);
+        }
+        if (tid < w.end - a1) {  // <= 3 tail rows
+            lab_t u[1] = {src[a1 + tid]}, v[1] = {dst[a1 + tid]};
+            wrote |= slice_rows<SM, 1>(L, sl, base, len, u, v);
+        }
+        const uint4* s4 = reinterpret_cast<const uint4*>(src + a0);
+        const uint4* d4 = reinterpret_cast<const uint4*>(dst + a0);
+        const int64_t nvec = (a1 - a0) >> 2;
+        int64_t q = tid;
+        uint4 a = make_uint4(0, 0, 0, 0), b = a;
+        if (PF && q < nvec) { a = __ldcs(s4 + q); b = __ldcs(d4 + q); }
+        for (; q < nvec; q += kBT) {
+            uint4 na = make_uint4(0, 0, 0, 0), nb = na;
+            if (PF) {
+                if (q + kBT < nvec) { na = __ldcs(s4 + q + kBT); nb = __ldcs(d4 + q + kBT); }
+            } else {
+                a = __ldcs(s4 + q);
+                b = __ldcs(d4 + q);
+            }
+            lab_t u[4] = {a.x, a.y, a.z, a.w}, v[4] = {b.x, b.y, b.z, b.w};
+            wrote |= slice_rows<SM, 4>(L, sl, base, len, u, v);
+            if (PF) { a = na; b = nb; }
+        }
+        __syncthreads();  // the next item overwrites the slice
+    }
+    if (__syncthreads_or(wrote) && threadIdx.x == 0) *flag = 1;
+}
+
+// Edge-agreement half of the early convergence check (engine.py:331-348)
+// on the dst-bucketed layout: L[v] comes from the item's slice in shared
+// memory, so the only global gathers are the src-sorted (coalescing) L[u].
+// Nothing is written during a check, so the slice equals global memory.
+// Same guards as the flat check: return at once when the sweep wrote
+// nothing or the check already failed; poll the failure word every 16 row
+// batches (one load per warp).
+__global__ void __launch_bounds__(kBT, 1)
+    k_check_slice(const lab_t* __restrict__ src, const lab_t* __restrict__ dst,
+                  const lab_t* __restrict__ L, const BucketItem* __restrict__ items, int n_items,
+                  int* flags, int wrote_idx, int check_idx) {
+    extern __shared__ __align__(128) lab_t sl[];
+    __shared__ __align__(8) uint64_t sbar;
+    volatile int* vf = flags;
+    if (!vf[wrote_idx] || vf[check_idx]) return;
+    const int tid = threadIdx.x;
+    if (tid == 0) {
+        mbar_init(&sbar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    uint32_t par = 0;
+    bool bad = false;
+    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+        const BucketItem w = items[it];
+        const lab_t base = w.base, len = w.len;
+        const lab_t lenb = len & ~3u;
+        if (tid == 0) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            mbar_expect_tx(&sbar, lenb * 4u);
+            if (lenb) bulk_g2s(sl, L + base, lenb * 4u, &sbar);
+        }
+        if (tid < len - lenb) sl[lenb + tid] = L[base + lenb + tid];
+        mbar_wait(&sbar, par);
+        par ^= 1u;
+        __syncthreads();
+        const int64_t a0 = min((w.start + 3) & ~(int64_t)3, w.end);
+        const int64_t a1 = max(a0, w.end & ~(int64_t)3);
+        if (tid < a0 - w.start) bad |= L[src[w.start + tid]] != sl[dst[w.start + tid] - base];
+        if (tid < w.end - a1) bad |= L[src[a1 + tid]] != sl[dst[a1 + tid] - base];
+        const uint4* s4 = reinterpret_cast<const uint4*>(src + a0);
+        const uint4* d4 = reinterpret_cast<const uint4*>(dst + a0);
+        const int64_t nvec = (a1 - a0) >> 2;
+        int k = 0;
+        for (int64_t q = tid; q < nvec && !bad; q += kBT) {
+            if ((++k & 15) == 0 && vf[check_idx]) break;
+            const uint4 a = __ldcs(s4 + q), b = __ldcs(d4 + q);
+            bad = (L[a.x] != sl[b.x - base]) | (L[a.y] != sl[b.y - base]) |
+                  (L[a.z] != sl[b.z - base]) | (L[a.w] != sl[b.w - base]);
+        }
+        if (bad) vf[check_idx] = 1;
+        // uniform exit decision (the slice is reused by the next item)
+        if (__syncthreads_or(bad || (tid == 0 && vf[check_idx]))) return;
+    }
+}
+
+// Dynamic shared memory: NS stages x (src, dst) x kStageRows labels, then the
+// slice of up to 2^bucket_shift labels.  Items must have len > 0.
+template <int SM, int NS>
+__global__ void __launch_bounds__(kBT, 1)
+    k_sweep_bucketed_tma(const lab_t* __restrict__ src, const lab_t* __restrict__ dst, lab_t* L,
+                         const BucketItem* __restrict__ items, int n_items,
+                         int* __restrict__ flag, const int* __restrict__ d_order) {
+    extern __shared__ __align__(128) lab_t smem[];
+    __shared__ __align__(8) uint64_t full[NS + 1];  // [NS] = slice barrier
+    if (d_order && *d_order != 2) return;
+    lab_t* sl = smem + NS * 2 * kStageRows;
+    const int tid = threadIdx.x;
+    if (tid == 0) {
+        for (int s = 0; s <= NS; ++s) mbar_init(&full[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    uint32_t par = 0;  // parity bit per barrier, identical in every thread
+    bool wrote = false;
+    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+        const BucketItem w = items[it];
+        const lab_t base = w.base, len = w.len;
+        const int64_t a0 = w.start & ~(int64_t)3;
+        const int64_t a1 = max(a0, w.end & ~(int64_t)3);
+        const int64_t nst = (a1 - a0 + kStageRows - 1) / kStageRows;
+        const lab_t lenb = len & ~3u;  // bulk part of the slice (16-byte multiple)
+        if (tid == 0) {
+            // order this CTA's earlier generic-proxy writes of the slice and
+            // stages (made visible by the __syncthreads) before the bulk writes
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            if (lenb) {
+                mbar_expect_tx(&full[NS], lenb * 4u);
+                bulk_g2s(sl, L + base, lenb * 4u, &full[NS]);
+            } else {
+                mbar_expect_tx(&full[NS], 0u);
+            }
+            for (int64_t k = 0; k < (nst < NS ? nst : (int64_t)NS); ++k) {
+                const int64_t r0 = a0 + k * kStageRows;
+                const uint32_t bytes = (uint32_t)(min((int64_t)kStageRows, a1 - r0) * 4);
+                lab_t* st = smem + k * 2 * kStageRows;
+                mbar_expect_tx(&full[k], 2u * bytes);
+                bulk_g2s(st, src + r0, bytes, &full[k]);
+                bulk_g2s(st + kStageRows, dst + r0, bytes, &full[k]);
+            }
+        }
+        for (lab_t i = lenb + tid; i < len; i += kBT) sl[i] = __ldcg(L + base + i);
+        mbar_wait(&full[NS], (par >> NS) & 1u);
+        par ^= 1u << NS;
+        __syncthreads();  // slice tail stores visible
+        for (int64_t k = 0; k < nst; ++k) {
+            const int s = (int)(k % NS);
+            mbar_wait(&full[s], (par >> s) & 1u);
+            par ^= 1u << s;
+            const int64_t r = a0 + k * kStageRows + 4 * tid;
+            const lab_t* st = smem + s * 2 * kStageRows;
+            lab_t u[4] = {0, 0, 0, 0}, v[4] = {0, 0, 0, 0};
+            if (r < a1) {
+                const uint4 a = reinterpret_cast<const uint4*>(st)[tid];
+                const uint4 b = reinterpret_cast<const uint4*>(st + kStageRows)[tid];
+                u[0] = a.x; u[1] = a.y; u[2] = a.z; u[3] = a.w;
+                v[0] = b.x; v[1] = b.y; v[2] = b.z; v[3] = b.w;
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    if (r + j < w.start) v[j] = u[j];  // head rows of the previous item
+            }
+            wrote |= slice_rows<SM, 4>(L, sl, base, len, u, v);
+            __syncthreads();  // stage s consumed by every thread
+            if (tid == 0 && k + NS < nst) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                const int64_t r0 = a0 + (k + NS) * kStageRows;
+                const uint32_t bytes = (uint32_t)(min((int64_t)kStageRows, a1 - r0) * 4);
+                lab_t* sp = smem + s * 2 * kStageRows;
+                mbar_expect_tx(&full[s], 2u * bytes);
+                bulk_g2s(sp, src + r0, bytes, &full[s]);
+                bulk_g2s(sp + kStageRows, dst + r0, bytes, &full[s]);
+            }
+        }
+        for (int64_t r = max(a1, w.start) + tid; r < w.end; r += kBT) {
+            lab_t u[1] = {src[r]}, v[1] = {dst[r]};
+            wrote |= slice_rows<SM, 1>(L, sl, base, len, u, v);
         }
         __syncthreads();  // the next item overwrites the slice
     }

@@ -356,6 +356,35 @@ def test_graph_loop_matches_host_loop_all_variants(golden):
                     assert all(c == -1 for c in st.changed_per_sweep[:-1])
 
 
+def test_graph_loop_early_check(golden):
+    """The early convergence check inside the CUDA-graph loop (engine.py:318-320,
+    331-348): exact labels for every variant and layout; a run stopped by the
+    check ends on a changing sweep (until_stable == executed), one stopped by
+    the flag on a no-write sweep -- the reference's two outcomes."""
+    cases = [(g["n"], np.asarray(g["edges"], dtype=np.int64).reshape(-1, 2), g["labels"])
+             for g in golden["graphs"][::2]]
+    for n, e in (graphgen.grid(180, 210, 0.55, 4), graphgen.rmat(13, 16, 9),
+                 graphgen.forest(40, 5), spec.erdos_renyi(4097, 9000, 3)):
+        cases.append((n, e, oracle.rem_union_find(n, e).tolist()))
+    seen = set()
+    for layout in ("input", "chunk_sorted", "dst_bucketed"):
+        for n, e, exp in cases:
+            for variant in ("C-1", "C-2", "C-m", "C-1m1m"):
+                sched = make_schedule(variant, 6, sync=False)
+                lg, sg = run_contour((n, e), sched, count_changes=False, early_check=True,
+                                     layout=layout)
+                assert lg.tolist() == exp, (layout, variant, n)
+                check_invariants(lg, sg)
+                seen.add(sg.converged_by)
+                if sg.converged_by == "early-check":
+                    assert sg.sweeps_until_stable == sg.sweeps_executed
+                    assert all(c == -1 for c in sg.changed_per_sweep)
+                else:
+                    assert sg.sweeps_until_stable == sg.sweeps_executed - 1
+                    assert sg.changed_per_sweep[-1] == 0
+    assert "early-check" in seen
+
+
 def test_graph_loop_cap_and_rebuild():
     ctx = _lib.Context(0)
     e = np.array([[5, 4], [4, 3], [3, 2], [2, 1], [1, 0]])
@@ -377,10 +406,16 @@ def test_graph_loop_cap_and_rebuild():
     ctx.close()
 
 
-@pytest.mark.parametrize("bshift,item_rows,threads", [(8, 1024, 256), (12, 5000, 512),
-                                                      (15, 1 << 18, 1024)])
-def test_dst_bucketed_layout_exact(bshift, item_rows, threads):
-    """Layout 3 + the shared-memory bucketed order-2 sweep, host and graph loops,
+@pytest.mark.parametrize("bshift,item_rows,threads,pipe,order",
+                         [(8, 1024, 256, 0, 0), (12, 5000, 512, 0, 1), (15, 1 << 18, 1024, 0, 0),
+                          (8, 1024, 1024, 3, 0), (12, 5001, 1024, 2, 1),
+                          (15, 1 << 18, 1024, 3, 0), (15, 9999, 1024, 3, 1),
+                          (9, 1027, 1024, 1, 0), (15, 1 << 18, 1024, 1, 1),
+                          (14, 7001, 1024, 2, 0), (15, 65536, 1024, 2, 1),
+                          (10, 3000, 1024, 1, 2)])
+def test_dst_bucketed_layout_exact(bshift, item_rows, threads, pipe, order):
+    """Layout 3 + the shared-memory bucketed order-2 sweeps (plain and bulk-copy
+    pipelined kernels, bucket- and run-major items), host and graph loops,
     plain and atomic schedules, on RMAT / grid / forest / ragged inputs."""
     graphs = [graphgen.rmat(14, 16, 5), graphgen.grid(150, 170, 0.55, 3),
               graphgen.forest(30, 2), spec.erdos_renyi(3001, 7777, 4)]
@@ -388,6 +423,9 @@ def test_dst_bucketed_layout_exact(bshift, item_rows, threads):
     ctx.set_option(_lib.CC_OPT_BUCKET_SHIFT, bshift)
     ctx.set_option(_lib.CC_OPT_ITEM_ROWS, item_rows)
     ctx.set_option(_lib.CC_OPT_BUCKET_THREADS, threads)
+    ctx.set_option(_lib.CC_OPT_BUCKET_PIPE, pipe)
+    ctx.set_option(_lib.CC_OPT_ITEM_ORDER, order)
+    ctx.set_option(_lib.CC_OPT_SORT_CHUNK, 100003)
     for n, e in graphs:
         exp = oracle.rem_union_find(n, e)
         engine.stage_graph(ctx, n, e, "dst_bucketed")

@@ -25,15 +25,26 @@ from paper_2311_02811_b200.engine import make_schedule  # noqa: E402
 
 
 def run(cfg, args):
-    spec = graphgen.CONFIGS[cfg]
+    spec = (dict(kind="rmat", scale=int(cfg[5:]), edgefactor=16) if cfg.startswith("rmat:")
+            else graphgen.CONFIGS[cfg])
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
     ctx = _lib.Context(0, stream.cuda_stream)
-    rec = {"config": cfg}
+    ctx.set_option(_lib.CC_OPT_SWEEP_VARIANT, args.variant)
+    ctx.set_option(_lib.CC_OPT_BUCKET_PIPE, args.pipe)
+    ctx.set_option(_lib.CC_OPT_ITEM_ORDER, args.item_order)
+    ctx.set_option(_lib.CC_OPT_ITEM_ROWS, args.item_rows)
+    ctx.set_option(_lib.CC_OPT_SORT_CHUNK, args.sort_chunk)
+    ctx.set_option(_lib.CC_OPT_BUCKET_SHIFT, args.bshift)
+    rec = {"seed": args.seed, "early_check": args.early_check, "sort_chunk": args.sort_chunk, "bshift": args.bshift, "config": cfg, "variant": args.variant, "pipe": args.pipe,
+           "item_order": args.item_order, "item_rows": args.item_rows}
     t0 = time.perf_counter()
     host = None
     if spec["kind"] == "rmat":
-        n, m = graphgen.rmat_device(ctx, spec["scale"], spec["edgefactor"], 1)
+        n, m = graphgen.rmat_device(ctx, spec["scale"], spec["edgefactor"], args.seed)
+        if args.runs:
+            ctx.set_option(_lib.CC_OPT_SORT_CHUNK, -(-m // args.runs))
+            rec["runs"] = args.runs
         lay = engine.resolve_layout(args.layout, m, n)
         t1 = time.perf_counter()
         _lib.check(ctx.lib.cc_reorder_edges(ctx.handle, engine.LAYOUTS[lay]))
@@ -49,7 +60,7 @@ def run(cfg, args):
     sched = make_schedule("c2")
     runs = []
     for _ in range(args.repeats):
-        _, st = engine.run_staged(ctx, sched, count_changes=False, early_check=False)
+        _, st = engine.run_staged(ctx, sched, count_changes=False, early_check=args.early_check)
         runs.append(st)
     best = min(runs, key=lambda s: s.device_seconds)
     rec.update(device_s=best.device_seconds, edges_per_s=m / best.device_seconds,
@@ -95,6 +106,15 @@ def main():
     ap.add_argument("--no-oracle", action="store_true")
     ap.add_argument("--repeats", type=int, default=3)
     ap.add_argument("--layout", default="auto")
+    ap.add_argument("--variant", type=int, default=1)
+    ap.add_argument("--pipe", type=int, default=3)
+    ap.add_argument("--item-order", type=int, default=0)
+    ap.add_argument("--item-rows", type=int, default=1 << 18)
+    ap.add_argument("--sort-chunk", type=int, default=1 << 23)
+    ap.add_argument("--bshift", type=int, default=15)
+    ap.add_argument("--early-check", type=int, default=0)
+    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--runs", type=int, default=0, help="bucketed run-major: runs (sets sort chunk)")
     args = ap.parse_args()
     for cfg in args.configs:
         run(cfg, args)
