@@ -366,8 +366,10 @@ def run_single(args, device):
             torch.cuda.synchronize()
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
-            engine.stage_graph(ctx, n, host_edges, args.layout)
-            engine.run_staged(ctx, sched, sweep_times=False, labels_out=labels_host, **kw)
+            # run_contour's host-graph path: one cc_run_host call (sweep 1
+            # streamed behind the copy where the layout allows it)
+            engine.run_host(ctx, n, host_edges, sched, layout=args.layout, sweep_times=False,
+                            labels_out=labels_host, **kw)
             b.record(stream)
             torch.cuda.synchronize()
             if i >= args.warmup:
@@ -375,8 +377,8 @@ def run_single(args, device):
         e2e_s = sum(e2e_times) / len(e2e_times)
         e2e = {"value": m / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(host_edges.nbytes),
                "d2h_bytes_per_step": int(labels_host.nbytes), "seconds_per_step": e2e_s,
-               "path": "cc_stage_edges(pinned int32 (m,2), chunk-sorted while copying) + "
-                       "cc_run(labels -> pinned int64)"}
+               "path": "cc_run_host(pinned int32 (m,2) edges, chunk-sorted and swept while "
+                       "copying; labels -> pinned int64), the run_contour host-graph path"}
 
     # ---- CPU baseline: the reference path (oracle port) on the host cores
     cpu = None

@@ -102,6 +102,18 @@ int cc_labels_device(cc_ctx* ctx, uint32_t** labels_dev);
 int cc_run(cc_ctx* ctx, const cc_schedule* sched, int flags, int64_t cap,
            void* labels_out, int out_elem_bytes, cc_stats* stats);
 
+/* Stage host edges (as cc_stage_edges) AND run (as cc_run) in one call --
+ * run_contour(g, ...) for a graph in host memory.  Asynchronous runs without
+ * COUNT_CHANGES / FIRST_SCATTER / HOST_LOOP, staged in input or chunk-sorted
+ * order (CC_OPT_STAGE_LAYOUT 0 or 2), run sweep 1 chunk by chunk right behind
+ * the host-to-device copy (each chunk is swept as soon as it is staged, while
+ * the next one is in flight), then its shortcut pass and early check, then
+ * the device-side loop from sweep 2 if needed; sweep_seconds[0] is the span
+ * of the streamed sweep.  Every other case stages, then runs. */
+int cc_run_host(cc_ctx* ctx, const void* edges_host, int elem_bytes, int64_t m, int64_t n,
+                const cc_schedule* sched, int flags, int64_t cap, void* labels_out,
+                int out_elem_bytes, cc_stats* stats);
+
 /* ---- building blocks (multi-GPU driver, tests) ---- */
 int cc_init_labels(cc_ctx* ctx);
 /* One sweep over the staged edges: sweep_edges(read, target, edges, 0, m, 0,

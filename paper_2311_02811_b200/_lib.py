@@ -60,6 +60,10 @@ SIGNATURES = {
     "cc_run": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(CCSchedule), ctypes.c_int,
                               ctypes.c_int64, ctypes.c_void_p, ctypes.c_int,
                               ctypes.POINTER(CCStats)]),
+    "cc_run_host": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int,
+                                   ctypes.c_int64, ctypes.c_int64, ctypes.POINTER(CCSchedule),
+                                   ctypes.c_int, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int,
+                                   ctypes.POINTER(CCStats)]),
     "cc_init_labels": (ctypes.c_int, [ctypes.c_void_p]),
     "cc_sweep": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                 ctypes.c_int, ctypes.POINTER(ctypes.c_int)]),

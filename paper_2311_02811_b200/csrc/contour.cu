@@ -209,9 +209,13 @@ __global__ void k_stage(const T* __restrict__ aos, int64_t rows, int64_t n, lab_
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < rows;
          e += (int64_t)gridDim.x * blockDim.x) {
         const T a = aos[2 * e], b = aos[2 * e + 1];
-        bad |= (a < 0) | (b < 0) | ((int64_t)a >= n) | ((int64_t)b >= n);
-        src[e] = (lab_t)a;
-        dst[e] = (lab_t)b;
+        const bool out = (a < 0) | (b < 0) | ((int64_t)a >= n) | ((int64_t)b >= n);
+        bad |= out;
+        // an out-of-range row fails the staging call; until then it is an
+        // inert self loop, so a sweep streamed behind the copy never indexes
+        // outside the label array
+        src[e] = out ? 0u : (lab_t)a;
+        dst[e] = out ? 0u : (lab_t)b;
     }
     if (__syncthreads_or(bad) && threadIdx.x == 0) flags[kFlagBad] = 1;
 }
@@ -422,9 +426,11 @@ __device__ __forceinline__ int order_for_dev(const cc_schedule& s, long long swe
     }
 }
 
-__global__ void k_loop_init(LoopState* st, int* flags, cc_schedule s) {
-    st->sweep = 0;
-    st->order = order_for_dev(s, 1);
+// start: sweeps already done before the loop (1 after cc_run_host's
+// streamed first sweep, else 0).
+__global__ void k_loop_init(LoopState* st, int* flags, cc_schedule s, long long start) {
+    st->sweep = start;
+    st->order = order_for_dev(s, start + 1);
     st->converged = 0;
     st->capped = 0;
     st->by_check = 0;
@@ -548,6 +554,7 @@ struct cc_ctx {
         int check;
         const void* items;
         int n_items;
+        int resume;
     } loop_key = {};
     std::mutex mu;
 };
@@ -575,11 +582,15 @@ int grid_for(const cc_ctx* c, int64_t work, int per_sm = 8) {
     return (int)b;
 }
 
-// Launch context of one sweep: the stream, and for graph capture the
-// device word holding the order (nullptr: use the host value).
+// Launch context of one sweep: the stream, for graph capture the device
+// word holding the order (nullptr: use the host value), and optionally a row
+// window [off, off + rows) of the staged edges (rows < 0: all m rows; the
+// flat k_sweep path only -- the streamed first sweep of cc_run_host).
 struct SweepLaunch {
     cudaStream_t stream;
     const int* d_order;
+    int64_t off = 0;
+    int64_t rows = -1;
 };
 
 template <int OK, int SM, int NV, int MINB = 1>
@@ -591,10 +602,11 @@ int launch_sweep_t(cc_ctx* c, const lab_t* R, lab_t* T, int order, SweepLaunch s
                                                       kThreads, 0);
         occ = o > 0 ? o : 1;
     }
-    const int64_t units = (c->m + 4 * NV - 1) / (4 * NV);
+    const int64_t m = sl.rows < 0 ? c->m : sl.rows;
+    const int64_t units = (m + 4 * NV - 1) / (4 * NV);
     const int blocks = grid_for(c, units, occ);
     cck::k_sweep<OK, SM, NV, MINB><<<blocks, kThreads, 0, sl.stream>>>(
-        c->src, c->dst, c->m, R, T, order, c->dflags + kFlagWrote, sl.d_order);
+        c->src + sl.off, c->dst + sl.off, m, R, T, order, c->dflags + kFlagWrote, sl.d_order);
     CUDA_TRY(cudaGetLastError());
     return CC_OK;
 }
@@ -668,11 +680,14 @@ int launch_o2(cc_ctx* c, const lab_t* R, lab_t* T, int sm, SweepLaunch sl) {
 
 // Order-specialised sweep: order 1 and 2 get unrolled batch kernels, any
 // other order the buffered chain walker.
-int launch_order(cc_ctx* c, const lab_t* R, lab_t* T, int order, int sm) {
-    const SweepLaunch sl{c->stream, nullptr};
+int launch_order_sl(cc_ctx* c, const lab_t* R, lab_t* T, int order, int sm, SweepLaunch sl) {
     if (order == 1) return launch_store_mode<1, 2>(c, R, T, order, sm, sl);
     if (order == 2) return launch_o2(c, R, T, sm, sl);
     return launch_store_mode<0, 1>(c, R, T, order, sm, sl);
+}
+
+int launch_order(cc_ctx* c, const lab_t* R, lab_t* T, int order, int sm) {
+    return launch_order_sl(c, R, T, order, sm, SweepLaunch{c->stream, nullptr});
 }
 
 int ensure_aux(cc_ctx* c, bool need_shadow, bool need_before) {
@@ -996,12 +1011,12 @@ bool same_schedule(const cc_schedule& a, const cc_schedule& b) {
 
 // Capture iota -> loop_init -> WHILE{ guarded sweeps -> loop_control } -> compress
 // into one executable graph.
-int build_loop(cc_ctx* c, const cc_schedule* s, int64_t cap, int sm, int check) {
+int build_loop(cc_ctx* c, const cc_schedule* s, int64_t cap, int sm, int check, int resume) {
     auto& k = c->loop_key;
     if (c->loop_exec && k.src == c->src && k.dst == c->dst && k.labels == c->labels &&
         k.m == c->m && k.n == c->n && k.cap == cap && same_schedule(k.s, *s) && k.sm == sm &&
         k.shortcut == c->shortcut && k.layout == c->layout && k.check == check &&
-        k.items == c->items && k.n_items == c->n_items)
+        k.items == c->items && k.n_items == c->n_items && k.resume == resume)
         return CC_OK;
     if (c->loop_exec) cudaGraphExecDestroy(c->loop_exec);
     if (c->loop_graph) cudaGraphDestroy(c->loop_graph);
@@ -1015,8 +1030,8 @@ int build_loop(cc_ctx* c, const cc_schedule* s, int64_t cap, int sm, int check) 
     }
     cudaStream_t cs = c->cap_stream;
     CUDA_TRY(cudaStreamBeginCapture(cs, cudaStreamCaptureModeRelaxed));
-    k_iota<<<grid_for(c, c->n), kThreads, 0, cs>>>(c->labels, c->n);
-    k_loop_init<<<1, 1, 0, cs>>>(c->dstate, c->dflags, *s);
+    if (!resume) k_iota<<<grid_for(c, c->n), kThreads, 0, cs>>>(c->labels, c->n);
+    k_loop_init<<<1, 1, 0, cs>>>(c->dstate, c->dflags, *s, resume ? 1 : 0);
     cudaStreamCaptureStatus status;
     cudaGraph_t g = nullptr;
     const cudaGraphNode_t* deps = nullptr;
@@ -1055,8 +1070,8 @@ int build_loop(cc_ctx* c, const cc_schedule* s, int64_t cap, int sm, int check) 
     k_compress<<<grid_for(c, c->n), kThreads, 0, cs>>>(c->labels, c->n, c->dflags);
     CUDA_TRY(cudaStreamEndCapture(cs, &c->loop_graph));
     CUDA_TRY(cudaGraphInstantiate(&c->loop_exec, c->loop_graph, 0));
-    k = {c->src,    c->dst,      c->labels, c->m,   c->n,     cap,        *s,
-         sm,        c->shortcut, c->layout, check, c->items, c->n_items};
+    k = {c->src, c->dst,   c->labels, c->m,     c->n,       cap,   *s,
+         sm,     c->shortcut, c->layout, check, c->items, c->n_items, resume};
     return CC_OK;
 }
 
@@ -1064,10 +1079,12 @@ int copy_out(cc_ctx* c, void* out, int eb);
 
 // The fast path of cc_run: async sweeps, no per-sweep counting or early
 // check -- the whole convergence loop is one graph launch.
+// resume = 1: sweep 1 already ran (cc_run_host); the loop starts at sweep 2
+// and leaves the stats entries of sweep 1 to the caller.
 int run_graph(cc_ctx* c, const cc_schedule* s, int64_t cap, void* labels_out, int out_eb,
-              cc_stats* st, int check) {
+              cc_stats* st, int check, int resume = 0) {
     const int sm = s->atomic ? c->store_mode_atomic : c->store_mode_plain;
-    CC_TRY(build_loop(c, s, cap, sm, check));
+    CC_TRY(build_loop(c, s, cap, sm, check, resume));
     CUDA_TRY(cudaEventRecord(c->evs, c->stream));
     CUDA_TRY(cudaGraphLaunch(c->loop_exec, c->stream));
     CUDA_TRY(cudaEventRecord(c->eve, c->stream));
@@ -1092,7 +1109,7 @@ int run_graph(cc_ctx* c, const cc_schedule* s, int64_t cap, void* labels_out, in
             CUDA_TRY(cudaStreamSynchronize(c->stream));
         }
         unsigned long long prev = c->hstate->t0;
-        for (long long i = 0; i < nrec && i < st->capacity; ++i) {
+        for (long long i = resume; i < nrec && i < st->capacity; ++i) {
             if (st->changed_per_sweep) st->changed_per_sweep[i] = c->hrec[i].wrote ? -1 : 0;
             if (st->sweep_seconds) st->sweep_seconds[i] = (c->hrec[i].t - prev) * 1e-9;
             prev = c->hrec[i].t;
@@ -1179,9 +1196,23 @@ int sort_rows(cc_ctx* c, int64_t off, int64_t len) {
     return CC_OK;
 }
 
+// ss != nullptr (cc_run_host): labels are initialised first and sweep 1 of
+// schedule ss runs chunk by chunk right behind the copy -- each chunk's rows
+// are swept as soon as they are staged, while the next chunk is in flight.
+// Sweeping the chunks one after another is one asynchronous sweep over all
+// rows in staging order (the grid-stride sweep visits rows in that order
+// too), so it is sweep 1 of the run, overlapped with the transfer.
 template <typename T>
-int stage_impl(cc_ctx* c, const T* edges, int64_t m, bool host) {
+int stage_impl(cc_ctx* c, const T* edges, int64_t m, bool host,
+               const cc_schedule* ss = nullptr, bool ss_check = false) {
     CUDA_TRY(cudaMemsetAsync(c->dflags + kFlagBad, 0, sizeof(int), c->stream));
+    const int ssm = ss ? (ss->atomic ? c->store_mode_atomic : c->store_mode_plain) : 0;
+    if (ss) {
+        k_iota<<<grid_for(c, c->n), kThreads, 0, c->stream>>>(c->labels, c->n);
+        CUDA_TRY(cudaGetLastError());
+        CUDA_TRY(cudaMemsetAsync(c->dflags, 0, sizeof(int) * kNumFlags, c->stream));
+        CUDA_TRY(cudaEventRecord(c->ev0, c->stream));
+    }
     const bool chunk_sort = c->stage_layout == 2;
     const int64_t chunk = std::min<int64_t>(c->sort_chunk, std::max<int64_t>(m, 1));
     if (m > 0) {
@@ -1205,7 +1236,7 @@ int stage_impl(cc_ctx* c, const T* edges, int64_t m, bool host) {
                 c->stage_buf_bytes = need;
             }
             for (int b = 0; b < 2; ++b) CUDA_TRY(cudaEventRecord(c->freed[b], c->stream));
-            int64_t k = 0;
+            int64_t k = 0, swept = 0;
             for (int64_t off = 0; off < m; off += chunk, ++k) {
                 const int b = (int)(k & 1);
                 T* buf = (T*)c->stage_buf[b];
@@ -1220,8 +1251,32 @@ int stage_impl(cc_ctx* c, const T* edges, int64_t m, bool host) {
                 CUDA_TRY(cudaGetLastError());
                 CUDA_TRY(cudaEventRecord(c->freed[b], c->stream));
                 if (chunk_sort) CC_TRY(sort_rows(c, off, rows));
+                if (ss) {
+                    // sweep windows start 16-byte aligned (the sweep's uint4 edge
+                    // loads): a chunk's last rows mod 4 wait for the next chunk
+                    const int64_t hi = off + rows == m ? m : (off + rows) & ~(int64_t)3;
+                    if (hi > swept)
+                        CC_TRY(launch_order_sl(c, c->labels, c->labels, order_for(ss, 1), ssm,
+                                               SweepLaunch{c->stream, nullptr, swept, hi - swept}));
+                    swept = hi;
+                }
             }
         }
+    }
+    if (ss) CUDA_TRY(cudaEventRecord(c->ev1, c->stream));
+    if (ss) {
+        // sweep 1's shortcut and early check, in the same synchronisation
+        for (int j = 0; j < c->shortcut; ++j)
+            k_compress<<<grid_for(c, c->n), kThreads, 0, c->stream>>>(c->labels, c->n,
+                                                                      c->dflags);
+        if (ss_check) {
+            k_gcheck_idem<<<grid_for(c, c->n), kThreads, 0, c->stream>>>(c->labels, c->n,
+                                                                          c->dflags);
+            if (m > 0)
+                k_gcheck_edges<<<grid_for(c, (m + 3) / 4), kThreads, 0, c->stream>>>(
+                    c->src, c->dst, m, c->labels, c->dflags);
+        }
+        CUDA_TRY(cudaGetLastError());
     }
     CC_TRY(read_flags(c));
     if (c->hflags[kFlagBad]) return fail(CC_EINVAL, "edge endpoint out of range (n=%lld)",
@@ -1229,13 +1284,14 @@ int stage_impl(cc_ctx* c, const T* edges, int64_t m, bool host) {
     return CC_OK;
 }
 
-int stage(cc_ctx* c, const void* edges, int eb, int64_t m, int64_t n, bool host) {
+int stage(cc_ctx* c, const void* edges, int eb, int64_t m, int64_t n, bool host,
+          const cc_schedule* ss = nullptr, bool ss_check = false) {
     if (eb != 4 && eb != 8) return fail(CC_EINVAL, "edge element size must be 4 or 8");
     if (m > 0 && !edges) return fail(CC_EINVAL, "null edge buffer");
     CC_TRY(set_graph(c, m, n));
     CC_TRY(ensure_edges(c, m));
-    if (eb == 4) return stage_impl<int32_t>(c, (const int32_t*)edges, m, host);
-    return stage_impl<int64_t>(c, (const int64_t*)edges, m, host);
+    if (eb == 4) return stage_impl<int32_t>(c, (const int32_t*)edges, m, host, ss, ss_check);
+    return stage_impl<int64_t>(c, (const int64_t*)edges, m, host, ss, ss_check);
 }
 
 }  // namespace
@@ -1469,16 +1525,22 @@ int cc_synchronize(cc_ctx* c) {
     return CC_OK;
 }
 
-// run_contour (engine.py:248-328) over the device kernels.
-int cc_run(cc_ctx* c, const cc_schedule* s, int flags, int64_t cap, void* labels_out, int out_eb,
-           cc_stats* st) {
+}  // extern "C"
+
+namespace {
+
+int check_run_args(cc_ctx* c, const cc_schedule* s, void* labels_out, int out_eb) {
     if (!c || !s) return fail(CC_EINVAL, "null argument");
     if (s->variant < CC_VAR_CSYN || s->variant > CC_VAR_C1M1M)
         return fail(CC_EINVAL, "unknown variant code %d", s->variant);
     if (labels_out && out_eb != 4 && out_eb != 8)
         return fail(CC_EINVAL, "label element size must be 4 or 8");
-    std::lock_guard<std::mutex> lk(c->mu);
-    DeviceGuard g(c->device);
+    return CC_OK;
+}
+
+// run_contour (engine.py:248-328) over the device kernels; caller holds c->mu.
+int run_impl(cc_ctx* c, const cc_schedule* s, int flags, int64_t cap, void* labels_out,
+             int out_eb, cc_stats* st) {
     const bool sync = s->sync != 0;
     const bool count = (flags & CC_RUN_COUNT_CHANGES) != 0;
     const bool check = (flags & CC_RUN_EARLY_CHECK) != 0;
@@ -1534,6 +1596,77 @@ int cc_run(cc_ctx* c, const cc_schedule* s, int flags, int64_t cap, void* labels
         st->converged_by = converged_by;
         st->compress_rounds = rounds;
         st->converge_seconds = total_ms * 1e-3;
+    }
+    return copy_out(c, labels_out, out_eb);
+}
+
+// The streamed path of cc_run_host: applies to asynchronous runs without
+// exact counting / first scatter / host loop / peers, staged in input or
+// chunk-sorted order (the orders a sweep can follow while rows arrive).
+bool streamable(const cc_ctx* c, const cc_schedule* s, int flags) {
+    return !s->sync && !(flags & (CC_RUN_COUNT_CHANGES | CC_RUN_FIRST_SCATTER | CC_RUN_HOST_LOOP)) &&
+           c->peers.n == 0 && (c->stage_layout == 0 || c->stage_layout == 2);
+}
+
+}  // namespace
+
+extern "C" {
+
+int cc_run(cc_ctx* c, const cc_schedule* s, int flags, int64_t cap, void* labels_out, int out_eb,
+           cc_stats* st) {
+    CC_TRY(check_run_args(c, s, labels_out, out_eb));
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard g(c->device);
+    return run_impl(c, s, flags, cap, labels_out, out_eb, st);
+}
+
+// Stage host edges AND run (run_contour(g, ...) for a graph in host memory):
+// sweep 1 streams behind the host-to-device copy (stage_impl), then its
+// shortcut pass and early check decide whether the device-side loop must
+// continue from sweep 2.
+int cc_run_host(cc_ctx* c, const void* edges_host, int elem_bytes, int64_t m, int64_t n,
+                const cc_schedule* s, int flags, int64_t cap, void* labels_out, int out_eb,
+                cc_stats* st) {
+    CC_TRY(check_run_args(c, s, labels_out, out_eb));
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard g(c->device);
+    if (!streamable(c, s, flags) || n == 0 || cap < 1) {
+        CC_TRY(stage(c, edges_host, elem_bytes, m, n, true));
+        return run_impl(c, s, flags, cap, labels_out, out_eb, st);
+    }
+    const bool check = (flags & CC_RUN_EARLY_CHECK) != 0;
+    CC_TRY(stage(c, edges_host, elem_bytes, m, n, true, s, check));
+    const bool wrote = c->hflags[kFlagWrote] != 0;
+    const bool passed = check && wrote && c->hflags[kFlagCheck] == 0;
+    float sweep1_ms = 0.f;
+    cudaEventElapsedTime(&sweep1_ms, c->ev0, c->ev1);
+    int64_t k = 1, until_stable = wrote ? 1 : 0;
+    int by = passed ? 1 : 0;
+    double seconds = sweep1_ms * 1e-3;
+    int rounds = 0;
+    if (wrote && !passed) {  // not converged after sweep 1: the loop from sweep 2
+        CUDA_TRY(cudaMemsetAsync(c->dflags, 0, sizeof(int) * kNumFlags, c->stream));
+        CC_TRY(run_graph(c, s, cap, nullptr, out_eb, st, check ? 1 : 0, 1));
+        if (st) {
+            k = st->sweeps_executed;
+            until_stable = st->sweeps_until_stable;
+            by = st->converged_by;
+            rounds = st->compress_rounds;
+            seconds += st->converge_seconds;
+        }
+    } else if (!passed) {
+        CC_TRY(compress(c, &rounds));  // (a passed check already proved idempotence)
+    }
+    if (st) {
+        st->sweeps_executed = k;
+        st->sweeps_until_stable = until_stable;
+        st->converged_by = by;
+        st->compress_rounds = rounds;
+        st->converge_seconds = seconds;
+        if (st->capacity >= 1) {
+            if (st->changed_per_sweep) st->changed_per_sweep[0] = wrote ? -1 : 0;
+            if (st->sweep_seconds) st->sweep_seconds[0] = sweep1_ms * 1e-3;
+        }
     }
     return copy_out(c, labels_out, out_eb);
 }

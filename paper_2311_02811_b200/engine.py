@@ -154,6 +154,17 @@ def resolve_layout(layout: str, m: int, n: int = 0) -> str:
     return layout
 
 
+def _host_edges(edges) -> np.ndarray:
+    e = np.asarray(edges)
+    if e.size == 0:
+        e = np.zeros((0, 2), dtype=np.int64)
+    if e.ndim != 2 or e.shape[1] != 2:
+        raise ValueError("edges must be a sequence of (u, v) pairs")
+    if e.dtype not in (np.int32, np.int64):
+        e = e.astype(np.int64)
+    return np.ascontiguousarray(e)
+
+
 def stage_graph(ctx: _lib.Context, n: int, edges, layout: str = "auto") -> None:
     """Stage an (m, 2) edge array (numpy int32/int64 on the host, or a CUDA
     tensor) as packed uint32 SoA in HBM, with the graph.py:73-79 range check.
@@ -177,14 +188,7 @@ def stage_graph(ctx: _lib.Context, n: int, edges, layout: str = "auto") -> None:
                                              e.shape[0], n))
         m = e.shape[0]
     else:
-        e = np.asarray(edges)
-        if e.size == 0:
-            e = np.zeros((0, 2), dtype=np.int64)
-        if e.ndim != 2 or e.shape[1] != 2:
-            raise ValueError("edges must be a sequence of (u, v) pairs")
-        if e.dtype not in (np.int32, np.int64):
-            e = e.astype(np.int64)
-        e = np.ascontiguousarray(e)
+        e = _host_edges(edges)
         m = e.shape[0]
         _lib.check(lib.cc_stage_edges(ctx.handle, ctypes.c_void_p(e.ctypes.data),
                                       e.dtype.itemsize, m, n))
@@ -203,28 +207,74 @@ def run_staged(ctx: _lib.Context, schedule: Schedule, *, count_changes: bool = T
     execute the whole convergence loop as one CUDA-graph launch unless
     ``host_loop`` forces the per-sweep host loop."""
     n = ctx.n
-    cap = n + 2 if cap is None else int(cap)  # engine.py:275
-    capacity = max(1, min(cap, 1 << 12 if not count_changes else 1 << 16))
-    changed = np.zeros(capacity, dtype=np.int64)
-    secs = np.zeros(capacity, dtype=np.float64)
-    st = _lib.CCStats()
-    st.capacity = capacity
-    st.changed_per_sweep = changed.ctypes.data_as(_lib._I64P)
-    st.sweep_seconds = secs.ctypes.data_as(_lib._DBLP)
-    flags = ((_lib.CC_RUN_EARLY_CHECK if early_check else 0)
-             | (_lib.CC_RUN_COUNT_CHANGES if count_changes else 0)
-             | (_lib.CC_RUN_SWEEP_TIMES if sweep_times else 0)
-             | (_lib.CC_RUN_FIRST_SCATTER if first_scatter else 0)
-             | (_lib.CC_RUN_HOST_LOOP if host_loop else 0))
-    sched = _cc_schedule(schedule)
-    out_ptr, eb = None, 8
-    if labels_out is not None:
-        if labels_out.dtype not in (np.int64, np.uint32, np.int32) or labels_out.size != n:
-            raise ValueError("labels_out must be a length-n int64/int32/uint32 array")
-        eb = labels_out.dtype.itemsize
-        out_ptr = ctypes.c_void_p(labels_out.ctypes.data)
-    _lib.check(ctx.lib.cc_run(ctx.handle, ctypes.byref(sched), flags, cap, out_ptr, eb,
-                              ctypes.byref(st)))
+    call = _RunCall(n, schedule, count_changes, early_check, sweep_times, cap, labels_out,
+                    first_scatter, host_loop)
+    _lib.check(ctx.lib.cc_run(ctx.handle, ctypes.byref(call.sched), call.flags, call.cap,
+                              call.out_ptr, call.eb, ctypes.byref(call.st)))
+    return labels_out, call.stats()
+
+
+class _RunCall:
+    """Arguments and stats buffers of one cc_run / cc_run_host call."""
+
+    def __init__(self, n, schedule, count_changes, early_check, sweep_times, cap, labels_out,
+                 first_scatter=False, host_loop=False):
+        self.cap = n + 2 if cap is None else int(cap)  # engine.py:275
+        capacity = max(1, min(self.cap, 1 << 12 if not count_changes else 1 << 16))
+        self.changed = np.zeros(capacity, dtype=np.int64)
+        self.secs = np.zeros(capacity, dtype=np.float64)
+        st = _lib.CCStats()
+        st.capacity = capacity
+        st.changed_per_sweep = self.changed.ctypes.data_as(_lib._I64P)
+        st.sweep_seconds = self.secs.ctypes.data_as(_lib._DBLP)
+        self.st = st
+        self.flags = ((_lib.CC_RUN_EARLY_CHECK if early_check else 0)
+                      | (_lib.CC_RUN_COUNT_CHANGES if count_changes else 0)
+                      | (_lib.CC_RUN_SWEEP_TIMES if sweep_times else 0)
+                      | (_lib.CC_RUN_FIRST_SCATTER if first_scatter else 0)
+                      | (_lib.CC_RUN_HOST_LOOP if host_loop else 0))
+        self.sched = _cc_schedule(schedule)
+        self.out_ptr, self.eb = None, 8
+        if labels_out is not None:
+            if labels_out.dtype not in (np.int64, np.uint32, np.int32) or labels_out.size != n:
+                raise ValueError("labels_out must be a length-n int64/int32/uint32 array")
+            self.eb = labels_out.dtype.itemsize
+            self.out_ptr = ctypes.c_void_p(labels_out.ctypes.data)
+
+    def stats(self) -> IterationStats:
+        st, changed, secs = self.st, self.changed, self.secs
+        capacity = st.capacity
+        return _stats_from(st, changed, secs, capacity)
+
+
+def run_host(ctx: _lib.Context, n: int, edges, schedule: Schedule, *, layout: str = "auto",
+             count_changes: bool = True, early_check: bool = True, sweep_times: bool = True,
+             cap: Optional[int] = None, labels_out: Optional[np.ndarray] = None,
+             first_scatter: bool = False, host_loop: bool = False):
+    """Stage host edges and run in ONE call (cc_run_host): for asynchronous
+    runs in input / chunk-sorted order, sweep 1 runs chunk by chunk right
+    behind the host-to-device copy, so the transfer hides it; every other
+    case stages, then runs, exactly as stage_graph + run_staged.  Returns
+    (labels_out, IterationStats)."""
+    e = _host_edges(edges)
+    m = e.shape[0]
+    layout = resolve_layout(layout, m, n)
+    if layout not in ("input", "chunk_sorted"):
+        stage_graph(ctx, n, e, layout)
+        return run_staged(ctx, schedule, count_changes=count_changes, early_check=early_check,
+                          sweep_times=sweep_times, cap=cap, labels_out=labels_out,
+                          first_scatter=first_scatter, host_loop=host_loop)
+    ctx.set_option(_lib.CC_OPT_STAGE_LAYOUT, 2 if layout == "chunk_sorted" else 0)
+    call = _RunCall(n, schedule, count_changes, early_check, sweep_times, cap, labels_out,
+                    first_scatter, host_loop)
+    _lib.check(ctx.lib.cc_run_host(ctx.handle, ctypes.c_void_p(e.ctypes.data), e.dtype.itemsize,
+                                   m, n, ctypes.byref(call.sched), call.flags, call.cap,
+                                   call.out_ptr, call.eb, ctypes.byref(call.st)))
+    ctx.n, ctx.m = n, m
+    return labels_out, call.stats()
+
+
+def _stats_from(st, changed, secs, capacity) -> IterationStats:
     k = int(st.sweeps_executed)
     cnt = changed[:min(k, capacity)].tolist() + [-1] * max(0, k - capacity)
     sec = secs[:min(k, capacity)].tolist() + [0.0] * max(0, k - capacity)
@@ -233,7 +283,7 @@ def run_staged(ctx: _lib.Context, schedule: Schedule, *, count_changes: bool = T
         changed_per_sweep=[int(x) for x in cnt],
         converged_by="early-check" if st.converged_by == 1 else "change-flag",
         sweep_seconds=sec, device_seconds=float(st.converge_seconds))
-    return labels_out, stats
+    return stats
 
 
 def verify_staged(ctx: _lib.Context) -> int:
@@ -265,11 +315,17 @@ def run_contour(g, schedule: Schedule, threads: int = 1, seed: Optional[int] = N
     if n < 0:
         raise ValueError("vertex count must be non-negative")
     ctx = _context(device)
-    stage_graph(ctx, n, edges, layout)
     labels = np.empty(n, dtype=np.int64)
-    _, stats = run_staged(ctx, schedule, count_changes=count_changes, early_check=early_check,
-                          sweep_times=sweep_times, labels_out=labels, first_scatter=first_scatter,
-                          host_loop=host_loop)
+    if hasattr(edges, "data_ptr") and getattr(edges, "is_cuda", False):
+        stage_graph(ctx, n, edges, layout)
+        _, stats = run_staged(ctx, schedule, count_changes=count_changes,
+                              early_check=early_check, sweep_times=sweep_times,
+                              labels_out=labels, first_scatter=first_scatter,
+                              host_loop=host_loop)
+    else:
+        _, stats = run_host(ctx, n, edges, schedule, layout=layout, count_changes=count_changes,
+                            early_check=early_check, sweep_times=sweep_times, labels_out=labels,
+                            first_scatter=first_scatter, host_loop=host_loop)
     return labels, stats
 
 

@@ -385,6 +385,43 @@ def test_graph_loop_early_check(golden):
     assert "early-check" in seen
 
 
+def test_run_host_streamed_first_sweep(golden):
+    """cc_run_host: sweep 1 streamed behind the host-to-device copy, then the
+    loop from sweep 2 -- exact labels, consistent stats, errors as staging."""
+    cases = [(g["n"], np.asarray(g["edges"], dtype=np.int64).reshape(-1, 2), g["labels"])
+             for g in golden["graphs"][::2]]
+    for n, e in (graphgen.grid(300, 310, 0.55, 4), graphgen.rmat(15, 16, 9),
+                 graphgen.forest(60, 5), spec.erdos_renyi(40001, 90000, 3)):
+        cases.append((n, e, oracle.rem_union_find(n, e).tolist()))
+    ctx = _lib.Context(0)
+    ctx.set_option(_lib.CC_OPT_SORT_CHUNK, 4099)  # many chunks: many streamed pieces
+    for layout in ("input", "chunk_sorted"):
+        for n, e, exp in cases:
+            for variant, atomic, early in (("C-2", True, True), ("C-2", False, False),
+                                           ("C-1", True, True), ("C-m", True, False),
+                                           ("C-1m1m", True, True)):
+                sched = make_schedule(variant, 5, atomic=atomic)
+                labels = np.empty(n, dtype=np.int64)
+                _, st = engine.run_host(ctx, n, e, sched, layout=layout, count_changes=False,
+                                        early_check=early, labels_out=labels)
+                assert labels.tolist() == exp, (layout, variant, n)
+                check_invariants(labels, st)
+                if st.converged_by == "early-check":
+                    assert st.sweeps_until_stable == st.sweeps_executed
+                else:
+                    assert st.sweeps_until_stable == st.sweeps_executed - 1
+                assert engine.verify_staged(ctx) == 0
+    # a bad endpoint fails the call (the streamed sweep never saw it)
+    with pytest.raises(ValueError):
+        engine.run_host(ctx, 10, np.array([[0, 1], [2, 10]]), make_schedule("c2"),
+                        count_changes=False)
+    labels = np.empty(5, dtype=np.int64)
+    _, st = engine.run_host(ctx, 5, np.zeros((0, 2), np.int64), make_schedule("c2"),
+                            count_changes=False, labels_out=labels)
+    assert labels.tolist() == list(range(5)) and st.converged_by == "change-flag"
+    ctx.close()
+
+
 def test_graph_loop_cap_and_rebuild():
     ctx = _lib.Context(0)
     e = np.array([[5, 4], [4, 3], [3, 2], [2, 1], [1, 0]])
