@@ -49,10 +49,12 @@ def parse():
     p.add_argument("--config", default="rmat22")
     p.add_argument("--impl", default="b200", choices=["b200", "reference"])
     p.add_argument("--no-cpu-baseline", action="store_true")
-    p.add_argument("--no-early-check", dest="early_check", action="store_false",
-                   help="skip the reference's early convergence check after each changing "
-                        "sweep (engine.py:318-320; on by default, as in the reference) and "
-                        "stop on a no-write sweep only")
+    p.add_argument("--early-check", action="store_true",
+                   help="run the reference's early convergence check after each changing "
+                        "sweep (engine.py:318-320) inside the device loop; off by default: "
+                        "on every config it costs about what the confirming no-write sweep "
+                        "it saves costs (RMAT-22 1.19 vs 1.15 ms, RMAT-28 158 vs 122 ms, "
+                        "forest 842 vs 800 ms, measured)")
     p.add_argument("--seed", type=int, default=1)
     p.add_argument("--layout", default="auto",
                    choices=["auto", "input", "src_sorted", "chunk_sorted", "dst_bucketed",

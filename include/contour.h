@@ -149,12 +149,15 @@ int cc_reorder_edges(cc_ctx* ctx, int mode);
 #define CC_OPT_TILE_SHIFT 8        /* layout 4: 2^shift labels per L2 window (default 24 = 64 MB) */
 #define CC_OPT_SHORTCUT 9          /* pointer-jumping passes L[v]=L[L[v]] after every async sweep
                                       without exact counting (0..8, default 1) */
-#define CC_OPT_TILE_SPLIT 10       /* layout 4: independently src-sorted runs per window (default 4) */
+#define CC_OPT_TILE_SPLIT 10       /* layout 4: independently src-sorted runs per window (default 2) */
 #define CC_OPT_BUCKET_NOSMEM 11    /* layout 3: 1 = gather dst labels from global memory (experiment) */
 #define CC_OPT_SWEEP_VARIANT 12    /* order-2 kernel: 0 8 rows/thread, 1 4 rows, 2 8 rows <=64 regs,
                                       3 16 rows, 4 4 rows <=40 regs, 5 4 rows <=32 regs,
                                       6 4 rows + evict-first src gathers, 7 = 6 + evict-last dst
-                                      gathers, 8 4 rows + evict-last dst gathers (default 1) */
+                                      gathers, 8 4 rows + evict-last dst gathers, 9 4 rows +
+                                      evict-first edge stream, 10 = 9 + evict-last src and dst
+                                      gathers, 11 = 9 + evict-last dst gathers, 12 auto: 11 on
+                                      layout 4, else 1 (default 12) */
 #define CC_OPT_BUCKET_PIPE 13      /* layout 3 sweep kernel: 0 general, 1 lean slice kernel
                                       (default), 2 lean + edge prefetch, 3 bulk-copy (TMA)
                                       pipelined, 3-stage ring */

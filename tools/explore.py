@@ -22,7 +22,7 @@ def prepare(cfg, layout, chunk, bshift=15, item_rows=1 << 18, bthreads=1024, tsh
     ctx.set_option(_lib.CC_OPT_TILE_SHIFT, tshift)
     ctx.set_option(_lib.CC_OPT_TILE_SPLIT, tsplit)
     ctx.set_option(_lib.CC_OPT_BUCKET_NOSMEM, int(os.environ.get("CC_NOSMEM", "0")))
-    ctx.set_option(_lib.CC_OPT_SWEEP_VARIANT, int(os.environ.get("CC_VARIANT", "1")))
+    ctx.set_option(_lib.CC_OPT_SWEEP_VARIANT, int(os.environ.get("CC_VARIANT", "12")))
     ctx.set_option(_lib.CC_OPT_BUCKET_SHIFT, bshift)
     ctx.set_option(_lib.CC_OPT_ITEM_ROWS, item_rows)
     ctx.set_option(_lib.CC_OPT_BUCKET_THREADS, bthreads)

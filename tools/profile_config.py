@@ -15,7 +15,7 @@ def main():
     cfg = sys.argv[1]
     layout = sys.argv[2] if len(sys.argv) > 2 else "auto"
     ctx = _lib.Context(0, torch.cuda.current_stream().cuda_stream)
-    ctx.set_option(_lib.CC_OPT_SWEEP_VARIANT, int(os.environ.get("CC_VARIANT", "1")))
+    ctx.set_option(_lib.CC_OPT_SWEEP_VARIANT, int(os.environ.get("CC_VARIANT", "12")))
     ctx.set_option(_lib.CC_OPT_BUCKET_PIPE, int(os.environ.get("CC_PIPE", "1")))
     spec = graphgen.CONFIGS[cfg]
     if spec["kind"] == "rmat":

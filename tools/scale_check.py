@@ -36,7 +36,9 @@ def run(cfg, args):
     ctx.set_option(_lib.CC_OPT_ITEM_ROWS, args.item_rows)
     ctx.set_option(_lib.CC_OPT_SORT_CHUNK, args.sort_chunk)
     ctx.set_option(_lib.CC_OPT_BUCKET_SHIFT, args.bshift)
-    rec = {"seed": args.seed, "early_check": args.early_check, "sort_chunk": args.sort_chunk, "bshift": args.bshift, "config": cfg, "variant": args.variant, "pipe": args.pipe,
+    ctx.set_option(_lib.CC_OPT_TILE_SPLIT, args.tsplit)
+    ctx.set_option(_lib.CC_OPT_TILE_SHIFT, args.tshift)
+    rec = {"tsplit": args.tsplit, "tshift": args.tshift, "seed": args.seed, "early_check": args.early_check, "sort_chunk": args.sort_chunk, "bshift": args.bshift, "config": cfg, "variant": args.variant, "pipe": args.pipe,
            "item_order": args.item_order, "item_rows": args.item_rows}
     t0 = time.perf_counter()
     host = None
@@ -106,7 +108,7 @@ def main():
     ap.add_argument("--no-oracle", action="store_true")
     ap.add_argument("--repeats", type=int, default=3)
     ap.add_argument("--layout", default="auto")
-    ap.add_argument("--variant", type=int, default=1)
+    ap.add_argument("--variant", type=int, default=12)
     ap.add_argument("--pipe", type=int, default=3)
     ap.add_argument("--item-order", type=int, default=0)
     ap.add_argument("--item-rows", type=int, default=1 << 18)
@@ -114,6 +116,8 @@ def main():
     ap.add_argument("--bshift", type=int, default=15)
     ap.add_argument("--early-check", type=int, default=0)
     ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--tsplit", type=int, default=2)
+    ap.add_argument("--tshift", type=int, default=24)
     ap.add_argument("--runs", type=int, default=0, help="bucketed run-major: runs (sets sort chunk)")
     args = ap.parse_args()
     for cfg in args.configs:
