@@ -243,13 +243,20 @@ def main():
         return run_reference_arm(args)
     rank, world, local = dist_env()
     import torch
+    ndev = max(1, torch.cuda.device_count())
+    # more ranks than GPUs only as a plumbing check (ranks share a GPU; their
+    # kernels never wait on one another, the host flag exchange uses gloo)
+    local, backend = (local, "nccl") if world <= ndev else (local % ndev, "gloo")
     torch.cuda.set_device(local)
     if world > 1 or args.sharded:
         import torch.distributed as dist
         if "MASTER_ADDR" not in os.environ:  # --sharded without torchrun: one local rank
             os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT="29533", RANK="0",
                               WORLD_SIZE="1")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
         return run_multi(args, rank, world, local)
     return run_single(args, local)
 
@@ -430,9 +437,7 @@ def run_multi(args, rank, world, device):
     import torch
     import torch.distributed as dist
 
-    from paper_2311_02811_b200 import distributed
-
-    from paper_2311_02811_b200 import engine
+    from paper_2311_02811_b200 import distributed, engine, graphgen
 
     spec = config_spec(args.config)
     if spec["kind"] != "rmat":
@@ -472,15 +477,48 @@ def run_multi(args, rank, world, device):
     ev1.record(stream)
     torch.cuda.synchronize()
     dist.barrier()
-    ms_local = ev0.elapsed_time(ev1) / args.steps
-    t = torch.tensor([ms_local], dtype=torch.float64, device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms = float(t.item())
+    tdev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+
+    def max_over_ranks(x):
+        t = torch.tensor([x], dtype=torch.float64, device=tdev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
     clk = clocks.stop() if clocks else None
     # certificate over all shards: every rank checks its edges on its replica
-    bad = torch.tensor([engine.verify_staged(runner.shard.ctx)], dtype=torch.int32,
-                       device="cuda")
-    dist.all_reduce(bad, op=dist.ReduceOp.MAX)
+    bad = max_over_ranks(engine.verify_staged(runner.shard.ctx))
+
+    # ---- e2e at N GPUs: every rank stages ITS host shard (pinned int32, its
+    # own PCIe link) and the ranks run to convergence; rank 0 reads the int64
+    # labels back.  Time = max over ranks of the per-rank CUDA-event time.
+    e2e = None
+    if not args.no_e2e:
+        lo, hi = distributed.shard_rows(m_total, rank, world)
+        host_t = torch.empty((hi - lo, 2), dtype=torch.int32, pin_memory=True)
+        graphgen.rmat(spec["scale"], spec.get("edgefactor", 16), args.seed, elem_bytes=4,
+                      row_lo=lo, row_hi=hi, out=host_t.numpy())
+        labels_t = torch.empty(n if rank == 0 else 1, dtype=torch.int64, pin_memory=True)
+        times = []
+        for i in range(args.warmup + args.steps):
+            dist.barrier()
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            runner.stage_host(host_t.numpy(), args.layout)
+            runner.run()
+            if rank == 0:
+                runner.read_labels(labels_t.numpy())
+            b.record(stream)
+            torch.cuda.synchronize()
+            if i >= args.warmup:
+                times.append(a.elapsed_time(b) / 1e3)
+        e2e_s = max_over_ranks(sum(times) / len(times))
+        e2e = {"value": m_total / e2e_s, "unit": UNIT,
+               "h2d_bytes_per_step": int(m_total * 8), "d2h_bytes_per_step": int(n * 8),
+               "seconds_per_step": e2e_s,
+               "path": "per rank: cc_stage_edges(pinned int32 shard, chunk-sorted while "
+                       "copying) + the sharded run; rank 0: labels -> pinned int64"}
     fused = isinstance(runner, distributed.FusedShardedContour)
     if fused:
         sched = (f"C-2 async atomic={bool(args.atomic)}, fused sweep + red.min into the peer "
@@ -503,7 +541,8 @@ def run_multi(args, rank, world, device):
                        "parallelism": f"edge-sharded x{world}, labels replicated",
                        "l2": "inputs larger than L2"},
             "exchanges_per_run": rounds,
-            "verified": int(bad.item()) == 0,
+            "verified": int(bad) == 0,
+            "e2e": e2e,
             "gpu_launches": launches,
             "clocks": clk,
         }

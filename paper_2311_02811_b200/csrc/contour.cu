@@ -181,13 +181,36 @@ __global__ void k_check_le(const lab_t* L, int64_t n, int* flags) {
 
 // Pointer-jumping compress L[v] = L[L[v]] (north-star step 4; the semantic
 // model is normalize_labels, baselines.py:146-152).
-__global__ void k_compress(lab_t* L, int64_t n, int* flags) {
+// Four labels per thread per iteration (one uint4 load, four independent
+// gathers): the pass is latency-bound on the dependent L[L[x]] load, so ILP
+// is what makes it fast (grid 4096^2: 41 -> see DESIGN 5.14).  Lowerings
+// use red.min: L[L[x]] <= L[x] always, and a concurrent writer (a peer GPU's
+// fused exchange) can never be overwritten by a larger value.
+// gate != nullptr: return at once if *gate == 0 (the graph loop's shortcut
+// after a sweep that wrote nothing, and its final pass after a loop that
+// ended on a no-write order >= 2 sweep or a passed early check -- the labels
+// are idempotent then).
+__global__ void __launch_bounds__(kThreads) k_compress(lab_t* L, int64_t n, int* flags,
+                                                       const int* gate = nullptr) {
+    if (gate && *(volatile const int*)gate == 0) return;
     bool ch = false;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t nv = n >> 2;
+    const uint4* L4 = reinterpret_cast<const uint4*>(L);
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (int64_t q = tid; q < nv; q += stride) {
+        const uint4 l = L4[q];
+        const lab_t a = L[l.x], b = L[l.y], c = L[l.z], d = L[l.w];
+        lab_t* p = L + 4 * q;
+        if (a != l.x) { atomicMin(p + 0, a); ch = true; }
+        if (b != l.y) { atomicMin(p + 1, b); ch = true; }
+        if (c != l.z) { atomicMin(p + 2, c); ch = true; }
+        if (d != l.w) { atomicMin(p + 3, d); ch = true; }
+    }
+    for (int64_t i = (nv << 2) + tid; i < n; i += stride) {
         const lab_t l = L[i];
         const lab_t ll = L[l];
-        if (ll != l) { L[i] = ll; ch = true; }
+        if (ll != l) { atomicMin(L + i, ll); ch = true; }
     }
     if (__syncthreads_or(ch) && threadIdx.x == 0) flags[kFlagCompress] = 1;
 }
@@ -400,6 +423,7 @@ struct LoopState {
     int converged;        // last sweep lowered nothing
     int capped;           // sweep cap reached while still changing
     int by_check;         // stopped by the early check (not the change flag)
+    int need_compress;    // the final pointer-jumping pass can change something
     unsigned long long t0;
 };
 struct SweepRec {
@@ -434,6 +458,7 @@ __global__ void k_loop_init(LoopState* st, int* flags, cc_schedule s, long long 
     st->converged = 0;
     st->capped = 0;
     st->by_check = 0;
+    st->need_compress = 1;
     flags[kFlagWrote] = 0;
     flags[kFlagCheck] = 0;
     flags[kFlagCompress] = 0;
@@ -454,10 +479,13 @@ __global__ void k_loop_control(LoopState* st, SweepRec* rec, int* flags, cc_sche
     }
     if (!wrote) {
         st->converged = 1;
+        // a no-write sweep of order >= 2 leaves every endpoint's parent a root
+        st->need_compress = st->order >= 2 ? 0 : 1;
         cudaGraphSetConditional(h, 0);
     } else if (check && !bad) {  // engine.py:318-320
         st->converged = 1;
         st->by_check = 1;
+        st->need_compress = 0;  // the check proved L[L[x]] == L[x]
         cudaGraphSetConditional(h, 0);
     } else if (k >= cap) {
         st->capped = 1;
@@ -971,7 +999,7 @@ int compress(cc_ctx* c, int* rounds) {
     if (c->n > 0) {
         for (int it = 0; it < 70; ++it) {
             CUDA_TRY(cudaMemsetAsync(c->dflags + kFlagCompress, 0, sizeof(int), c->stream));
-            k_compress<<<grid_for(c, c->n), kThreads, 0, c->stream>>>(c->labels, c->n, c->dflags);
+            k_compress<<<grid_for(c, (c->n + 3) / 4), kThreads, 0, c->stream>>>(c->labels, c->n, c->dflags);
             CUDA_TRY(cudaGetLastError());
             CC_TRY(read_flags(c));
             if (!c->hflags[kFlagCompress]) break;
@@ -1056,7 +1084,8 @@ int build_loop(cc_ctx* c, const cc_schedule* s, int64_t cap, int sm, int check, 
                                            cudaStreamCaptureModeRelaxed));
     CC_TRY(launch_guarded(c, s, sm, c->body_stream));
     for (int j = 0; j < c->shortcut; ++j)
-        k_compress<<<grid_for(c, c->n), kThreads, 0, c->body_stream>>>(c->labels, c->n, c->dflags);
+        k_compress<<<grid_for(c, (c->n + 3) / 4), kThreads, 0, c->body_stream>>>(
+            c->labels, c->n, c->dflags, c->dflags + kFlagWrote);
     if (check) {
         k_gcheck_idem<<<grid_for(c, c->n), kThreads, 0, c->body_stream>>>(c->labels, c->n,
                                                                           c->dflags);
@@ -1071,7 +1100,8 @@ int build_loop(cc_ctx* c, const cc_schedule* s, int64_t cap, int sm, int check, 
     CUDA_TRY(cudaGetLastError());
     cudaGraph_t body_out = nullptr;
     CUDA_TRY(cudaStreamEndCapture(c->body_stream, &body_out));
-    k_compress<<<grid_for(c, c->n), kThreads, 0, cs>>>(c->labels, c->n, c->dflags);
+    k_compress<<<grid_for(c, (c->n + 3) / 4), kThreads, 0, cs>>>(c->labels, c->n, c->dflags,
+                                                                 &c->dstate->need_compress);
     CUDA_TRY(cudaStreamEndCapture(cs, &c->loop_graph));
     CUDA_TRY(cudaGraphInstantiate(&c->loop_exec, c->loop_graph, 0));
     k = {c->src, c->dst,   c->labels, c->m,     c->n,       cap,   *s,
@@ -1271,7 +1301,7 @@ int stage_impl(cc_ctx* c, const T* edges, int64_t m, bool host,
     if (ss) {
         // sweep 1's shortcut and early check, in the same synchronisation
         for (int j = 0; j < c->shortcut; ++j)
-            k_compress<<<grid_for(c, c->n), kThreads, 0, c->stream>>>(c->labels, c->n,
+            k_compress<<<grid_for(c, (c->n + 3) / 4), kThreads, 0, c->stream>>>(c->labels, c->n,
                                                                       c->dflags);
         if (ss_check) {
             k_gcheck_idem<<<grid_for(c, c->n), kThreads, 0, c->stream>>>(c->labels, c->n,
@@ -1413,6 +1443,7 @@ int cc_attach_soa(cc_ctx* c, uint32_t* src, uint32_t* dst, int64_t m, int64_t n)
 
 int cc_attach_labels(cc_ctx* c, uint32_t* labels) {
     if (!c || !labels) return fail(CC_EINVAL, "null argument");
+    if ((uintptr_t)labels & 15) return fail(CC_EINVAL, "label buffer must be 16-byte aligned");
     std::lock_guard<std::mutex> lk(c->mu);
     if (c->own_labels && c->labels) cudaFree(c->labels);
     c->labels = labels;
@@ -1466,7 +1497,7 @@ int cc_shortcut(cc_ctx* c, int passes) {
     std::lock_guard<std::mutex> lk(c->mu);
     DeviceGuard g(c->device);
     for (int j = 0; j < passes && c->n > 0; ++j)
-        k_compress<<<grid_for(c, c->n), kThreads, 0, c->stream>>>(c->labels, c->n, c->dflags);
+        k_compress<<<grid_for(c, (c->n + 3) / 4), kThreads, 0, c->stream>>>(c->labels, c->n, c->dflags);
     CUDA_TRY(cudaGetLastError());
     return CC_OK;
 }
@@ -1567,7 +1598,7 @@ int run_impl(cc_ctx* c, const cc_schedule* s, int flags, int64_t cap, void* labe
         CC_TRY(enqueue_sweep(c, order, sync, s->atomic, count, sweep == 1 && first_scatter));
         if (!sync && !count)
             for (int j = 0; j < c->shortcut; ++j)
-                k_compress<<<grid_for(c, c->n), kThreads, 0, c->stream>>>(c->labels, c->n,
+                k_compress<<<grid_for(c, (c->n + 3) / 4), kThreads, 0, c->stream>>>(c->labels, c->n,
                                                                           c->dflags);
         if (times) CUDA_TRY(cudaEventRecord(c->ev1, c->stream));
         CC_TRY(read_flags(c));

@@ -98,7 +98,23 @@ class PeerShard:
         self.peer_ptrs = []
 
 
-class FusedShardedContour:
+class _HostIO:
+    """Host-side input/output of a per-rank driver (the end-to-end path)."""
+
+    def stage_host(self, edges, layout: str = "auto") -> None:
+        """Stage this rank's host edge shard on its GPU (own PCIe link); the
+        label buffer -- and so any peer mapping of it -- is kept."""
+        from .engine import stage_graph
+        stage_graph(self.shard.ctx, self.n, edges, layout)
+
+    def read_labels(self, out) -> None:
+        """Copy the (converged) label replica into a host array of n
+        int64/int32 entries."""
+        _lib.check(self.shard.ctx.lib.cc_read_labels(
+            self.shard.ctx.handle, ctypes.c_void_p(out.ctypes.data), out.dtype.itemsize))
+
+
+class FusedShardedContour(_HostIO):
     """Per-rank driver of the fused exchange: init; barrier; then rounds of
     one fused order-2 sweep + a MAX all-reduce of the local "wrote" bit until
     no rank lowered anything (every replica then equals the min over all
@@ -175,7 +191,7 @@ def nccl_allreduce_min(group=None):
     return reduce
 
 
-class ShardedContour:
+class ShardedContour(_HostIO):
     """Per-rank driver.  ``allreduce`` performs the in-place MIN exchange of
     the (n+1)-slot label tensor (default: torch.distributed over the default
     NCCL/gloo group)."""
