@@ -37,8 +37,10 @@ def run(cfg, args):
     ctx.set_option(_lib.CC_OPT_SORT_CHUNK, args.sort_chunk)
     ctx.set_option(_lib.CC_OPT_BUCKET_SHIFT, args.bshift)
     ctx.set_option(_lib.CC_OPT_TILE_SPLIT, args.tsplit)
+    ctx.set_option(_lib.CC_OPT_SHORTCUT, args.shortcut)
     ctx.set_option(_lib.CC_OPT_TILE_SHIFT, args.tshift)
-    rec = {"tsplit": args.tsplit, "tshift": args.tshift, "seed": args.seed, "early_check": args.early_check, "sort_chunk": args.sort_chunk, "bshift": args.bshift, "config": cfg, "variant": args.variant, "pipe": args.pipe,
+    rec = {"first_scatter": args.first_scatter, "host_loop": args.host_loop,
+           "shortcut": args.shortcut, "tsplit": args.tsplit, "tshift": args.tshift, "seed": args.seed, "early_check": args.early_check, "sort_chunk": args.sort_chunk, "bshift": args.bshift, "config": cfg, "variant": args.variant, "pipe": args.pipe,
            "item_order": args.item_order, "item_rows": args.item_rows}
     t0 = time.perf_counter()
     host = None
@@ -62,7 +64,9 @@ def run(cfg, args):
     sched = make_schedule("c2")
     runs = []
     for _ in range(args.repeats):
-        _, st = engine.run_staged(ctx, sched, count_changes=False, early_check=args.early_check)
+        _, st = engine.run_staged(ctx, sched, count_changes=False, early_check=args.early_check,
+                                  first_scatter=bool(args.first_scatter),
+                                  host_loop=bool(args.host_loop))
         runs.append(st)
     best = min(runs, key=lambda s: s.device_seconds)
     rec.update(device_s=best.device_seconds, edges_per_s=m / best.device_seconds,
@@ -117,6 +121,9 @@ def main():
     ap.add_argument("--early-check", type=int, default=0)
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--tsplit", type=int, default=2)
+    ap.add_argument("--shortcut", type=int, default=1)
+    ap.add_argument("--first-scatter", type=int, default=0)
+    ap.add_argument("--host-loop", type=int, default=0)
     ap.add_argument("--tshift", type=int, default=24)
     ap.add_argument("--runs", type=int, default=0, help="bucketed run-major: runs (sets sort chunk)")
     args = ap.parse_args()
