@@ -479,8 +479,10 @@ __global__ void k_loop_control(LoopState* st, SweepRec* rec, int* flags, cc_sche
     }
     if (!wrote) {
         st->converged = 1;
-        // a no-write sweep of order >= 2 leaves every endpoint's parent a root
-        st->need_compress = st->order >= 2 ? 0 : 1;
+        // after a no-write sweep of any order every edge has L[u] == L[v], so
+        // each component holds one common value, a member whose label is
+        // itself: the labels are final
+        st->need_compress = 0;
         cudaGraphSetConditional(h, 0);
     } else if (check && !bad) {  // engine.py:318-320
         st->converged = 1;
@@ -1150,9 +1152,8 @@ int run_graph(cc_ctx* c, const cc_schedule* s, int64_t cap, void* labels_out, in
         }
     }
     int rounds = 0;
-    // the post-loop pass changed something: only possible when the last
-    // sweep was order 1 (a no-write order >= 2 sweep or a passed early check
-    // leaves idempotent labels)
+    // the post-loop pass is gated off (final labels after a no-write sweep or
+    // a passed check); should it ever change something, finish on the host
     if (c->hflags[kFlagCompress]) {
         CC_TRY(compress(c, &rounds));
         ++rounds;
