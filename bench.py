@@ -49,16 +49,17 @@ def parse():
     p.add_argument("--config", default="rmat22")
     p.add_argument("--impl", default="b200", choices=["b200", "reference"])
     p.add_argument("--no-cpu-baseline", action="store_true")
-    p.add_argument("--early-check", action="store_true",
-                   help="run the reference's early convergence check after each changing "
-                        "sweep (engine.py:318-320) inside the device loop; off by default: "
-                        "on every config it costs about what the confirming no-write sweep "
-                        "it saves costs (RMAT-22 1.19 vs 1.15 ms, RMAT-28 158 vs 122 ms, "
-                        "forest 842 vs 800 ms, measured)")
+    p.add_argument("--early-check", default="auto", choices=["auto", "on", "off"],
+                   help="the reference's early convergence check after each changing sweep "
+                        "(engine.py:318-320), inside the device loop.  auto: on for the hybrid "
+                        "layout, whose shared-memory check (0.28 ms on RMAT-22) is cheaper "
+                        "than the confirming sweep it saves; off elsewhere, where the check "
+                        "costs what that sweep costs (RMAT-22 1.19 vs 1.15 ms, RMAT-28 158 vs "
+                        "122 ms, forest 842 vs 800 ms, measured)")
     p.add_argument("--seed", type=int, default=1)
     p.add_argument("--layout", default="auto",
                    choices=["auto", "input", "src_sorted", "chunk_sorted", "dst_bucketed",
-                            "l2_tiled"],
+                            "l2_tiled", "hybrid"],
                    help="staging-time edge layout (auto: chunk_sorted -- each 2^23-row chunk "
                         "radix-sorted by src on device while the next chunk is copied in -- "
                         "when the labels fit L2, l2_tiled windows otherwise)")
@@ -277,19 +278,29 @@ def run_single(args, device):
         ctx.set_option(_lib.CC_OPT_STORE_MODE_ATOMIC if args.atomic else
                        _lib.CC_OPT_STORE_MODE_PLAIN, args.store_mode)
     # ---- inputs resident in HBM in the staged layout (not timed)
+    layout_arg = args.layout
     if spec["kind"] == "rmat":
         n, m = graphgen.rmat_device(ctx, spec["scale"], spec.get("edgefactor", 16), args.seed)
         args.layout = engine.resolve_layout(args.layout, m, n)
         if args.layout != "input":
-            _lib.check(ctx.lib.cc_reorder_edges(ctx.handle, engine.LAYOUTS[args.layout]))
+            engine.apply_layout(ctx, args.layout)
         host_edges = None
     else:
         n, host_edges = graphgen.make(spec, args.seed, elem_bytes=4)
         m = host_edges.shape[0]
         args.layout = engine.resolve_layout(args.layout, m, n)
         engine.stage_graph(ctx, n, host_edges, args.layout)
+    # e2e is a one-shot run from host memory: "auto" keeps chunk-sorted rows
+    # there so sweep 1 streams behind the copy (engine.resolve_layout)
+    e2e_layout = engine.resolve_layout(layout_arg, m, n, resident=False)
+
+    def early_for(layout):
+        return args.early_check == "on" or (args.early_check == "auto" and layout == "hybrid")
+
+    args.early = early_for(args.layout)
+    hybrid = args.layout == "hybrid"
     sched = make_schedule("c2", atomic=bool(args.atomic))
-    kw = dict(count_changes=False, early_check=args.early_check,
+    kw = dict(count_changes=False, early_check=args.early,
               first_scatter=args.first_scatter, host_loop=args.host_loop)
 
     for _ in range(args.warmup):
@@ -315,25 +326,33 @@ def run_single(args, device):
 
     sweeps = [s.sweeps_executed for s in stats]
     shortcut = 1  # CC_OPT_SHORTCUT default: one pointer-jumping pass after every sweep
-    check = 2 if args.early_check else 0  # idempotence + edge-agreement kernels
+    check = 2 if args.early else 0  # idempotence + edge-agreement kernels
     if args.host_loop:  # iota + (sweep + shortcut + check) per sweep + compress
         launches = sum(2 + s.sweeps_executed * (1 + shortcut + check) for s in stats)
-    else:  # iota + loop_init + (sweep + shortcut + check + control) per sweep + compress
-        launches = sum(3 + s.sweeps_executed * (2 + shortcut + check) for s in stats)
+    else:  # iota + loop_init + (guarded sweeps + shortcut + check + control) per sweep + compress
+        per = (2 if hybrid else 1) + shortcut + check + 1
+        launches = sum(3 + s.sweeps_executed * per for s in stats)
 
-    # ---- roofline of the sweep kernel: its own launch time, CUDA events on
-    # the launching stream around each sweep (+ its shortcut pass) in the
-    # host-driven loop -- the graph loop's per-sweep records include the check
-    rt = []
+    # ---- roofline of the sweep kernels: their own launch times, CUDA events
+    # on the launching stream around each sweep (+ its shortcut pass) in
+    # host-driven runs without the check (the graph loop's per-sweep records
+    # include control and check kernels).  Hybrid layout: sweep 1 is the
+    # chunk-sorted kernel, later sweeps the shared-memory slice kernel.
+    rt1, rt2 = [], []
     for _ in range(max(1, min(args.steps, 3))):
         _, st = engine.run_staged(ctx, sched, sweep_times=True, count_changes=False,
-                                  early_check=args.early_check, host_loop=True)
-        rt.extend(st.sweep_seconds)
-    t_sweep = sum(rt) / len(rt)
+                                  early_check=False, host_loop=True)
+        if hybrid:
+            rt1.append(st.sweep_seconds[0])
+            rt2.extend(st.sweep_seconds[1:])
+        else:
+            rt1.extend(st.sweep_seconds)
+    t_sweep = sum(rt1) / len(rt1)
     b_sweep = 8 * m + 4 * n  # edge stream + one label-array read
     achieved = b_sweep / t_sweep / 1e9
     peak, peak_src = peak_hbm()
     traffic = (load_traffic().get(args.config) or {}).get("dram_bytes_per_launch")
+    rt = rt1
 
     # ---- the paper's comparison baseline on the same device and staged edges:
     # GPU FastSV (baselines.py:81-131), not part of `value`
@@ -367,6 +386,7 @@ def run_single(args, device):
         t.numpy()[:] = host_edges
         host_edges = t.numpy()
     e2e = None
+    e2e_kw = dict(kw, early_check=early_for(e2e_layout))
     if not args.no_e2e:
         labels_t = torch.empty(n, dtype=torch.int64, pin_memory=True)
         labels_host = labels_t.numpy()
@@ -377,8 +397,8 @@ def run_single(args, device):
             a.record(stream)
             # run_contour's host-graph path: one cc_run_host call (sweep 1
             # streamed behind the copy where the layout allows it)
-            engine.run_host(ctx, n, host_edges, sched, layout=args.layout, sweep_times=False,
-                            labels_out=labels_host, **kw)
+            engine.run_host(ctx, n, host_edges, sched, layout=e2e_layout, sweep_times=False,
+                            labels_out=labels_host, **e2e_kw)
             b.record(stream)
             torch.cuda.synchronize()
             if i >= args.warmup:
@@ -408,9 +428,10 @@ def run_single(args, device):
         "vs_baseline": None, "dtype": "u32", "data": "synthetic",
         "config": {"workload": workload_name(args.config, n, m), "n": n, "m_input": m,
                    "schedule": f"C-2 async atomic={bool(args.atomic)}, ballot/OR flag"
-                               + (", early check" if args.early_check else "")
+                               + (", early check (engine.py:318-320)" if args.early else "")
                                + (", load-free sweep 1" if args.first_scatter else ""),
                    "layout": args.layout,
+                   "e2e_layout": e2e_layout,
                    "parallelism": "single GPU",
                    "l2": "inputs larger than L2 (edge stream 8m B > 126 MB); no flush"},
         "sweeps_per_run": sweeps,
@@ -423,6 +444,13 @@ def run_single(args, device):
                      "launch_ms": [round(t * 1e3, 4) for t in rt],
                      "bytes_per_launch": b_sweep, "avg_launch_s": t_sweep,
                      "peak_source": peak_src},
+        # hybrid layout: the later sweeps' kernel (shared-memory dst slices)
+        "roofline_slice_kernel": None if not rt2 else {
+            "bound": "hbm", "kernel": "cck::k_sweep_slice<3, true> (dst-bucketed copy, dst labels "
+                                      "in shared memory) + one shortcut pass",
+            "achieved": b_sweep / (sum(rt2) / len(rt2)) / 1e9, "peak": peak, "unit": "GB/s",
+            "frac": b_sweep / (sum(rt2) / len(rt2)) / 1e9 / peak,
+            "launch_ms": [round(t * 1e3, 4) for t in rt2]},
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": launches,

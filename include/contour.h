@@ -134,7 +134,10 @@ int cc_sweep(cc_ctx* ctx, int order, int sync, int atomic, int first, int* wrote
  * mode 4 partitions rows by dst into L2-sized windows of 2^CC_OPT_TILE_SHIFT
  * vertices and sorts each window's rows by src (any m; 8m bytes scratch), so
  * a grid-stride sweep gathers dst labels from one L2-resident window at a
- * time -- for label arrays larger than L2 (RMAT-28: 1 GB). */
+ * time -- for label arrays larger than L2 (RMAT-28: 1 GB); mode 5 (hybrid)
+ * keeps the current row order for sweep 1 and builds a mode-3 copy of the
+ * rows (8m more bytes) that the later order-2 sweeps and checks walk with
+ * shared-memory dst slices. */
 int cc_reorder_edges(cc_ctx* ctx, int mode);
 
 /* Tuning knobs of a context.  Store modes for async sweeps:
@@ -158,8 +161,8 @@ int cc_reorder_edges(cc_ctx* ctx, int mode);
                                       evict-first edge stream, 10 = 9 + evict-last src and dst
                                       gathers, 11 = 9 + evict-last dst gathers, 12 auto: 11 on
                                       layout 4, else 1 (default 12) */
-#define CC_OPT_BUCKET_PIPE 13      /* layout 3 sweep kernel: 0 general, 1 lean slice kernel
-                                      (default), 2 lean + edge prefetch, 3 bulk-copy (TMA)
+#define CC_OPT_BUCKET_PIPE 13      /* layout 3/5 sweep kernel: 0 general, 1 lean slice kernel,
+                                      2 lean + edge prefetch (default), 3 bulk-copy (TMA)
                                       pipelined, 3-stage ring */
 #define CC_OPT_ITEM_ORDER 14       /* layout 3: 0 bucket-major work items (default), 1 run-major:
                                       rows cut into sort_chunk runs in input order, items ordered

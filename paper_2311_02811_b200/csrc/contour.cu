@@ -424,6 +424,8 @@ struct LoopState {
     int capped;           // sweep cap reached while still changing
     int by_check;         // stopped by the early check (not the change flag)
     int need_compress;    // the final pointer-jumping pass can change something
+    int order_first;      // layout 5 guards: the next sweep's order if it is sweep 1, else 0
+    int order_rest;       // ... if it is a later sweep, else 0
     unsigned long long t0;
 };
 struct SweepRec {
@@ -455,6 +457,8 @@ __device__ __forceinline__ int order_for_dev(const cc_schedule& s, long long swe
 __global__ void k_loop_init(LoopState* st, int* flags, cc_schedule s, long long start) {
     st->sweep = start;
     st->order = order_for_dev(s, start + 1);
+    st->order_first = start == 0 ? st->order : 0;
+    st->order_rest = start == 0 ? 0 : st->order;
     st->converged = 0;
     st->capped = 0;
     st->by_check = 0;
@@ -494,6 +498,8 @@ __global__ void k_loop_control(LoopState* st, SweepRec* rec, int* flags, cc_sche
         cudaGraphSetConditional(h, 0);
     } else {
         st->order = order_for_dev(s, k + 1);
+        st->order_first = 0;
+        st->order_rest = st->order;
         cudaGraphSetConditional(h, 1);
     }
 }
@@ -553,9 +559,12 @@ struct cc_ctx {
     cck::PeerSet peers = {};  // peer label replicas for the fused sweep + exchange
     int64_t item_rows = (int64_t)1 << 18;     // layout 3: rows per work item
     int bucket_threads = 1024;
-    int bucket_pipe = 1;  // layout 3 kernel (launch_bucketed)
+    int bucket_pipe = 2;  // layout 3/5 kernel (launch_bucketed): lean + edge prefetch
     int item_order = 0;   // layout 3: 0 bucket-major items, 1 run-major (see reorder_bucketed)
-    cck::BucketItem* items = nullptr;         // layout 3 work items (device)
+    cck::BucketItem* items = nullptr;         // layout 3/5 work items (device)
+    lab_t* bsrc = nullptr;                    // layout 5: dst-bucketed copy of the rows
+    lab_t* bdst = nullptr;
+    int64_t bcap = 0;
     int n_items = 0;
     int stage_layout = 0;                     // layout applied by cc_stage_edges*
     lab_t* sort_ks = nullptr;                 // cached radix-sort scratch
@@ -585,6 +594,7 @@ struct cc_ctx {
         const void* items;
         int n_items;
         int resume;
+        const void* bsrc;
     } loop_key = {};
     std::mutex mu;
 };
@@ -622,6 +632,12 @@ struct SweepLaunch {
     int64_t off = 0;
     int64_t rows = -1;
 };
+
+// Rows the bucketed kernels walk: the rows themselves (layout 3) or the
+// dst-bucketed copy kept next to the chunk-sorted rows (layout 5).
+const lab_t* bucket_src(const cc_ctx* c) { return c->layout == 5 ? c->bsrc : c->src; }
+const lab_t* bucket_dst(const cc_ctx* c) { return c->layout == 5 ? c->bdst : c->dst; }
+bool has_buckets(const cc_ctx* c) { return (c->layout == 3 || c->layout == 5) && c->items; }
 
 template <int OK, int SM, int NV, int MINB = 1>
 int launch_sweep_t(cc_ctx* c, const lab_t* R, lab_t* T, int order, SweepLaunch sl) {
@@ -813,7 +829,8 @@ int launch_bucketed_t(cc_ctx* c, SweepLaunch sl) {
     if (occ < 1) occ = 1;
     const int blocks = std::min<int64_t>(c->n_items, (int64_t)c->sm_count * occ);
     cck::k_sweep_bucketed<SM, U><<<std::max(blocks, 1), c->bucket_threads, smem, sl.stream>>>(
-        c->src, c->dst, c->labels, c->items, c->n_items, c->dflags + kFlagWrote, sl.d_order);
+        bucket_src(c), bucket_dst(c), c->labels, c->items, c->n_items, c->dflags + kFlagWrote,
+        sl.d_order);
     CUDA_TRY(cudaGetLastError());
     return CC_OK;
 }
@@ -838,7 +855,8 @@ int launch_check_slice(cc_ctx* c, cudaStream_t st) {
     }
     const int blocks = (int)std::min<int64_t>(c->n_items, (int64_t)c->sm_count);
     cck::k_check_slice<<<std::max(blocks, 1), cck::kBT, smem, st>>>(
-        c->src, c->dst, c->labels, c->items, c->n_items, c->dflags, kFlagWrote, kFlagCheck);
+        bucket_src(c), bucket_dst(c), c->labels, c->items, c->n_items, c->dflags, kFlagWrote,
+        kFlagCheck);
     CUDA_TRY(cudaGetLastError());
     return CC_OK;
 }
@@ -855,7 +873,8 @@ int launch_bucketed_pipe_t(cc_ctx* c, SweepLaunch sl) {
     }
     const int blocks = (int)std::min<int64_t>(c->n_items, (int64_t)c->sm_count);
     cck::k_sweep_bucketed_tma<SM, NS><<<std::max(blocks, 1), cck::kBT, smem, sl.stream>>>(
-        c->src, c->dst, c->labels, c->items, c->n_items, c->dflags + kFlagWrote, sl.d_order);
+        bucket_src(c), bucket_dst(c), c->labels, c->items, c->n_items, c->dflags + kFlagWrote,
+        sl.d_order);
     CUDA_TRY(cudaGetLastError());
     return CC_OK;
 }
@@ -883,7 +902,8 @@ int launch_slice_t(cc_ctx* c, SweepLaunch sl) {
     }
     const int blocks = (int)std::min<int64_t>(c->n_items, (int64_t)c->sm_count);
     kern<<<std::max(blocks, 1), cck::kBT, smem, sl.stream>>>(
-        c->src, c->dst, c->labels, c->items, c->n_items, c->dflags + kFlagWrote, sl.d_order);
+        bucket_src(c), bucket_dst(c), c->labels, c->items, c->n_items, c->dflags + kFlagWrote,
+        sl.d_order);
     CUDA_TRY(cudaGetLastError());
     return CC_OK;
 }
@@ -926,8 +946,10 @@ int launch_first(cc_ctx* c, lab_t* T) {
 }
 
 // first: labels are the identity (sweep 1 after init) -> load-free scatter.
+// sweep_no: 1-based sweep index (layout 5 runs sweep 1 on the chunk-sorted
+// rows and later order-2 sweeps on the bucketed copy); 0 = unknown.
 int enqueue_sweep(cc_ctx* c, int order, int sync, int atomic, bool count_changes,
-                  bool first = false) {
+                  bool first = false, int64_t sweep_no = 0) {
     if (order < 1) return fail(CC_EINVAL, "operator order must be >= 1");
     CUDA_TRY(cudaMemsetAsync(c->dflags + kFlagWrote, 0, sizeof(int), c->stream));
     CUDA_TRY(cudaMemsetAsync(c->dcount, 0, sizeof(unsigned long long), c->stream));
@@ -955,7 +977,7 @@ int enqueue_sweep(cc_ctx* c, int order, int sync, int atomic, bool count_changes
     int rc;
     if (first) {
         rc = launch_first(c, L);
-    } else if (order == 2 && c->layout == 3 && c->items) {
+    } else if (order == 2 && has_buckets(c) && (c->layout == 3 || sweep_no > 1)) {
         rc = launch_bucketed(c, sm, SweepLaunch{c->stream, nullptr});
     } else {
         rc = launch_order(c, L, L, order, sm);
@@ -1031,8 +1053,15 @@ int launch_guarded(cc_ctx* c, const cc_schedule* s, int sm, cudaStream_t st) {
     }
     const SweepLaunch sl{st, &c->dstate->order};
     lab_t* L = c->labels;
-    if (need2 && c->layout == 3 && c->items) CC_TRY(launch_bucketed(c, sm, sl));
-    else if (need2) CC_TRY(launch_o2(c, L, L, sm, sl));
+    if (need2 && c->layout == 5 && c->items) {
+        // sweep 1 on the chunk-sorted rows, later sweeps on the bucketed copy
+        CC_TRY(launch_o2(c, L, L, sm, SweepLaunch{st, &c->dstate->order_first}));
+        CC_TRY(launch_bucketed(c, sm, SweepLaunch{st, &c->dstate->order_rest}));
+    } else if (need2 && c->layout == 3 && c->items) {
+        CC_TRY(launch_bucketed(c, sm, sl));
+    } else if (need2) {
+        CC_TRY(launch_o2(c, L, L, sm, sl));
+    }
     if (need1) CC_TRY((launch_store_mode<1, 2>(c, L, L, 1, sm, sl)));
     if (needh) CC_TRY((launch_store_mode<0, 1>(c, L, L, s->high_order, sm, sl)));
     return CC_OK;
@@ -1050,7 +1079,8 @@ int build_loop(cc_ctx* c, const cc_schedule* s, int64_t cap, int sm, int check, 
     if (c->loop_exec && k.src == c->src && k.dst == c->dst && k.labels == c->labels &&
         k.m == c->m && k.n == c->n && k.cap == cap && same_schedule(k.s, *s) && k.sm == sm &&
         k.shortcut == c->shortcut && k.layout == c->layout && k.check == check &&
-        k.items == c->items && k.n_items == c->n_items && k.resume == resume)
+        k.items == c->items && k.n_items == c->n_items && k.resume == resume &&
+        k.bsrc == c->bsrc)
         return CC_OK;
     if (c->loop_exec) cudaGraphExecDestroy(c->loop_exec);
     if (c->loop_graph) cudaGraphDestroy(c->loop_graph);
@@ -1091,7 +1121,7 @@ int build_loop(cc_ctx* c, const cc_schedule* s, int64_t cap, int sm, int check, 
     if (check) {
         k_gcheck_idem<<<grid_for(c, c->n), kThreads, 0, c->body_stream>>>(c->labels, c->n,
                                                                           c->dflags);
-        if (c->m > 0 && c->layout == 3 && c->items && !c->bucket_nosmem)
+        if (c->m > 0 && has_buckets(c) && !c->bucket_nosmem)
             CC_TRY(launch_check_slice(c, c->body_stream));
         else if (c->m > 0)
             k_gcheck_edges<<<grid_for(c, (c->m + 3) / 4), kThreads, 0, c->body_stream>>>(
@@ -1107,7 +1137,7 @@ int build_loop(cc_ctx* c, const cc_schedule* s, int64_t cap, int sm, int check, 
     CUDA_TRY(cudaStreamEndCapture(cs, &c->loop_graph));
     CUDA_TRY(cudaGraphInstantiate(&c->loop_exec, c->loop_graph, 0));
     k = {c->src, c->dst,   c->labels, c->m,     c->n,       cap,   *s,
-         sm,     c->shortcut, c->layout, check, c->items, c->n_items, resume};
+         sm,     c->shortcut, c->layout, check, c->items, c->n_items, resume, c->bsrc};
     return CC_OK;
 }
 
@@ -1379,6 +1409,8 @@ void cc_destroy(cc_ctx* c) {
     DeviceGuard g(c->device);
     cudaStreamSynchronize(c->stream);
     if (c->own_edges) { cudaFree(c->src); cudaFree(c->dst); }
+    cudaFree(c->bsrc);
+    cudaFree(c->bdst);
     if (c->own_labels) cudaFree(c->labels);
     cudaFree(c->wide);
     cudaFree(c->shadow);
@@ -1596,7 +1628,8 @@ int run_impl(cc_ctx* c, const cc_schedule* s, int flags, int64_t cap, void* labe
                         (long long)cap, (long long)c->n, (long long)c->m);
         const int order = order_for(s, sweep);
         if (times) CUDA_TRY(cudaEventRecord(c->ev0, c->stream));
-        CC_TRY(enqueue_sweep(c, order, sync, s->atomic, count, sweep == 1 && first_scatter));
+        CC_TRY(enqueue_sweep(c, order, sync, s->atomic, count, sweep == 1 && first_scatter,
+                             sweep));
         if (!sync && !count)
             for (int j = 0; j < c->shortcut; ++j)
                 k_compress<<<grid_for(c, (c->n + 3) / 4), kThreads, 0, c->stream>>>(c->labels, c->n,
@@ -1914,8 +1947,10 @@ int cc_set_option(cc_ctx* c, int option, int64_t value) {
 namespace {
 
 template <typename K>
+// Output rows go to (osrc, odst): the row arrays themselves (layout 3) or
+// the bucketed copy (layout 5); the input rows are read from c->src/c->dst.
 int reorder_bucketed_t(cc_ctx* c, int sbits, int total_bits, int64_t nb, int runs,
-                       int run_major) {
+                       int run_major, lab_t* osrc, lab_t* odst, int layout) {
     const int64_t m = c->m;
     K *kin = nullptr, *kout = nullptr;
     lab_t* vout = nullptr;
@@ -1933,9 +1968,9 @@ int reorder_bucketed_t(cc_ctx* c, int sbits, int total_bits, int64_t nb, int run
     CUDA_TRY(cub::DeviceRadixSort::SortPairs(tmp, tb, kin, kout, c->dst, vout, (int)m, 0,
                                              total_bits, c->stream));
     k_unkey<K><<<grid_for(c, m, 16), kThreads, 0, c->stream>>>(kout, m,
-                                                                (K)(((K)1 << sbits) - 1), c->src);
+                                                                (K)(((K)1 << sbits) - 1), osrc);
     CUDA_TRY(cudaGetLastError());
-    CUDA_TRY(cudaMemcpyAsync(c->dst, vout, sizeof(lab_t) * m, cudaMemcpyDeviceToDevice,
+    CUDA_TRY(cudaMemcpyAsync(odst, vout, sizeof(lab_t) * m, cudaMemcpyDeviceToDevice,
                              c->stream));
     // group g = bucket (bucket-major) or run * nb + bucket (run-major)
     const int64_t ng = nb * runs;
@@ -2003,15 +2038,31 @@ int reorder_bucketed_t(cc_ctx* c, int sbits, int total_bits, int64_t nb, int run
         CUDA_TRY(cudaMemcpy(c->items, items.data(), sizeof(cck::BucketItem) * items.size(),
                             cudaMemcpyHostToDevice));
     }
-    c->layout = 3;
+    c->layout = layout;
     return CC_OK;
 }
 
 // Layout 3: rows grouped by dst bucket, src-sorted inside (one global sort).
 // item_order 1: rows first cut, in their current order, into runs of
 // sort_chunk rows; groups are (run, bucket).
-int reorder_bucketed(cc_ctx* c) {
+// layout 5 (hybrid): the rows keep their order (sweep 1 runs on them) and a
+// dst-bucketed copy is built next to them for the later sweeps / checks.
+int reorder_bucketed(cc_ctx* c, int layout = 3) {
     if (c->m >= ((int64_t)1 << 31)) return fail(CC_EINVAL, "bucketed layout needs m < 2^31");
+    lab_t *osrc = c->src, *odst = c->dst;
+    if (layout == 5) {
+        if (c->bcap < c->m) {
+            cudaFree(c->bsrc);
+            cudaFree(c->bdst);
+            c->bsrc = c->bdst = nullptr;
+            c->bcap = 0;
+            CUDA_TRY(cudaMalloc(&c->bsrc, sizeof(lab_t) * c->m));
+            CUDA_TRY(cudaMalloc(&c->bdst, sizeof(lab_t) * c->m));
+            c->bcap = c->m;
+        }
+        osrc = c->bsrc;
+        odst = c->bdst;
+    }
     const int sbits = std::max<int>(1, (int)ccgen::perm_bits((uint64_t)c->n));
     const int64_t B = (int64_t)1 << c->bucket_shift;
     const int64_t nb = (c->n + B - 1) / B;
@@ -2020,8 +2071,10 @@ int reorder_bucketed(cc_ctx* c) {
         run_major ? (int)std::max<int64_t>(1, (c->m + c->sort_chunk - 1) / c->sort_chunk) : 1;
     const int bbits = std::max<int>(1, (int)ccgen::perm_bits((uint64_t)(nb * runs)));
     if (sbits + bbits <= 32)
-        return reorder_bucketed_t<uint32_t>(c, sbits, sbits + bbits, nb, runs, run_major);
-    return reorder_bucketed_t<unsigned long long>(c, sbits, sbits + bbits, nb, runs, run_major);
+        return reorder_bucketed_t<uint32_t>(c, sbits, sbits + bbits, nb, runs, run_major, osrc,
+                                            odst, layout);
+    return reorder_bucketed_t<unsigned long long>(c, sbits, sbits + bbits, nb, runs, run_major,
+                                                  osrc, odst, layout);
 }
 
 // Layout 4: rows partitioned by dst into L2-window buckets of 2^tile_shift
@@ -2103,11 +2156,11 @@ extern "C" {
 int cc_reorder_edges(cc_ctx* c, int mode) {
     if (!c) return fail(CC_EINVAL, "null context");
     if (mode == 0) return CC_OK;
-    if (mode < 1 || mode > 4) return fail(CC_EINVAL, "unknown edge layout mode %d", mode);
+    if (mode < 1 || mode > 5) return fail(CC_EINVAL, "unknown edge layout mode %d", mode);
     std::lock_guard<std::mutex> lk(c->mu);
     DeviceGuard g(c->device);
     if (c->m < 2) return CC_OK;
-    if (mode == 3) return reorder_bucketed(c);
+    if (mode == 3 || mode == 5) return reorder_bucketed(c, mode);
     if (mode == 4) return reorder_l2tiles(c);
     c->layout = mode;
     // mode 1: one global sort by src; mode 2: independent sorts of

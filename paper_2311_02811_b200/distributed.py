@@ -138,7 +138,7 @@ class FusedShardedContour(_HostIO):
         total = 2 * edgefactor * n
         lo, hi = shard_rows(total, rank, world)
         graphgen.rmat_device(ctx, scale, edgefactor, seed, row_lo=lo, row_hi=hi)
-        layout = resolve_layout(layout, hi - lo, n)
+        layout = resolve_layout(layout, hi - lo, n, resident=False)  # no bucketed copy
         if LAYOUTS[layout]:
             _lib.check(ctx.lib.cc_reorder_edges(ctx.handle, LAYOUTS[layout]))
         runner = cls(PeerShard(ctx, n, atomic, group), n, total)
@@ -221,7 +221,7 @@ class ShardedContour(_HostIO):
         total = 2 * edgefactor * n
         lo, hi = shard_rows(total, rank, world)
         graphgen.rmat_device(ctx, scale, edgefactor, seed, row_lo=lo, row_hi=hi)
-        layout = resolve_layout(layout, hi - lo, n)
+        layout = resolve_layout(layout, hi - lo, n, resident=False)  # no bucketed copy
         if LAYOUTS[layout]:
             _lib.check(ctx.lib.cc_reorder_edges(ctx.handle, LAYOUTS[layout]))
         runner = cls(CudaShard(ctx, n, atomic), n, total, **kw)

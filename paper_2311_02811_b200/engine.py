@@ -134,21 +134,35 @@ def _unpack_graph(g):
     return int(n), edges
 
 
-LAYOUTS = {"input": 0, "src_sorted": 1, "chunk_sorted": 2, "dst_bucketed": 3, "l2_tiled": 4}
+LAYOUTS = {"input": 0, "src_sorted": 1, "chunk_sorted": 2, "dst_bucketed": 3, "l2_tiled": 4,
+           "hybrid": 5}
 AUTO_SORT_MIN_ROWS = 1 << 20
 
 
 AUTO_L2_LABEL_BYTES = 96 << 20  # the 126 MB L2 holds the labels plus the edge stream's lines
 
 
-def resolve_layout(layout: str, m: int, n: int = 0) -> str:
-    """"auto": input order below 2^20 rows; chunk-sorted staging while the
-    label array fits comfortably in L2 (it hides under the host->device copy,
-    ~2x faster sweeps); L2-window tiles (layout 4) for larger label arrays."""
+AUTO_HYBRID_MIN_DEGREE = 8  # rows per vertex from which the bucketed copy pays (measured)
+
+
+def resolve_layout(layout: str, m: int, n: int = 0, resident: bool = True) -> str:
+    """"auto": input order below 2^20 rows; while the label array fits
+    comfortably in L2, chunk-sorted staging (it hides under the host->device
+    copy, ~2x faster sweeps) -- plus, for graphs staged once and run from HBM
+    (``resident``) with >= 8 rows per vertex and m < 2^31, the dst-bucketed
+    copy of the hybrid layout (later sweeps and the early check gather dst
+    labels from shared memory: RMAT-20..23 12-17 % faster per run; grid and
+    ER are slower with it); L2-window tiles (layout 4) for larger label
+    arrays.  One-shot runs from host memory (run_host) keep chunk_sorted so
+    sweep 1 streams behind the copy."""
     if layout == "auto":
         if m < AUTO_SORT_MIN_ROWS:
             return "input"
-        return "chunk_sorted" if 4 * n <= AUTO_L2_LABEL_BYTES else "l2_tiled"
+        if 4 * n > AUTO_L2_LABEL_BYTES:
+            return "l2_tiled"
+        if resident and m < (1 << 31) and m >= AUTO_HYBRID_MIN_DEGREE * n:
+            return "hybrid"
+        return "chunk_sorted"
     if layout not in LAYOUTS:
         raise ValueError(f"unknown edge layout '{layout}'")
     return layout
@@ -165,6 +179,15 @@ def _host_edges(edges) -> np.ndarray:
     return np.ascontiguousarray(e)
 
 
+def apply_layout(ctx: _lib.Context, layout: str) -> None:
+    """Reorder rows already staged in HBM (e.g. generated on device) into
+    ``layout``; "hybrid" = chunk-sorted rows plus a dst-bucketed copy."""
+    if layout == "hybrid":
+        _lib.check(ctx.lib.cc_reorder_edges(ctx.handle, LAYOUTS["chunk_sorted"]))
+    if LAYOUTS[layout]:
+        _lib.check(ctx.lib.cc_reorder_edges(ctx.handle, LAYOUTS[layout]))
+
+
 def stage_graph(ctx: _lib.Context, n: int, edges, layout: str = "auto") -> None:
     """Stage an (m, 2) edge array (numpy int32/int64 on the host, or a CUDA
     tensor) as packed uint32 SoA in HBM, with the graph.py:73-79 range check.
@@ -177,7 +200,7 @@ def stage_graph(ctx: _lib.Context, n: int, edges, layout: str = "auto") -> None:
     m_rows = int(edges.shape[0]) if hasattr(edges, "shape") and len(edges.shape) == 2 \
         else len(edges)
     layout = resolve_layout(layout, m_rows, n)
-    ctx.set_option(_lib.CC_OPT_STAGE_LAYOUT, 2 if layout == "chunk_sorted" else 0)
+    ctx.set_option(_lib.CC_OPT_STAGE_LAYOUT, 2 if layout in ("chunk_sorted", "hybrid") else 0)
     lib = ctx.lib
     if hasattr(edges, "data_ptr") and getattr(edges, "is_cuda", False):
         e = edges.reshape(-1, 2).contiguous()
@@ -193,7 +216,7 @@ def stage_graph(ctx: _lib.Context, n: int, edges, layout: str = "auto") -> None:
         _lib.check(lib.cc_stage_edges(ctx.handle, ctypes.c_void_p(e.ctypes.data),
                                       e.dtype.itemsize, m, n))
     ctx.n, ctx.m = n, m
-    if layout in ("src_sorted", "dst_bucketed", "l2_tiled"):
+    if layout in ("src_sorted", "dst_bucketed", "l2_tiled", "hybrid"):
         _lib.check(lib.cc_reorder_edges(ctx.handle, LAYOUTS[layout]))
 
 
@@ -258,7 +281,7 @@ def run_host(ctx: _lib.Context, n: int, edges, schedule: Schedule, *, layout: st
     (labels_out, IterationStats)."""
     e = _host_edges(edges)
     m = e.shape[0]
-    layout = resolve_layout(layout, m, n)
+    layout = resolve_layout(layout, m, n, resident=False)
     if layout not in ("input", "chunk_sorted"):
         stage_graph(ctx, n, e, layout)
         return run_staged(ctx, schedule, count_changes=count_changes, early_check=early_check,

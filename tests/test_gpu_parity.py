@@ -367,7 +367,7 @@ def test_graph_loop_early_check(golden):
                  graphgen.forest(40, 5), spec.erdos_renyi(4097, 9000, 3)):
         cases.append((n, e, oracle.rem_union_find(n, e).tolist()))
     seen = set()
-    for layout in ("input", "chunk_sorted", "dst_bucketed"):
+    for layout in ("input", "chunk_sorted", "dst_bucketed", "hybrid"):
         for n, e, exp in cases:
             for variant in ("C-1", "C-2", "C-m", "C-1m1m"):
                 sched = make_schedule(variant, 6, sync=False)
@@ -383,6 +383,33 @@ def test_graph_loop_early_check(golden):
                     assert sg.sweeps_until_stable == sg.sweeps_executed - 1
                     assert sg.changed_per_sweep[-1] == 0
     assert "early-check" in seen
+
+
+@pytest.mark.parametrize("pipe", [0, 1, 2])
+def test_hybrid_layout_exact(pipe):
+    """Layout 5: sweep 1 on chunk-sorted rows, later order-2 sweeps and the
+    check on the dst-bucketed copy -- graph and host loops, every variant."""
+    ctx = _lib.Context(0)
+    ctx.set_option(_lib.CC_OPT_BUCKET_PIPE, pipe)
+    ctx.set_option(_lib.CC_OPT_BUCKET_SHIFT, 11)
+    ctx.set_option(_lib.CC_OPT_ITEM_ROWS, 3001)
+    ctx.set_option(_lib.CC_OPT_SORT_CHUNK, 50000)
+    for n, e in (graphgen.rmat(15, 16, 2), graphgen.grid(210, 190, 0.55, 5),
+                 graphgen.forest(50, 4), spec.erdos_renyi(6001, 15000, 9)):
+        exp = oracle.rem_union_find(n, e)
+        engine.stage_graph(ctx, n, e, "hybrid")
+        for variant in ("C-2", "C-1", "C-m", "C-1m1m"):
+            for host_loop, early in ((False, False), (False, True), (True, True)):
+                labels = np.empty(n, dtype=np.int64)
+                _, st = engine.run_staged(ctx, make_schedule(variant, 5), count_changes=False,
+                                          early_check=early, host_loop=host_loop,
+                                          labels_out=labels)
+                assert np.array_equal(labels, exp), (n, variant, host_loop, early)
+                check_invariants(labels, st)
+        labels = np.empty(n, dtype=np.int64)
+        engine.run_staged(ctx, make_schedule("c2", sync=True), labels_out=labels)
+        assert np.array_equal(labels, exp)
+    ctx.close()
 
 
 def test_run_host_streamed_first_sweep(golden):

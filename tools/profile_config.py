@@ -21,7 +21,7 @@ def main():
     if spec["kind"] == "rmat":
         n, m = graphgen.rmat_device(ctx, spec["scale"], spec["edgefactor"], 1)
         lay = engine.resolve_layout(layout, m, n)
-        _lib.check(ctx.lib.cc_reorder_edges(ctx.handle, engine.LAYOUTS[lay]))
+        engine.apply_layout(ctx, lay)
     else:
         n, e = graphgen.make(spec, 1, elem_bytes=8)
         lay = engine.resolve_layout(layout, e.shape[0], n)

@@ -51,7 +51,7 @@ def run(cfg, args):
             rec["runs"] = args.runs
         lay = engine.resolve_layout(args.layout, m, n)
         t1 = time.perf_counter()
-        _lib.check(ctx.lib.cc_reorder_edges(ctx.handle, engine.LAYOUTS[lay]))
+        engine.apply_layout(ctx, lay)
     else:
         n, host = graphgen.make(spec, 1, elem_bytes=8)
         m = host.shape[0]
