@@ -845,16 +845,18 @@ int launch_bucketed_u(cc_ctx* c, int sm, SweepLaunch sl) {
     }
 }
 
+constexpr int kCheckNV = 4;  // 16 rows per thread per iteration of the slice check (8 spills)
+
 int launch_check_slice(cc_ctx* c, cudaStream_t st) {
     const size_t smem = sizeof(lab_t) * ((size_t)1 << c->bucket_shift);
     static size_t smem_set = 0;
     if (smem_set != smem) {
-        CUDA_TRY(cudaFuncSetAttribute(cck::k_check_slice,
+        CUDA_TRY(cudaFuncSetAttribute(cck::k_check_slice<kCheckNV>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         smem_set = smem;
     }
     const int blocks = (int)std::min<int64_t>(c->n_items, (int64_t)c->sm_count);
-    cck::k_check_slice<<<std::max(blocks, 1), cck::kBT, smem, st>>>(
+    cck::k_check_slice<kCheckNV><<<std::max(blocks, 1), cck::kBT, smem, st>>>(
         bucket_src(c), bucket_dst(c), c->labels, c->items, c->n_items, c->dflags, kFlagWrote,
         kFlagCheck);
     CUDA_TRY(cudaGetLastError());

@@ -750,6 +750,8 @@ __global__ void __launch_bounds__(kBT, 1)
 // Same guards as the flat check: return at once when the sweep wrote
 // nothing or the check already failed; poll the failure word every 16 row
 // batches (one load per warp).
+// NV uint4 row vectors per thread per iteration (4*NV independent gathers).
+template <int NV>
 __global__ void __launch_bounds__(kBT, 1)
     k_check_slice(const lab_t* __restrict__ src, const lab_t* __restrict__ dst,
                   const lab_t* __restrict__ L, const BucketItem* __restrict__ items, int n_items,
@@ -787,11 +789,20 @@ __global__ void __launch_bounds__(kBT, 1)
         const uint4* d4 = reinterpret_cast<const uint4*>(dst + a0);
         const int64_t nvec = (a1 - a0) >> 2;
         int k = 0;
-        for (int64_t q = tid; q < nvec && !bad; q += kBT) {
-            if ((++k & 15) == 0 && vf[check_idx]) break;
-            const uint4 a = __ldcs(s4 + q), b = __ldcs(d4 + q);
-            bad = (L[a.x] != sl[b.x - base]) | (L[a.y] != sl[b.y - base]) |
-                  (L[a.z] != sl[b.z - base]) | (L[a.w] != sl[b.w - base]);
+        for (int64_t q = tid; q < nvec && !bad; q += (int64_t)kBT * NV) {
+            if ((++k & 7) == 0 && vf[check_idx]) break;
+            uint4 a[NV], b[NV];
+#pragma unroll
+            for (int j = 0; j < NV; ++j) {
+                const int64_t i = q + (int64_t)j * kBT;
+                if (i < nvec) { a[j] = __ldcs(s4 + i); b[j] = __ldcs(d4 + i); }
+            }
+#pragma unroll
+            for (int j = 0; j < NV; ++j) {
+                if (q + (int64_t)j * kBT < nvec)
+                    bad |= (L[a[j].x] != sl[b[j].x - base]) | (L[a[j].y] != sl[b[j].y - base]) |
+                           (L[a[j].z] != sl[b[j].z - base]) | (L[a[j].w] != sl[b[j].w - base]);
+            }
         }
         if (bad) vf[check_idx] = 1;
         // uniform exit decision (the slice is reused by the next item)
