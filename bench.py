@@ -74,9 +74,11 @@ def parse():
                    help="use the edge-sharded NCCL driver even with one rank (plumbing check)")
     p.add_argument("--cadence", type=int, default=1,
                    help="local sweeps per MIN exchange in the sharded driver")
-    p.add_argument("--exchange", default="peer", choices=["peer", "nccl"],
-                   help="multi-GPU label exchange: fused red.min into peer replicas (CUDA IPC) "
-                        "or an NCCL allreduce-min of the labels")
+    p.add_argument("--exchange", default="hybrid", choices=["hybrid", "peer", "nccl"],
+                   help="multi-GPU label exchange: hybrid (default: one all-reduce-MIN "
+                        "after the local sweep 1, then fused red.min into the peer replicas), "
+                        "peer (fused from the start, CUDA IPC) or nccl (all-reduce-MIN every "
+                        "--cadence local sweeps)")
     p.add_argument("--clock-interval-ms", type=int, default=100,
                    help="nvidia-smi sampling interval during the timed region")
     p.add_argument("--atomic", type=int, default=1,
@@ -474,11 +476,18 @@ def run_multi(args, rank, world, device):
     torch.cuda.set_stream(stream)
     exchange = args.exchange
     runner = None
-    if exchange == "peer":
+    if exchange in ("peer", "hybrid"):
         try:  # fused sweep + red.min into the peers' replicas (CUDA IPC over NVLink)
-            runner = distributed.FusedShardedContour.from_rmat(
-                spec["scale"], spec.get("edgefactor", 16), args.seed, rank, world, device,
-                layout=args.layout, atomic=bool(args.atomic))
+            cls = (distributed.HybridShardedContour if exchange == "hybrid"
+                   else distributed.FusedShardedContour)
+            runner = cls.from_rmat(spec["scale"], spec.get("edgefactor", 16), args.seed, rank,
+                                   world, device, layout=args.layout, atomic=bool(args.atomic))
+            if exchange == "hybrid" and dist.get_backend() == "gloo":
+                def gloo_min(t):  # plumbing-check runs (ranks sharing a GPU)
+                    c = t.cpu()
+                    dist.all_reduce(c, op=dist.ReduceOp.MIN)
+                    t.copy_(c)
+                runner.allreduce = gloo_min
         except RuntimeError as exc:  # no IPC peer mapping on this node: use NCCL, say so
             exchange = f"nccl (peer IPC unavailable: {str(exc)[:80]})"
     if runner is None:
@@ -547,8 +556,14 @@ def run_multi(args, rank, world, device):
                "seconds_per_step": e2e_s,
                "path": "per rank: cc_stage_edges(pinned int32 shard, chunk-sorted while "
                        "copying) + the sharded run; rank 0: labels -> pinned int64"}
-    fused = isinstance(runner, distributed.FusedShardedContour)
-    if fused:
+    fused = isinstance(runner, (distributed.FusedShardedContour,
+                                distributed.HybridShardedContour))
+    if isinstance(runner, distributed.HybridShardedContour):
+        sched = (f"C-2 async atomic={bool(args.atomic)}; round 1: local sweep + shortcut, "
+                 f"all-reduce-MIN of the n+1 labels; later rounds: fused sweep + red.min into "
+                 f"the peer replicas (CUDA IPC / NVLink), 1-word MAX all-reduce")
+        launches = sum(5 + r for r in rounds)  # init, sweep, fold, shortcut, +1/round, compress
+    elif fused:
         sched = (f"C-2 async atomic={bool(args.atomic)}, fused sweep + red.min into the peer "
                  f"replicas (CUDA IPC / NVLink), 1-word MAX all-reduce per round")
         launches = sum(2 + r for r in rounds)  # init + fused sweep per round + compress

@@ -91,6 +91,28 @@ class PeerShard:
         arr = (ctypes.c_uint64 * max(1, len(self.peer_ptrs)))(*self.peer_ptrs)
         _lib.check(ctx.lib.cc_set_peers(ctx.handle, arr, len(self.peer_ptrs)))
 
+    def enable(self, on: bool) -> None:
+        """Route this rank's order-2 sweeps into the peers' replicas (on) or
+        into the local replica only (off)."""
+        if on:
+            arr = (ctypes.c_uint64 * max(1, len(self.peer_ptrs)))(*self.peer_ptrs)
+            _lib.check(self.ctx.lib.cc_set_peers(self.ctx.handle, arr, len(self.peer_ptrs)))
+        else:
+            _lib.check(self.ctx.lib.cc_set_peers(self.ctx.handle, None, 0))
+
+    def labels_tensor(self):
+        """A torch view (no copy) of the context's own n+1 int32 labels, for
+        collective exchanges (NCCL all-reduce) on the same buffer the peers
+        write into."""
+        import torch
+        ptr = ctypes.c_void_p(0)
+        _lib.check(self.ctx.lib.cc_labels_device(self.ctx.handle, ctypes.byref(ptr)))
+
+        class _View:
+            __cuda_array_interface__ = {"shape": (self.n + 1,), "typestr": "<i4",
+                                        "data": (ptr.value, False), "version": 3}
+        return torch.as_tensor(_View(), device=f"cuda:{self.ctx.device}")
+
     def close(self):
         _lib.check(self.ctx.lib.cc_set_peers(self.ctx.handle, None, 0))
         for p in self.peer_ptrs:
@@ -173,6 +195,77 @@ class FusedShardedContour(_HostIO):
                 break
         r = ctypes.c_int(0)
         _lib.check(ctx.lib.cc_compress(ctx.handle, ctypes.byref(r)))
+        return rounds
+
+
+class HybridShardedContour(_HostIO):
+    """Dense first exchange, sparse later ones.  Sweep 1 lowers most labels:
+    there a dense all-reduce-MIN of the n+1 labels (NCCL; ~2 x 4n bytes per
+    rank) moves less than sending every lowering to every peer (~lowerings x
+    (p-1) x 4 bytes).  Later sweeps lower few labels: there the fused sweep +
+    peer red.min moves only those.  So round 1 = ``first_sweeps`` local
+    sweeps (+ shortcut) folded into slot n, then one all-reduce-MIN of the
+    replicas (converged if slot n == 1 after it, as in ShardedContour); from
+    round 2 the FusedShardedContour protocol on the now identical replicas."""
+
+    def __init__(self, shard: PeerShard, n: int, m_total: int, cap=None, allreduce=None,
+                 first_sweeps: int = 1):
+        self.shard = shard
+        self.n = n
+        self.m_total = m_total
+        self.cap = n + 2 if cap is None else cap
+        self.layout = "input"
+        self.first_sweeps = max(1, int(first_sweeps))
+        self.labels = shard.labels_tensor()
+        self.allreduce = allreduce or nccl_allreduce_min(shard.group)
+
+    @classmethod
+    def from_rmat(cls, scale: int, edgefactor: int, seed: int, rank: int, world: int,
+                  device: int, layout: str = "auto", atomic: bool = True, group=None):
+        base = FusedShardedContour.from_rmat(scale, edgefactor, seed, rank, world, device,
+                                             layout=layout, atomic=atomic, group=group)
+        runner = cls(base.shard, base.n, base.m_total)
+        runner.layout = base.layout
+        return runner
+
+    def run(self) -> int:
+        import torch
+        import torch.distributed as dist
+        shard, ctx = self.shard, self.shard.ctx
+        lib = ctx.lib
+        _lib.check(lib.cc_init_labels(ctx.handle))
+        shard.enable(False)
+        for k in range(self.first_sweeps):
+            _lib.check(lib.cc_sweep(ctx.handle, 2, 0, int(shard.atomic), 0, None))
+            _lib.check(lib.cc_fold_flag(ctx.handle, int(k == 0)))
+            _lib.check(lib.cc_shortcut(ctx.handle, 1))
+        _lib.check(lib.cc_synchronize(ctx.handle))
+        self.allreduce(self.labels)
+        rounds = 1
+        if int(self.labels[self.n].item()) != 1:
+            # every replica finished its all-reduce before any peer lowers into it
+            torch.cuda.synchronize(ctx.device)
+            dist.barrier(group=shard.group)
+            shard.enable(True)
+            try:
+                while True:
+                    rounds += 1
+                    if rounds > self.cap:
+                        from .errors import IterationCapExceeded
+                        raise IterationCapExceeded(f"no convergence after {self.cap} sweeps")
+                    wrote = ctypes.c_int(0)
+                    _lib.check(lib.cc_sweep(ctx.handle, 2, 0, int(shard.atomic), 0,
+                                            ctypes.byref(wrote)))
+                    t = torch.tensor([wrote.value], dtype=torch.int32,
+                                     device="cpu" if dist.get_backend(shard.group) == "gloo"
+                                     else f"cuda:{ctx.device}")
+                    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=shard.group)
+                    if not int(t.item()):
+                        break
+            finally:
+                shard.enable(False)
+        r = ctypes.c_int(0)
+        _lib.check(lib.cc_compress(ctx.handle, ctypes.byref(r)))
         return rounds
 
 

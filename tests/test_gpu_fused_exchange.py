@@ -20,13 +20,20 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, cfg, q):
+def _gloo_allreduce_min(t):
+    import torch.distributed as dist
+    c = t.cpu()
+    dist.all_reduce(c, op=dist.ReduceOp.MIN)
+    t.copy_(c)
+
+
+def _worker(rank, world, port, cfg, q, exchange="fused"):
     import torch
     import torch.distributed as dist
 
     from paper_2311_02811_b200 import _lib, engine
-    from paper_2311_02811_b200.distributed import (FusedShardedContour, PeerShard,
-                                                   shard_rows)
+    from paper_2311_02811_b200.distributed import (FusedShardedContour, HybridShardedContour,
+                                                   PeerShard, shard_rows)
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -36,7 +43,10 @@ def _worker(rank, world, port, cfg, q):
         ctx = _lib.Context(0)
         engine.stage_graph(ctx, n, e[lo:hi], "chunk_sorted" if e.shape[0] > 1 << 16 else "input")
         shard = PeerShard(ctx, n, atomic=True)
-        runner = FusedShardedContour(shard, n, e.shape[0])
+        if exchange == "hybrid":
+            runner = HybridShardedContour(shard, n, e.shape[0], allreduce=_gloo_allreduce_min)
+        else:
+            runner = FusedShardedContour(shard, n, e.shape[0])
         rounds = runner.run()
         labels = np.empty(n, dtype=np.int64)
         _lib.check(ctx.lib.cc_read_labels(ctx.handle, ctypes.c_void_p(labels.ctypes.data), 8))
@@ -48,8 +58,10 @@ def _worker(rank, world, port, cfg, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,graph", [(2, "rmat"), (3, "grid"), (2, "forest")])
-def test_fused_exchange_ranks_on_one_gpu(world, graph):
+@pytest.mark.parametrize("world,graph,exchange",
+                         [(2, "rmat", "fused"), (3, "grid", "fused"), (2, "forest", "fused"),
+                          (2, "rmat", "hybrid"), (3, "grid", "hybrid"), (2, "forest", "hybrid")])
+def test_fused_exchange_ranks_on_one_gpu(world, graph, exchange):
     import torch.multiprocessing as mp
 
     from oracle import gen, oracle
@@ -63,7 +75,8 @@ def test_fused_exchange_ranks_on_one_gpu(world, graph):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, cfg, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, cfg, q, exchange))
+             for r in range(world)]
     for p in procs:
         p.start()
     results = [q.get(timeout=300) for _ in range(world)]
