@@ -701,10 +701,16 @@ int launch_o2(cc_ctx* c, const lab_t* R, lab_t* T, int sm, SweepLaunch sl) {
             default: return launch_o2_peers<cck::kStoreCheckRed>(c, T, sl);
         }
     }
-    // 12 (auto): variant 11 on L2-window tiles -- there the edge stream and
-    // the src gathers would evict the tile's dst window from L2 (RMAT-28: 84 ms
-    // vs 122 ms per run with tile split 2, measured) -- else variant 1
-    const int variant = c->sweep_variant == 12 ? (c->layout == 4 ? 11 : 1) : c->sweep_variant;
+    // 12 (auto): on L2-window tiles the cache hints of variant 11 -- there the
+    // edge stream and the src gathers would evict the tile's dst window from
+    // L2 (RMAT-28: 84 ms vs 122 ms per run with tile split 2, measured); for a
+    // sparse graph (m < 4n, the forest: DRAM-latency-bound random gathers,
+    // 1.7 % issue) with 16 rows per thread (variant 13: 682 vs 773 ms; the
+    // same on RMAT-28, L2-request-bound, costs 3.7x); elsewhere variant 1
+    const int variant = c->sweep_variant != 12 ? c->sweep_variant
+                        : c->layout != 4       ? 1
+                        : c->m < 4 * c->n      ? 13
+                                               : 11;
     switch (variant) {
         case 1: return launch_store_mode<2, 1>(c, R, T, 2, sm, sl);
         case 2: return launch_store_mode<2, 2, 4>(c, R, T, 2, sm, sl);
@@ -723,6 +729,9 @@ int launch_o2(cc_ctx* c, const lab_t* R, lab_t* T, int sm, SweepLaunch sl) {
                 c, R, T, 2, sm, sl);
         case 11:
             return launch_store_mode<2, 1, 1, cck::kHintEdgeFirst | cck::kHintDstKeep>(c, R, T, 2,
+                                                                                       sm, sl);
+        case 13:
+            return launch_store_mode<2, 4, 1, cck::kHintEdgeFirst | cck::kHintDstKeep>(c, R, T, 2,
                                                                                        sm, sl);
         default: return launch_store_mode<2, 2>(c, R, T, 2, sm, sl);
     }
@@ -1908,7 +1917,7 @@ int cc_set_option(cc_ctx* c, int option, int64_t value) {
             c->shortcut = (int)value;
             return CC_OK;
         case CC_OPT_SWEEP_VARIANT:
-            if (value < 0 || value > 12) return fail(CC_EINVAL, "sweep variant must be 0..12");
+            if (value < 0 || value > 13) return fail(CC_EINVAL, "sweep variant must be 0..13");
             c->sweep_variant = (int)value;
             c->loop_key.m = -1;
             return CC_OK;
