@@ -38,8 +38,10 @@ def run(cfg, args):
     ctx.set_option(_lib.CC_OPT_BUCKET_SHIFT, args.bshift)
     ctx.set_option(_lib.CC_OPT_TILE_SPLIT, args.tsplit)
     ctx.set_option(_lib.CC_OPT_SHORTCUT, args.shortcut)
+    if args.store_mode >= 0:
+        ctx.set_option(_lib.CC_OPT_STORE_MODE_ATOMIC, args.store_mode)
     ctx.set_option(_lib.CC_OPT_TILE_SHIFT, args.tshift)
-    rec = {"first_scatter": args.first_scatter, "host_loop": args.host_loop,
+    rec = {"store_mode": args.store_mode, "first_scatter": args.first_scatter, "host_loop": args.host_loop,
            "shortcut": args.shortcut, "tsplit": args.tsplit, "tshift": args.tshift, "seed": args.seed, "early_check": args.early_check, "sort_chunk": args.sort_chunk, "bshift": args.bshift, "config": cfg, "variant": args.variant, "pipe": args.pipe,
            "item_order": args.item_order, "item_rows": args.item_rows}
     t0 = time.perf_counter()
@@ -113,7 +115,7 @@ def main():
     ap.add_argument("--repeats", type=int, default=3)
     ap.add_argument("--layout", default="auto")
     ap.add_argument("--variant", type=int, default=12)
-    ap.add_argument("--pipe", type=int, default=3)
+    ap.add_argument("--pipe", type=int, default=2)
     ap.add_argument("--item-order", type=int, default=0)
     ap.add_argument("--item-rows", type=int, default=1 << 18)
     ap.add_argument("--sort-chunk", type=int, default=1 << 23)
@@ -123,6 +125,7 @@ def main():
     ap.add_argument("--tsplit", type=int, default=2)
     ap.add_argument("--shortcut", type=int, default=1)
     ap.add_argument("--first-scatter", type=int, default=0)
+    ap.add_argument("--store-mode", type=int, default=-1)
     ap.add_argument("--host-loop", type=int, default=0)
     ap.add_argument("--tshift", type=int, default=24)
     ap.add_argument("--runs", type=int, default=0, help="bucketed run-major: runs (sets sort chunk)")
