@@ -11,7 +11,13 @@
 //   edge stream  : 8 B/edge, read once with 128-bit streaming loads (ld.global.cs)
 //   label gathers: L[u], L[v], then L[L[u]], L[L[v]] (4 x 4 B random, L2-resident
 //                  when 4n bytes fit the 126 MB L2) -- predicated off at fixed points
-//   label stores : <= 4 plain conditional 4 B stores, only where a cell is lowered
+//   label stores : <= 4 conditional 4 B lowerings, only where a cell is lowered
+//                  (red.global.min after an L2 re-check of hot cells by default,
+//                  plain stores for atomic=False schedules; see the store modes)
+// Kernels here: k_sweep (flat rows, any order), k_sweep_o2_peers (fused
+// multi-GPU exchange), k_sweep_slice / k_sweep_bucketed[_tma] (dst labels in
+// shared memory, dst-bucketed rows), k_check_slice (early check on those
+// rows), k_sweep_first (load-free identity sweep).
 // The "something was lowered" bit is a per-thread bool folded by
 // __syncthreads_or and published with ONE plain store per block (no atomics).
 #pragma once
