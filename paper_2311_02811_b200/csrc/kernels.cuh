@@ -641,16 +641,30 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
     } while (!ok);
 }
 
+__device__ __forceinline__ lab_t lds_u32(uint32_t addr) {
+    lab_t r;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(r) : "r"(addr));
+    return r;
+}
+
+// Shared-memory address of slice entry v is sadj + 4 v, sadj = smem(sl) -
+// 4 base (mod 2^32): one IMAD per gather, and the compiler no longer
+// re-derives the shared window base (S2R SR_CgaCtaId + LEA) per batch.
+__device__ __forceinline__ uint32_t slice_adj(const lab_t* sl, lab_t base) {
+    return smem_addr(sl) - 4u * base;
+}
+
 // Rows (u[k], v[k]) with v[k] in the slice [base, base+len); u == v rows are
 // inert (self loops and the masked rows of a partial stage).
 template <int SM, int NE>
 __device__ __forceinline__ bool slice_rows(lab_t* L, lab_t* sl, lab_t base, lab_t len,
                                            const lab_t (&u)[NE], const lab_t (&v)[NE]) {
+    const uint32_t sadj = slice_adj(sl, base);
     lab_t lu[NE], lv[NE], zu[NE], zv[NE];
 #pragma unroll
     for (int k = 0; k < NE; ++k) {
         const bool live = u[k] != v[k];
-        lv[k] = live ? sl[v[k] - base] : v[k];
+        lv[k] = live ? lds_u32(sadj + 4u * v[k]) : v[k];
         lu[k] = live ? L[u[k]] : u[k];
     }
 #pragma unroll
@@ -729,20 +743,37 @@ __global__ void __launch_bounds__(kBT, 1)
         const uint4* s4 = reinterpret_cast<const uint4*>(src + a0);
         const uint4* d4 = reinterpret_cast<const uint4*>(dst + a0);
         const int64_t nvec = (a1 - a0) >> 2;
-        int64_t q = tid;
-        uint4 a = make_uint4(0, 0, 0, 0), b = a;
-        if (PF && q < nvec) { a = __ldcs(s4 + q); b = __ldcs(d4 + q); }
-        for (; q < nvec; q += kBT) {
-            uint4 na = make_uint4(0, 0, 0, 0), nb = na;
-            if (PF) {
-                if (q + kBT < nvec) { na = __ldcs(s4 + q + kBT); nb = __ldcs(d4 + q + kBT); }
-            } else {
-                a = __ldcs(s4 + q);
-                b = __ldcs(d4 + q);
+        const uint4 zero = make_uint4(0, 0, 0, 0);  // u == v: inert
+        if (PF) {
+            // ping-pong: batch q's vectors in (a0, b0) while q + kBT's load into
+            // (a1, b1) and the other way round -- no register moves per batch
+            uint4 a0v = zero, b0v = zero, a1v, b1v;
+            int64_t q = tid;
+            if (q < nvec) { a0v = __ldcs(s4 + q); b0v = __ldcs(d4 + q); }
+            for (; q < nvec; q += 2 * kBT) {
+                a1v = zero;
+                b1v = zero;
+                if (q + kBT < nvec) { a1v = __ldcs(s4 + q + kBT); b1v = __ldcs(d4 + q + kBT); }
+                {
+                    lab_t u[4] = {a0v.x, a0v.y, a0v.z, a0v.w}, v[4] = {b0v.x, b0v.y, b0v.z, b0v.w};
+                    wrote |= slice_rows<SM, 4>(L, sl, base, len, u, v);
+                }
+                if (q + kBT >= nvec) break;
+                a0v = zero;
+                b0v = zero;
+                if (q + 2 * kBT < nvec) {
+                    a0v = __ldcs(s4 + q + 2 * kBT);
+                    b0v = __ldcs(d4 + q + 2 * kBT);
+                }
+                lab_t u[4] = {a1v.x, a1v.y, a1v.z, a1v.w}, v[4] = {b1v.x, b1v.y, b1v.z, b1v.w};
+                wrote |= slice_rows<SM, 4>(L, sl, base, len, u, v);
             }
-            lab_t u[4] = {a.x, a.y, a.z, a.w}, v[4] = {b.x, b.y, b.z, b.w};
-            wrote |= slice_rows<SM, 4>(L, sl, base, len, u, v);
-            if (PF) { a = na; b = nb; }
+        } else {
+            for (int64_t q = tid; q < nvec; q += kBT) {
+                const uint4 a = __ldcs(s4 + q), b = __ldcs(d4 + q);
+                lab_t u[4] = {a.x, a.y, a.z, a.w}, v[4] = {b.x, b.y, b.z, b.w};
+                wrote |= slice_rows<SM, 4>(L, sl, base, len, u, v);
+            }
         }
         __syncthreads();  // the next item overwrites the slice
     }
@@ -791,6 +822,7 @@ __global__ void __launch_bounds__(kBT, 1)
         const int64_t a1 = max(a0, w.end & ~(int64_t)3);
         if (tid < a0 - w.start) bad |= L[src[w.start + tid]] != sl[dst[w.start + tid] - base];
         if (tid < w.end - a1) bad |= L[src[a1 + tid]] != sl[dst[a1 + tid] - base];
+        const uint32_t sadj = slice_adj(sl, base);
         const uint4* s4 = reinterpret_cast<const uint4*>(src + a0);
         const uint4* d4 = reinterpret_cast<const uint4*>(dst + a0);
         const int64_t nvec = (a1 - a0) >> 2;
@@ -806,8 +838,10 @@ __global__ void __launch_bounds__(kBT, 1)
 #pragma unroll
             for (int j = 0; j < NV; ++j) {
                 if (q + (int64_t)j * kBT < nvec)
-                    bad |= (L[a[j].x] != sl[b[j].x - base]) | (L[a[j].y] != sl[b[j].y - base]) |
-                           (L[a[j].z] != sl[b[j].z - base]) | (L[a[j].w] != sl[b[j].w - base]);
+                    bad |= (L[a[j].x] != lds_u32(sadj + 4u * b[j].x)) |
+                           (L[a[j].y] != lds_u32(sadj + 4u * b[j].y)) |
+                           (L[a[j].z] != lds_u32(sadj + 4u * b[j].z)) |
+                           (L[a[j].w] != lds_u32(sadj + 4u * b[j].w));
             }
         }
         if (bad) vf[check_idx] = 1;
