@@ -739,6 +739,10 @@ int launch_o2(cc_ctx* c, const lab_t* R, lab_t* T, int sm, SweepLaunch sl) {
         case 15:
             return launch_store_mode<2, 2, 3, cck::kHintEdgeFirst | cck::kHintDstKeep>(c, R, T, 2,
                                                                                        sm, sl);
+        case 16: return launch_store_mode<2, 1, 1, cck::kHintDstCg>(c, R, T, 2, sm, sl);
+        case 17:
+            return launch_store_mode<2, 1, 1, cck::kHintDstCg | cck::kHintEdgeFirst>(c, R, T, 2,
+                                                                                     sm, sl);
         default: return launch_store_mode<2, 2>(c, R, T, 2, sm, sl);
     }
 }
@@ -1923,7 +1927,7 @@ int cc_set_option(cc_ctx* c, int option, int64_t value) {
             c->shortcut = (int)value;
             return CC_OK;
         case CC_OPT_SWEEP_VARIANT:
-            if (value < 0 || value > 15) return fail(CC_EINVAL, "sweep variant must be 0..15");
+            if (value < 0 || value > 17) return fail(CC_EINVAL, "sweep variant must be 0..17");
             c->sweep_variant = (int)value;
             c->loop_key.m = -1;
             return CC_OK;

@@ -96,8 +96,9 @@ __device__ __forceinline__ bool batch_o1(const lab_t* R, lab_t* T, const lab_t (
 // loaded evict-last) out of L2.
 // kHintEdgeFirst: the edge stream is loaded L1::no_allocate with an L2
 // evict-first policy; kHintSrcKeep: src-side gathers evict-last.
+// kHintDstCg: dst gathers bypass L1 (ld.global.cg; they almost never hit it).
 constexpr int kStoreMask = 7, kHintSrcStream = 8, kHintDstKeep = 16, kHintEdgeFirst = 32,
-              kHintSrcKeep = 64;
+              kHintSrcKeep = 64, kHintDstCg = 128;
 
 __device__ __forceinline__ lab_t ld_evict_last(const lab_t* p) {
     uint64_t pol;
@@ -129,6 +130,7 @@ __device__ __forceinline__ bool batch_o2(const lab_t* R, lab_t* T, const lab_t (
         else if (SMH & kHintSrcKeep) lu[k] = live ? ld_evict_last(R + u[k]) : u[k];
         else lu[k] = live ? R[u[k]] : u[k];
         if (SMH & kHintDstKeep) lv[k] = live ? ld_evict_last(R + v[k]) : v[k];
+        else if (SMH & kHintDstCg) lv[k] = live ? __ldcg(R + v[k]) : v[k];
         else lv[k] = live ? R[v[k]] : v[k];
     }
 #pragma unroll
