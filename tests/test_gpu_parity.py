@@ -412,6 +412,47 @@ def test_hybrid_layout_exact(pipe):
     ctx.close()
 
 
+def test_random_graphs_every_layout_and_loop():
+    """Seeded fuzz: random multigraphs (self loops, duplicates, isolated
+    vertices, ragged sizes) through every layout, both loops, check on/off,
+    small buckets / items / chunks so every kernel path sees many items."""
+    rng = np.random.default_rng(20261020)
+    ctx = _lib.Context(0)
+    layouts = ("input", "src_sorted", "chunk_sorted", "dst_bucketed", "l2_tiled", "hybrid")
+    for t in range(120):
+        n = int(rng.integers(1, 6000))
+        m = int(rng.integers(0, 25000))
+        e = rng.integers(0, n, size=(m, 2), dtype=np.int64)
+        if m and t % 3 == 0:  # chains: long paths stress the propagation order
+            perm = rng.permutation(n)
+            k = min(m, n - 1)
+            e[:k, 0], e[:k, 1] = perm[:k], perm[1:k + 1]
+        exp = oracle.rem_union_find(n, e)
+        layout = layouts[t % len(layouts)]
+        ctx.set_option(_lib.CC_OPT_BUCKET_SHIFT, int(rng.integers(8, 12)))
+        ctx.set_option(_lib.CC_OPT_ITEM_ROWS, int(rng.integers(1024, 5000)))
+        ctx.set_option(_lib.CC_OPT_SORT_CHUNK, int(rng.integers(1, 9000)))
+        ctx.set_option(_lib.CC_OPT_TILE_SHIFT, 10)
+        ctx.set_option(_lib.CC_OPT_ITEM_ORDER, int(t % 3))
+        ctx.set_option(_lib.CC_OPT_BUCKET_PIPE, int(rng.integers(0, 4)))
+        engine.stage_graph(ctx, n, e, layout)
+        for variant in ("C-2", "C-1", "C-m"):
+            for host_loop in (False, True):
+                early = bool(rng.integers(0, 2))
+                atomic = bool(rng.integers(0, 2))
+                labels = np.empty(n, dtype=np.int64)
+                _, st = engine.run_staged(ctx, make_schedule(variant, 4, atomic=atomic),
+                                          count_changes=False, early_check=early,
+                                          host_loop=host_loop, labels_out=labels)
+                assert np.array_equal(labels, exp), (t, n, m, layout, variant, host_loop, early)
+                check_invariants(labels, st)
+        labels = np.empty(n, dtype=np.int64)
+        _, st = engine.run_host(ctx, n, e, make_schedule("c2"), count_changes=False,
+                                labels_out=labels)
+        assert np.array_equal(labels, exp), (t, "run_host")
+    ctx.close()
+
+
 def test_run_host_streamed_first_sweep(golden):
     """cc_run_host: sweep 1 streamed behind the host-to-device copy, then the
     loop from sweep 2 -- exact labels, consistent stats, errors as staging."""
