@@ -182,8 +182,8 @@ __global__ void k_check_le(const lab_t* L, int64_t n, int* flags) {
 // Pointer-jumping compress L[v] = L[L[v]] (north-star step 4; the semantic
 // model is normalize_labels, baselines.py:146-152).
 // Four labels per thread per iteration (one uint4 load, four independent
-// gathers): the pass is latency-bound on the dependent L[L[x]] load, so ILP
-// is what makes it fast (grid 4096^2: 41 -> see DESIGN 5.14).  Lowerings
+// gathers): the pass is bound by the dependent, random L[L[x]] load, so ILP
+// is what makes it fast.  Lowerings
 // use red.min: L[L[x]] <= L[x] always, and a concurrent writer (a peer GPU's
 // fused exchange) can never be overwritten by a larger value.
 // gate != nullptr: return at once if *gate == 0 (the graph loop's shortcut
