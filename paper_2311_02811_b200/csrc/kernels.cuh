@@ -798,8 +798,12 @@ __global__ void __launch_bounds__(kBT, 1)
     extern __shared__ __align__(128) lab_t sl[];
     __shared__ __align__(8) uint64_t sbar;
     volatile int* vf = flags;
-    if (!vf[wrote_idx] || vf[check_idx]) return;
     const int tid = threadIdx.x;
+    // the skip decision must be uniform across the CTA: another CTA can set
+    // the failure word while this one's threads read it, and a thread that
+    // left early could be the one that issues the slice copy the others wait
+    // for (mbarrier) -- a hang, seen once in ~50 test runs
+    if (__syncthreads_or(tid == 0 && (!vf[wrote_idx] || vf[check_idx]))) return;
     if (tid == 0) {
         mbar_init(&sbar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
