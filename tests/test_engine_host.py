@@ -56,3 +56,22 @@ def test_defaults_match_reference():
 def test_threads_validated_before_any_device_work():
     with pytest.raises(ValueError):
         run_contour((3, [(0, 1), (1, 2)]), make_schedule("c2"), threads=0)
+
+
+def test_auto_layout_policy():
+    """engine.resolve_layout: input order for small inputs, L2 windows for label
+    arrays beyond L2, the hybrid layout only for dense graphs staged once and
+    run from HBM (m >= 8n, m < 2^31), chunk_sorted otherwise and for one-shot
+    host runs (sweep 1 streams behind the copy)."""
+    from paper_2311_02811_b200.engine import resolve_layout
+    assert resolve_layout("auto", (1 << 20) - 1, 1000) == "input"
+    assert resolve_layout("auto", 134217728, 4194304) == "hybrid"               # RMAT-22
+    assert resolve_layout("auto", 134217728, 4194304, resident=False) == "chunk_sorted"
+    assert resolve_layout("auto", 18446634, 16777216) == "chunk_sorted"          # grid 4096^2
+    assert resolve_layout("auto", 8589934592, 268435456) == "l2_tiled"           # RMAT-28
+    assert resolve_layout("auto", 1845476017, 2307095021) == "l2_tiled"          # forest
+    assert resolve_layout("auto", 1 << 31, 1 << 24) == "chunk_sorted"            # m >= 2^31
+    for lay in ("input", "src_sorted", "chunk_sorted", "dst_bucketed", "l2_tiled", "hybrid"):
+        assert resolve_layout(lay, 10, 10) == lay
+    with pytest.raises(ValueError):
+        resolve_layout("bogus", 10, 10)
