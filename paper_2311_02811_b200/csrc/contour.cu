@@ -575,6 +575,7 @@ struct cc_ctx {
     void* stage_buf[2] = {nullptr, nullptr};  // cached H2D staging buffers
     size_t stage_buf_bytes = 0;
     cudaEvent_t copied[2] = {nullptr, nullptr}, freed[2] = {nullptr, nullptr};
+    cudaEvent_t spec_ready = nullptr, spec_done = nullptr;  // speculative label read-back
     // graph-captured convergence loop (built lazily, rebuilt when its key changes)
     cudaStream_t cap_stream = nullptr, body_stream = nullptr;
     cudaGraph_t loop_graph = nullptr;
@@ -1224,6 +1225,30 @@ int run_graph(cc_ctx* c, const cc_schedule* s, int64_t cap, void* labels_out, in
     return copy_out(c, labels_out, out_eb);
 }
 
+// Enqueue the label read-back on stream st (int32/uint32 or int64 host array).
+int copy_labels_async(cc_ctx* c, void* out, int eb, cudaStream_t st) {
+    if (c->n == 0 || !out) return CC_OK;
+    if (eb == 4) {
+        CUDA_TRY(cudaMemcpyAsync(out, c->labels, sizeof(lab_t) * c->n, cudaMemcpyDeviceToHost,
+                                 st));
+        return CC_OK;
+    }
+    if (eb != 8) return fail(CC_EINVAL, "label element size must be 4 or 8");
+    if (c->wide_cap < c->n) {
+        CUDA_TRY(cudaStreamSynchronize(c->stream));
+        CUDA_TRY(cudaStreamSynchronize(c->copy_stream));
+        cudaFree(c->wide);
+        c->wide = nullptr;
+        c->wide_cap = 0;
+        CUDA_TRY(cudaMalloc((void**)&c->wide, sizeof(int64_t) * c->n));
+        c->wide_cap = c->n;
+    }
+    k_widen<<<grid_for(c, c->n), kThreads, 0, st>>>(c->labels, c->n, c->wide);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaMemcpyAsync(out, c->wide, sizeof(int64_t) * c->n, cudaMemcpyDeviceToHost, st));
+    return CC_OK;
+}
+
 int copy_out(cc_ctx* c, void* out, int eb) {
     if (c->n == 0 || !out) return CC_OK;
     if (eb == 4) {
@@ -1290,7 +1315,8 @@ int sort_rows(cc_ctx* c, int64_t off, int64_t len) {
 // too), so it is sweep 1 of the run, overlapped with the transfer.
 template <typename T>
 int stage_impl(cc_ctx* c, const T* edges, int64_t m, bool host,
-               const cc_schedule* ss = nullptr, bool ss_check = false) {
+               const cc_schedule* ss = nullptr, bool ss_check = false, void* spec_out = nullptr,
+               int spec_eb = 8) {
     CUDA_TRY(cudaMemsetAsync(c->dflags + kFlagBad, 0, sizeof(int), c->stream));
     const int ssm = ss ? (ss->atomic ? c->store_mode_atomic : c->store_mode_plain) : 0;
     if (ss) {
@@ -1355,6 +1381,16 @@ int stage_impl(cc_ctx* c, const T* edges, int64_t m, bool host,
         for (int j = 0; j < c->shortcut; ++j)
             k_compress<<<grid_for(c, (c->n + 3) / 4), kThreads, 0, c->stream>>>(c->labels, c->n,
                                                                       c->dflags);
+        if (spec_out) {
+            // speculative read-back of the labels after sweep 1 on the copy
+            // stream, overlapped with the check / confirming sweep: it is the
+            // answer whenever nothing changes after this point
+            // (cc_run_host decides, spec_valid)
+            CUDA_TRY(cudaEventRecord(c->spec_ready, c->stream));
+            CUDA_TRY(cudaStreamWaitEvent(c->copy_stream, c->spec_ready, 0));
+            CC_TRY(copy_labels_async(c, spec_out, spec_eb, c->copy_stream));
+            CUDA_TRY(cudaEventRecord(c->spec_done, c->copy_stream));
+        }
         if (ss_check) {
             k_gcheck_idem<<<grid_for(c, c->n), kThreads, 0, c->stream>>>(c->labels, c->n,
                                                                           c->dflags);
@@ -1364,20 +1400,27 @@ int stage_impl(cc_ctx* c, const T* edges, int64_t m, bool host,
         }
         CUDA_TRY(cudaGetLastError());
     }
-    CC_TRY(read_flags(c));
+    const int rc = read_flags(c);
+    if (spec_out && (rc || c->hflags[kFlagBad]))
+        cudaEventSynchronize(c->spec_done);  // no read-back in flight after a failure
+    if (rc) return rc;
     if (c->hflags[kFlagBad]) return fail(CC_EINVAL, "edge endpoint out of range (n=%lld)",
                                          (long long)c->n);
     return CC_OK;
 }
 
 int stage(cc_ctx* c, const void* edges, int eb, int64_t m, int64_t n, bool host,
-          const cc_schedule* ss = nullptr, bool ss_check = false) {
+          const cc_schedule* ss = nullptr, bool ss_check = false, void* spec_out = nullptr,
+          int spec_eb = 8) {
     if (eb != 4 && eb != 8) return fail(CC_EINVAL, "edge element size must be 4 or 8");
     if (m > 0 && !edges) return fail(CC_EINVAL, "null edge buffer");
     CC_TRY(set_graph(c, m, n));
     CC_TRY(ensure_edges(c, m));
-    if (eb == 4) return stage_impl<int32_t>(c, (const int32_t*)edges, m, host, ss, ss_check);
-    return stage_impl<int64_t>(c, (const int64_t*)edges, m, host, ss, ss_check);
+    if (eb == 4)
+        return stage_impl<int32_t>(c, (const int32_t*)edges, m, host, ss, ss_check, spec_out,
+                                   spec_eb);
+    return stage_impl<int64_t>(c, (const int64_t*)edges, m, host, ss, ss_check, spec_out,
+                               spec_eb);
 }
 
 }  // namespace
@@ -1419,6 +1462,8 @@ int cc_create(int device, void* stream, cc_ctx** out) {
         CUDA_TRY(cudaEventCreateWithFlags(&c->copied[b], cudaEventDisableTiming));
         CUDA_TRY(cudaEventCreateWithFlags(&c->freed[b], cudaEventDisableTiming));
     }
+    CUDA_TRY(cudaEventCreateWithFlags(&c->spec_ready, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&c->spec_done, cudaEventDisableTiming));
     CUDA_TRY(cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
     CUDA_TRY(cudaStreamCreateWithFlags(&c->body_stream, cudaStreamNonBlocking));
     *out = c;
@@ -1449,6 +1494,8 @@ void cc_destroy(cc_ctx* c) {
         cudaEventDestroy(c->freed[b]);
         cudaFree(c->stage_buf[b]);
     }
+    cudaEventDestroy(c->spec_ready);
+    cudaEventDestroy(c->spec_done);
     cudaFree(c->sort_ks);
     cudaFree(c->sort_vs);
     cudaFree(c->sort_tmp);
@@ -1725,7 +1772,7 @@ int cc_run_host(cc_ctx* c, const void* edges_host, int elem_bytes, int64_t m, in
         return run_impl(c, s, flags, cap, labels_out, out_eb, st);
     }
     const bool check = (flags & CC_RUN_EARLY_CHECK) != 0;
-    CC_TRY(stage(c, edges_host, elem_bytes, m, n, true, s, check));
+    CC_TRY(stage(c, edges_host, elem_bytes, m, n, true, s, check, labels_out, out_eb));
     const bool wrote = c->hflags[kFlagWrote] != 0;
     const bool passed = check && wrote && c->hflags[kFlagCheck] == 0;
     float sweep1_ms = 0.f;
@@ -1736,16 +1783,33 @@ int cc_run_host(cc_ctx* c, const void* edges_host, int elem_bytes, int64_t m, in
     int rounds = 0;
     if (wrote && !passed) {  // not converged after sweep 1: the loop from sweep 2
         CUDA_TRY(cudaMemsetAsync(c->dflags, 0, sizeof(int) * kNumFlags, c->stream));
-        CC_TRY(run_graph(c, s, cap, nullptr, out_eb, st, check ? 1 : 0, 1));
-        if (st) {
-            k = st->sweeps_executed;
-            until_stable = st->sweeps_until_stable;
-            by = st->converged_by;
-            rounds = st->compress_rounds;
-            seconds += st->converge_seconds;
+        cc_stats local = {};
+        cc_stats* gs = st ? st : &local;
+        const int rc = run_graph(c, s, cap, nullptr, out_eb, gs, check ? 1 : 0, 1);
+        if (rc) {  // (e.g. the cap) -- no read-back may still be writing the caller's buffer
+            if (labels_out) cudaEventSynchronize(c->spec_done);
+            return rc;
         }
+        k = gs->sweeps_executed;
+        until_stable = gs->sweeps_until_stable;
+        by = gs->converged_by;
+        rounds = gs->compress_rounds;
+        seconds += gs->converge_seconds;
     } else if (!passed) {
-        CC_TRY(compress(c, &rounds));  // (a passed check already proved idempotence)
+        const int rc = compress(c, &rounds);  // (a passed check already proved idempotence)
+        if (rc) {
+            if (labels_out) cudaEventSynchronize(c->spec_done);
+            return rc;
+        }
+    }
+    // the speculative read-back (stage_impl) holds the final labels iff nothing
+    // changed after sweep 1's shortcut: converged at sweep 1, or sweep 2 was a
+    // no-write sweep (its shortcut and the final compress are then gated off)
+    // and no compress round changed anything
+    const bool spec_valid = rounds == 0 && (k == 1 || (k == 2 && by == 0));
+    if (labels_out && c->n > 0) {
+        CUDA_TRY(cudaEventSynchronize(c->spec_done));  // before the buffer is reused
+        if (spec_valid) labels_out = nullptr;
     }
     if (st) {
         st->sweeps_executed = k;
