@@ -132,14 +132,20 @@ __global__ void k_check_edges(const lab_t* __restrict__ src, const lab_t* __rest
 // returns when idempotence already failed, and polls the failure word every
 // 16 iterations (one load per warp), so a failing check -- the common case
 // before convergence -- costs a small fraction of a pass.
+// Launched after the edge half (which fails fast before convergence), so it
+// mostly returns at once; the CTA-wide skip decision is uniform (the flag can
+// be set by another CTA meanwhile) because the pass ends in a barrier.
 __global__ void __launch_bounds__(kThreads) k_gcheck_idem(const lab_t* __restrict__ L, int64_t n,
                                                           int* flags) {
-    if (!*(volatile int*)&flags[kFlagWrote]) return;
+    volatile int* vf = flags;
+    if (__syncthreads_or(threadIdx.x == 0 && (!vf[kFlagWrote] || vf[kFlagCheck]))) return;
     bool bad = false;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+    int it = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n && !bad;
          i += (int64_t)gridDim.x * blockDim.x) {
+        if ((++it & 15) == 0 && vf[kFlagCheck]) break;
         const lab_t l = L[i];
-        bad |= (L[l] != l);
+        bad = (L[l] != l);
     }
     if (__syncthreads_or(bad) && threadIdx.x == 0) flags[kFlagCheck] = 1;
 }
@@ -1140,14 +1146,14 @@ int build_loop(cc_ctx* c, const cc_schedule* s, int64_t cap, int sm, int check, 
     for (int j = 0; j < c->shortcut; ++j)
         k_compress<<<grid_for(c, (c->n + 3) / 4), kThreads, 0, c->body_stream>>>(
             c->labels, c->n, c->dflags, c->dflags + kFlagWrote);
-    if (check) {
-        k_gcheck_idem<<<grid_for(c, c->n), kThreads, 0, c->body_stream>>>(c->labels, c->n,
-                                                                          c->dflags);
+    if (check) {  // edge half first: it fails within microseconds before convergence
         if (c->m > 0 && has_buckets(c) && !c->bucket_nosmem)
             CC_TRY(launch_check_slice(c, c->body_stream));
         else if (c->m > 0)
             k_gcheck_edges<<<grid_for(c, (c->m + 3) / 4), kThreads, 0, c->body_stream>>>(
                 c->src, c->dst, c->m, c->labels, c->dflags);
+        k_gcheck_idem<<<grid_for(c, c->n), kThreads, 0, c->body_stream>>>(c->labels, c->n,
+                                                                          c->dflags);
     }
     k_loop_control<<<1, 1, 0, c->body_stream>>>(c->dstate, c->drec, c->dflags, *s, cap, check,
                                                 h);
@@ -1392,11 +1398,11 @@ int stage_impl(cc_ctx* c, const T* edges, int64_t m, bool host,
             CUDA_TRY(cudaEventRecord(c->spec_done, c->copy_stream));
         }
         if (ss_check) {
-            k_gcheck_idem<<<grid_for(c, c->n), kThreads, 0, c->stream>>>(c->labels, c->n,
-                                                                          c->dflags);
             if (m > 0)
                 k_gcheck_edges<<<grid_for(c, (m + 3) / 4), kThreads, 0, c->stream>>>(
                     c->src, c->dst, m, c->labels, c->dflags);
+            k_gcheck_idem<<<grid_for(c, c->n), kThreads, 0, c->stream>>>(c->labels, c->n,
+                                                                          c->dflags);
         }
         CUDA_TRY(cudaGetLastError());
     }
