@@ -89,6 +89,16 @@ def parse():
     return p.parse_args()
 
 
+def physical_cores():
+    """Physical core count of the host (SURVEY 8(d) asks for it beside the
+    logical count the CPU legs use), or None when psutil cannot tell."""
+    try:
+        import psutil
+        return psutil.cpu_count(logical=False)
+    except Exception:  # noqa: BLE001 -- reporting only
+        return None
+
+
 def dist_env():
     return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
             int(os.environ.get("LOCAL_RANK", 0)))
@@ -221,6 +231,7 @@ def run_reference_arm(args):
                    "schedule": f"C-2 async atomic={atomic}",
                    "parallelism": f"{threads} host threads (static edge chunks, engine.py:296-308)"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "cores_physical": physical_cores(),
                          "sample": f"full workload, {args.steps} timed runs after {args.warmup} "
                                    f"warm-up; sweeps_executed={st.sweeps_executed}, "
                                    f"converged_by={st.converged_by}"},
@@ -417,6 +428,7 @@ def run_single(args, device):
         threads = os.cpu_count() or 1
         t_cpu, st_cpu = cpu_baseline(n, host_edges, threads, atomic=bool(args.atomic))
         cpu = {"value": m / t_cpu, "unit": UNIT, "cores": threads, "kind": "port",
+               "cores_physical": physical_cores(),
                "sample": f"1 full run of the same workload (oracle port of run_contour, C-2 "
                          f"async atomic={bool(args.atomic)}, {threads} threads): {t_cpu:.2f} s, "
                          f"sweeps_executed={st_cpu.sweeps_executed}"}
