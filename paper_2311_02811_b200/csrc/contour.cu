@@ -440,6 +440,7 @@ struct SweepRec {
     unsigned long long t;
 };
 constexpr int kMaxRec = 4096;
+constexpr int kEagerRec = 64;  // records copied back with every graph run
 
 __device__ __forceinline__ unsigned long long globaltimer() {
     unsigned long long t;
@@ -1162,6 +1163,15 @@ int build_loop(cc_ctx* c, const cc_schedule* s, int64_t cap, int sm, int check, 
     CUDA_TRY(cudaStreamEndCapture(c->body_stream, &body_out));
     k_compress<<<grid_for(c, (c->n + 3) / 4), kThreads, 0, cs>>>(c->labels, c->n, c->dflags,
                                                                  &c->dstate->need_compress);
+    // the loop state, the first records and the flags come back inside the
+    // graph (memcpy nodes into pinned memory): run_graph then needs one
+    // launch and one synchronisation, no further API calls per run
+    CUDA_TRY(cudaMemcpyAsync(c->hstate, c->dstate, sizeof(LoopState), cudaMemcpyDeviceToHost,
+                             cs));
+    CUDA_TRY(cudaMemcpyAsync(c->hrec, c->drec, sizeof(SweepRec) * kEagerRec,
+                             cudaMemcpyDeviceToHost, cs));
+    CUDA_TRY(cudaMemcpyAsync(c->hflags, c->dflags, sizeof(int) * kNumFlags,
+                             cudaMemcpyDeviceToHost, cs));
     CUDA_TRY(cudaStreamEndCapture(cs, &c->loop_graph));
     CUDA_TRY(cudaGraphInstantiate(&c->loop_exec, c->loop_graph, 0));
     k = {c->src, c->dst,   c->labels, c->m,     c->n,       cap,   *s,
@@ -1182,15 +1192,10 @@ int run_graph(cc_ctx* c, const cc_schedule* s, int64_t cap, void* labels_out, in
     CUDA_TRY(cudaEventRecord(c->evs, c->stream));
     CUDA_TRY(cudaGraphLaunch(c->loop_exec, c->stream));
     CUDA_TRY(cudaEventRecord(c->eve, c->stream));
-    // one synchronisation: state, flags and the first records come back together
-    constexpr int kEagerRec = 64;
+    // one synchronisation: state, flags and the first records were copied
+    // back by the graph itself (build_loop)
     const bool want_rec = st && (st->changed_per_sweep || st->sweep_seconds);
-    CUDA_TRY(cudaMemcpyAsync(c->hstate, c->dstate, sizeof(LoopState), cudaMemcpyDeviceToHost,
-                             c->stream));
-    if (want_rec)
-        CUDA_TRY(cudaMemcpyAsync(c->hrec, c->drec, sizeof(SweepRec) * kEagerRec,
-                                 cudaMemcpyDeviceToHost, c->stream));
-    CC_TRY(read_flags(c));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
     const long long k = c->hstate->sweep;
     if (c->hstate->capped)
         return fail(CC_ECAP, "no convergence after %lld sweeps on n=%lld, m=%lld",

@@ -244,8 +244,9 @@ class _RunCall:
                  first_scatter=False, host_loop=False):
         self.cap = n + 2 if cap is None else int(cap)  # engine.py:275
         capacity = max(1, min(self.cap, 1 << 12 if not count_changes else 1 << 16))
-        self.changed = np.zeros(capacity, dtype=np.int64)
-        self.secs = np.zeros(capacity, dtype=np.float64)
+        # the library writes entries [0, sweeps_executed) -- no need to clear
+        self.changed = np.empty(capacity, dtype=np.int64)
+        self.secs = np.empty(capacity, dtype=np.float64)
         st = _lib.CCStats()
         st.capacity = capacity
         st.changed_per_sweep = self.changed.ctypes.data_as(_lib._I64P)
