@@ -189,6 +189,10 @@ int cc_early_check(cc_ctx* ctx, int* ok_out);
  * L[x] > x; 0 means every component carries one root label <= its IDs. */
 int cc_verify(cc_ctx* ctx, int* result);
 int cc_read_labels(cc_ctx* ctx, void* out_host, int elem_bytes);
+/* Load caller labels (n int64 or int32 host values, each in 0..n-1, else
+ * CC_EINVAL) as the device labels -- e.g. before cc_early_check on labels
+ * from elsewhere (early_convergence_check(g, labels), engine.py:331-348). */
+int cc_write_labels(cc_ctx* ctx, const void* labels_host, int elem_bytes);
 int cc_synchronize(cc_ctx* ctx);
 
 /* Single-edge operator mm_order(target, read, w, v, order, atomic)

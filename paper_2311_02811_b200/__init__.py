@@ -5,10 +5,14 @@ points (engine.py) mirrored here as a drop-in."""
 
 from .engine import (
     VARIANTS,
+    ForestDiagnostics,
     IterationStats,
     LabelArray,
     Schedule,
     canonical_variant,
+    conditional_min_assign,
+    early_convergence_check,
+    forest_diagnostics,
     make_schedule,
     mm_order,
     run_contour,
@@ -18,6 +22,8 @@ from .errors import IterationCapExceeded
 __version__ = "0.1.0"
 
 __all__ = [
-    "VARIANTS", "IterationStats", "LabelArray", "Schedule", "canonical_variant",
-    "make_schedule", "mm_order", "run_contour", "IterationCapExceeded", "__version__",
+    "VARIANTS", "ForestDiagnostics", "IterationStats", "LabelArray", "Schedule",
+    "canonical_variant", "conditional_min_assign", "early_convergence_check",
+    "forest_diagnostics", "make_schedule", "mm_order", "run_contour", "IterationCapExceeded",
+    "__version__",
 ]

@@ -396,6 +396,21 @@ __global__ void k_widen(const lab_t* L, int64_t n, int64_t* out) {
         out[i] = (int64_t)L[i];
 }
 
+// Caller labels (int64 or int32/uint32 as T) -> device labels, with the
+// range check 0 <= x < n (kFlagBad).
+template <typename T>
+__global__ void k_labels_in(const T* in, int64_t n, lab_t* L, int* flags) {
+    bool bad = false;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const T x = in[i];
+        const bool out = (int64_t)x < 0 || (int64_t)x >= n;
+        bad |= out;
+        L[i] = out ? (lab_t)i : (lab_t)x;
+    }
+    if (__syncthreads_or(bad) && threadIdx.x == 0) flags[kFlagBad] = 1;
+}
+
 __global__ void k_from64(const int64_t* in, int64_t n, lab_t* L) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x)
@@ -1655,6 +1670,34 @@ int cc_verify(cc_ctx* c, int* result) {
         edge_bad = c->hflags[kFlagBad];
     }
     *result = (edge_bad ? 1 : 0) | (idem_bad ? 2 : 0) | (le_bad ? 4 : 0);
+    return CC_OK;
+}
+
+int cc_write_labels(cc_ctx* c, const void* in, int eb) {
+    if (!c || (!in && c->n > 0)) return fail(CC_EINVAL, "null argument");
+    if (eb != 4 && eb != 8) return fail(CC_EINVAL, "label element size must be 4 or 8");
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard g(c->device);
+    if (c->n == 0) return CC_OK;
+    CC_TRY(ensure_labels(c));
+    if (c->wide_cap < c->n) {  // staging buffer: the int64 read-back buffer
+        cudaFree(c->wide);
+        c->wide = nullptr;
+        c->wide_cap = 0;
+        CUDA_TRY(cudaMalloc((void**)&c->wide, sizeof(int64_t) * c->n));
+        c->wide_cap = c->n;
+    }
+    CUDA_TRY(cudaMemcpyAsync(c->wide, in, (size_t)eb * c->n, cudaMemcpyHostToDevice, c->stream));
+    CUDA_TRY(cudaMemsetAsync(c->dflags + kFlagBad, 0, sizeof(int), c->stream));
+    if (eb == 8)
+        k_labels_in<int64_t><<<grid_for(c, c->n), kThreads, 0, c->stream>>>(
+            (const int64_t*)c->wide, c->n, c->labels, c->dflags);
+    else
+        k_labels_in<int32_t><<<grid_for(c, c->n), kThreads, 0, c->stream>>>(
+            (const int32_t*)c->wide, c->n, c->labels, c->dflags);
+    CUDA_TRY(cudaGetLastError());
+    CC_TRY(read_flags(c));
+    if (c->hflags[kFlagBad]) return fail(CC_EINVAL, "labels reference vertices outside 0..n-1");
     return CC_OK;
 }
 

@@ -21,8 +21,9 @@ from . import _lib
 from .errors import IterationCapExceeded
 
 __all__ = [
-    "LabelArray", "Schedule", "IterationStats", "VARIANTS", "canonical_variant",
-    "make_schedule", "run_contour", "mm_order", "IterationCapExceeded", "stage_graph",
+    "LabelArray", "Schedule", "IterationStats", "ForestDiagnostics", "VARIANTS",
+    "canonical_variant", "conditional_min_assign", "make_schedule", "run_contour", "mm_order",
+    "early_convergence_check", "forest_diagnostics", "IterationCapExceeded", "stage_graph",
 ]
 
 LabelArray = np.ndarray  # (n,) int64, as engine.py:44
@@ -351,6 +352,96 @@ def run_contour(g, schedule: Schedule, threads: int = 1, seed: Optional[int] = N
                             early_check=early_check, sweep_times=sweep_times, labels_out=labels,
                             first_scatter=first_scatter, host_loop=host_loop)
     return labels, stats
+
+
+def early_convergence_check(g, labels, parallel: bool = False, *, device: int = 0) -> bool:
+    """True iff the labels are idempotent (L[L[x]] == L[x]) and both endpoints
+    of every edge agree -- engine.py:331-348, evaluated on the device
+    (cc_write_labels + cc_early_check).  ``parallel`` is accepted for the
+    reference's signature; the device check is always parallel.  Labels must
+    lie in 0..n-1 (ValueError otherwise; numpy indexing in the reference would
+    fail or wrap on such input)."""
+    n, edges = _unpack_graph(g)
+    lab = np.asarray(labels)
+    if lab.shape[0] != n:
+        raise ValueError("label array length does not match vertex count")  # engine.py:339-340
+    if n == 0:
+        return True
+    if lab.dtype not in (np.int64, np.int32):
+        lab = lab.astype(np.int64)
+    lab = np.ascontiguousarray(lab)
+    ctx = _context(device)
+    stage_graph(ctx, n, edges, "input")
+    _lib.check(ctx.lib.cc_write_labels(ctx.handle, ctypes.c_void_p(lab.ctypes.data),
+                                       lab.dtype.itemsize))
+    ok = ctypes.c_int(0)
+    _lib.check(ctx.lib.cc_early_check(ctx.handle, ctypes.byref(ok)))
+    return bool(ok.value)
+
+
+_cas_lock = threading.Lock()
+
+
+def conditional_min_assign(labels: np.ndarray, cells, value: int, atomic: bool = False) -> bool:
+    """Lower every referenced cell holding more than ``value`` to it; True if
+    any changed (engine.py:158-189).  The scalar host form of the update the
+    device sweeps apply (``lower`` in csrc/kernels.cuh); ``atomic`` makes
+    each lowering a compare-and-swap, so concurrent callers never lose one."""
+    changed = False
+    for i in cells:
+        if atomic:
+            with _cas_lock:  # the CAS retry loop collapses to one locked compare
+                if labels[i] > value:
+                    labels[i] = value
+                    changed = True
+        elif labels[i] > value:
+            labels[i] = value
+            changed = True
+    return changed
+
+
+@dataclass
+class ForestDiagnostics:
+    """Pointer-graph structure v -> labels[v] (engine.py:92-105): the roots,
+    each root's tree height, label-class sizes, number of label values."""
+
+    roots: np.ndarray
+    heights: dict
+    class_sizes: dict
+    merged_min_count: int
+
+
+def forest_diagnostics(labels) -> ForestDiagnostics:
+    """Roots, per-root tree heights and label-class sizes of a pointer graph
+    (engine.py:373-405).  Host-side diagnostics, not part of the run: depths
+    by pointer doubling (O(n log depth) gathers); a cycle raises
+    IterationCapExceeded as in the reference."""
+    lab = np.asarray(labels, dtype=np.int64)
+    n = lab.shape[0]
+    if n and (lab.min() < 0 or lab.max() >= n):
+        raise ValueError("labels reference vertices outside 0..n-1")
+    idx = np.arange(n, dtype=np.int64)
+    # jump[x] = 2^k-th ancestor, dist[x] = steps taken to reach it (stops at roots)
+    jump = lab.copy()
+    dist = (jump != idx).astype(np.int64)
+    for _ in range(64):
+        nxt = jump[jump]
+        if np.array_equal(nxt, jump):
+            break
+        dist = dist + dist[jump]
+        jump = nxt
+    else:
+        raise IterationCapExceeded("cycle detected in pointer graph")
+    if n and np.any(lab[jump] != jump):
+        raise IterationCapExceeded("cycle detected in pointer graph")
+    roots = np.flatnonzero(lab == idx)
+    height = np.zeros(n, dtype=np.int64)
+    if n:
+        np.maximum.at(height, jump, dist)
+    values, counts = np.unique(lab, return_counts=True)
+    return ForestDiagnostics(roots=roots, heights={int(r): int(height[r]) for r in roots},
+                             class_sizes={int(v): int(c) for v, c in zip(values, counts)},
+                             merged_min_count=int(values.size))
 
 
 def mm_order(target: np.ndarray, read: np.ndarray, w: int, v: int, order: int,

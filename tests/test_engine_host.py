@@ -75,3 +75,48 @@ def test_auto_layout_policy():
         assert resolve_layout(lay, 10, 10) == lay
     with pytest.raises(ValueError):
         resolve_layout("bogus", 10, 10)
+
+
+def test_conditional_min_assign_semantics():
+    """engine.py:158-189: only cells strictly above the value are lowered;
+    atomic and plain modes agree."""
+    import numpy as np
+    from paper_2311_02811_b200 import conditional_min_assign
+    a = np.array([5, 2, 8, 3], dtype=np.int64)
+    assert conditional_min_assign(a, [0, 2, 3], 3) is True
+    assert a.tolist() == [3, 2, 3, 3]
+    assert conditional_min_assign(a, [1, 3], 3) is False  # equal or below: untouched
+    b = np.array([6, 1, 9], dtype=np.int64)
+    c = b.copy()
+    assert conditional_min_assign(b, [0, 2], 4) == conditional_min_assign(c, [0, 2], 4, True)
+    assert b.tolist() == c.tolist() == [4, 1, 4]
+
+
+def test_forest_diagnostics_matches_a_chain_walk():
+    """engine.py:373-405 restated by pointer doubling: roots, heights, class
+    sizes against a direct per-vertex chain walk, plus the error cases."""
+    import numpy as np
+    from paper_2311_02811_b200 import IterationCapExceeded, forest_diagnostics
+    rng = np.random.default_rng(7)
+    for n in (0, 1, 2, 9, 200, 1500):
+        lab = np.array([int(rng.integers(0, i + 1)) for i in range(n)], dtype=np.int64)
+        d = forest_diagnostics(lab)
+        roots = [x for x in range(n) if lab[x] == x]
+        heights = {r: 0 for r in roots}
+        for x in range(n):
+            y, depth = x, 0
+            while lab[y] != y:
+                y, depth = int(lab[y]), depth + 1
+            heights[y] = max(heights[y], depth)
+        sizes = {}
+        for v in lab.tolist():
+            sizes[v] = sizes.get(v, 0) + 1
+        assert d.roots.tolist() == roots
+        assert d.heights == heights
+        assert d.class_sizes == sizes and d.merged_min_count == len(sizes)
+    d = forest_diagnostics(np.array([0, 0, 1, 2, 3]))
+    assert d.heights == {0: 4} and d.class_sizes == {0: 2, 1: 1, 2: 1, 3: 1}
+    with pytest.raises(ValueError):
+        forest_diagnostics(np.array([0, 3]))
+    with pytest.raises(IterationCapExceeded):
+        forest_diagnostics(np.array([1, 0, 2]))  # 0 <-> 1 cycle

@@ -453,6 +453,31 @@ def test_random_graphs_every_layout_and_loop():
     ctx.close()
 
 
+def test_early_convergence_check_api():
+    """early_convergence_check(g, labels) (engine.py:331-348) on the device
+    through cc_write_labels + cc_early_check, against the oracle restatement."""
+    from paper_2311_02811_b200 import early_convergence_check
+    rng = np.random.default_rng(11)
+    assert early_convergence_check((0, np.zeros((0, 2), np.int64)), np.zeros(0, np.int64))
+    assert not early_convergence_check((3, np.zeros((0, 2), np.int64)), np.array([0, 0, 1]))
+    assert early_convergence_check((3, np.zeros((0, 2), np.int64)), np.array([0, 1, 2]))
+    with pytest.raises(ValueError):
+        early_convergence_check((3, [(0, 1)]), np.array([0, 0]))
+    with pytest.raises(ValueError):
+        early_convergence_check((3, [(0, 1)]), np.array([0, 0, 7]))
+    for n, e in (graphgen.rmat(12, 16, 4), graphgen.grid(60, 70, 0.55, 2),
+                 spec.erdos_renyi(3000, 4000, 5)):
+        done = oracle.rem_union_find(n, e)
+        assert early_convergence_check((n, e), done) is True
+        for _ in range(6):
+            lab = done.copy()
+            x = int(rng.integers(0, n))
+            lab[x] = x if done[x] != x else lab[x]  # detach one vertex (or keep a root)
+            exp = oracle.early_convergence_check(n, e, lab)
+            assert early_convergence_check((n, e), lab) is exp
+            assert early_convergence_check((n, e), lab.astype(np.int32)) is exp
+
+
 def test_run_host_streamed_first_sweep(golden):
     """cc_run_host: sweep 1 streamed behind the host-to-device copy, then the
     loop from sweep 2 -- exact labels, consistent stats, errors as staging."""
