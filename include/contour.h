@@ -170,6 +170,9 @@ int cc_reorder_edges(cc_ctx* ctx, int mode);
                                       rows cut into sort_chunk runs in input order, items ordered
                                       (run, bucket) so the GPU walks each run's src range in order,
                                       2 run-major with the items of a run staggered over src */
+#define CC_OPT_WARP_TRANSPOSE 15   /* sorted layouts: store each 128-row block transposed so a
+                                      warp's k-th gather reads 32 consecutive sorted rows (default
+                                      1; applied when the layout is built) */
 #define CC_OPT_STAGE_LAYOUT 4     /* layout applied while staging: 0 input order (default),
                                       2 chunk-sorted, each chunk sorted as soon as it lands,
                                       overlapped with the next chunk's host->device copy */

@@ -377,10 +377,14 @@ int run_impl(cc_ctx* c, const cc_schedule* s, int flags, int64_t cap, void* labe
         }
         if (!wrote && changed == 0) { converged_by = 0; break; }
         until_stable = sweep;
-        if (check) {
-            int ok = 0;
-            CC_TRY(early_check(c, &ok));
-            if (ok) { converged_by = 1; break; }
+        if (check) {  // the graph loop's check kernels (same layout-aware halves)
+            CUDA_TRY(cudaMemsetAsync(c->dflags + kFlagCheck, 0, sizeof(int), c->stream));
+            // the check kernels skip when the wrote word is 0; this sweep changed
+            // labels (sync / count modes tell it by the diff count)
+            CUDA_TRY(cudaMemsetAsync(c->dflags + kFlagWrote, 1, 1, c->stream));
+            CC_TRY(enqueue_loop_check(c, c->stream));
+            CC_TRY(read_flags(c));
+            if (!c->hflags[kFlagCheck]) { converged_by = 1; break; }
         }
     }
     int rounds = 0;
@@ -679,6 +683,9 @@ int cc_set_option(cc_ctx* c, int option, int64_t value) {
         case CC_OPT_TILE_SHIFT:
             if (value < 10 || value > 30) return fail(CC_EINVAL, "tile shift must be in [10, 30]");
             c->tile_shift = (int)value;
+            return CC_OK;
+        case CC_OPT_WARP_TRANSPOSE:
+            c->warp_transpose = value != 0;
             return CC_OK;
         case CC_OPT_BUCKET_THREADS:
             if (value != 256 && value != 512 && value != 1024)

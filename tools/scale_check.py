@@ -37,7 +37,6 @@ def run(cfg, args):
     ctx.set_option(_lib.CC_OPT_SORT_CHUNK, args.sort_chunk)
     ctx.set_option(_lib.CC_OPT_BUCKET_SHIFT, args.bshift)
     ctx.set_option(_lib.CC_OPT_TILE_SPLIT, args.tsplit)
-    ctx.set_option(_lib.CC_OPT_SHORTCUT, args.shortcut)
     if args.store_mode >= 0:
         ctx.set_option(_lib.CC_OPT_STORE_MODE_ATOMIC, args.store_mode)
     ctx.set_option(_lib.CC_OPT_TILE_SHIFT, args.tshift)
@@ -64,6 +63,19 @@ def run(cfg, args):
     rec.update(n=int(n), m_input=int(m), layout=lay, layout_s=round(time.perf_counter() - t1, 3),
                prep_s=round(time.perf_counter() - t0, 2))
     sched = make_schedule("c2")
+    shortcuts = [int(x) for x in str(args.shortcut).split(",")]
+    for sc in shortcuts[:-1]:  # extra shortcut settings: timing lines only
+        ctx.set_option(_lib.CC_OPT_SHORTCUT, sc)
+        runs = [engine.run_staged(ctx, sched, count_changes=False, early_check=args.early_check,
+                                  host_loop=bool(args.host_loop))[1] for _ in range(args.repeats)]
+        best = min(runs, key=lambda s: s.device_seconds)
+        print(json.dumps(dict(rec, shortcut=sc, n=int(n), m_input=int(m), layout=lay,
+                              device_s=best.device_seconds,
+                              sweeps=[s.sweeps_executed for s in runs],
+                              sweep_ms=[round(t * 1e3, 3) for t in best.sweep_seconds],
+                              verify=engine.verify_staged(ctx))), flush=True)
+    ctx.set_option(_lib.CC_OPT_SHORTCUT, shortcuts[-1])
+    rec["shortcut"] = shortcuts[-1]
     runs = []
     for _ in range(args.repeats):
         _, st = engine.run_staged(ctx, sched, count_changes=False, early_check=args.early_check,
@@ -123,7 +135,7 @@ def main():
     ap.add_argument("--early-check", type=int, default=0)
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--tsplit", type=int, default=2)
-    ap.add_argument("--shortcut", type=int, default=1)
+    ap.add_argument("--shortcut", default="1", help="comma list: pointer-jumping passes per sweep")
     ap.add_argument("--first-scatter", type=int, default=0)
     ap.add_argument("--store-mode", type=int, default=-1)
     ap.add_argument("--host-loop", type=int, default=0)
