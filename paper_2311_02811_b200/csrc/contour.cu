@@ -111,6 +111,7 @@ void cc_destroy(cc_ctx* c) {
     if (c->own_edges) { cudaFree(c->src); cudaFree(c->dst); }
     cudaFree(c->bsrc);
     cudaFree(c->bdst);
+    cudaFree(c->bdst16);
     if (c->own_labels) cudaFree(c->labels);
     cudaFree(c->wide);
     cudaFree(c->shadow);

@@ -695,15 +695,36 @@ __device__ __forceinline__ bool slice_rows(lab_t* L, lab_t* sl, lab_t base, lab_
     return wrote;
 }
 
+// Dst column of a bucketed row range: absolute uint32 vertex IDs, or (DT =
+// uint16_t, the compact hybrid copy) 16-bit offsets into the item's slice
+// [base, base + 2^bucket_shift), 2 B per row instead of 4.
+template <typename DT>
+__device__ __forceinline__ void load_dst4(const DT* __restrict__ d, int64_t q, lab_t base,
+                                          lab_t (&v)[4]) {
+    if constexpr (sizeof(DT) == 4) {
+        const uint4 b = __ldcs(reinterpret_cast<const uint4*>(d) + q);
+        v[0] = b.x; v[1] = b.y; v[2] = b.z; v[3] = b.w;
+    } else {
+        const uint2 b = __ldcs(reinterpret_cast<const uint2*>(d) + q);
+        v[0] = base + (b.x & 0xFFFFu); v[1] = base + (b.x >> 16);
+        v[2] = base + (b.y & 0xFFFFu); v[3] = base + (b.y >> 16);
+    }
+}
+template <typename DT>
+__device__ __forceinline__ lab_t load_dst1(const DT* __restrict__ d, int64_t r, lab_t base) {
+    if constexpr (sizeof(DT) == 4) return d[r];
+    else return base + (lab_t)d[r];
+}
+
 // Lean form of k_sweep_bucketed for items with a slice (len > 0): the
 // first-hop dst gather is an unconditional (predicated) shared-memory load
 // and the second hops are predicated global loads -- no divergent branches
 // around the loads, so a thread's gathers issue back to back.  Warps run
 // independently inside an item (no barrier per row batch).  PF: the next
 // batch's edge vectors are loaded before the current batch is processed.
-template <int SM, bool PF>
+template <int SM, bool PF, typename DT = lab_t>
 __global__ void __launch_bounds__(kBT, 1)
-    k_sweep_slice(const lab_t* __restrict__ src, const lab_t* __restrict__ dst, lab_t* L,
+    k_sweep_slice(const lab_t* __restrict__ src, const DT* __restrict__ dst, lab_t* L,
                   const BucketItem* __restrict__ items, int n_items, int* __restrict__ flag,
                   const int* __restrict__ d_order) {
     extern __shared__ __align__(128) lab_t sl[];
@@ -735,45 +756,49 @@ __global__ void __launch_bounds__(kBT, 1)
         const int64_t a0 = min((w.start + 3) & ~(int64_t)3, w.end);
         const int64_t a1 = max(a0, w.end & ~(int64_t)3);
         if (tid < a0 - w.start) {  // <= 3 head rows
-            lab_t u[1] = {src[w.start + tid]}, v[1] = {dst[w.start + tid]};
+            lab_t u[1] = {src[w.start + tid]}, v[1] = {load_dst1(dst, w.start + tid, base)};
             wrote |= slice_rows<SM, 1>(L, sl, base, len, u, v);
         }
         if (tid < w.end - a1) {  // <= 3 tail rows
-            lab_t u[1] = {src[a1 + tid]}, v[1] = {dst[a1 + tid]};
+            lab_t u[1] = {src[a1 + tid]}, v[1] = {load_dst1(dst, a1 + tid, base)};
             wrote |= slice_rows<SM, 1>(L, sl, base, len, u, v);
         }
         const uint4* s4 = reinterpret_cast<const uint4*>(src + a0);
-        const uint4* d4 = reinterpret_cast<const uint4*>(dst + a0);
+        const DT* d0 = dst + a0;
         const int64_t nvec = (a1 - a0) >> 2;
-        const uint4 zero = make_uint4(0, 0, 0, 0);  // u == v: inert
+        // masked rows are inert (u == v): u = base pairs with a zero offset
+        // (compact copy) and u = 0 with a zero vertex ID
+        const lab_t uf = sizeof(DT) == 2 ? base : 0u;
+        const uint4 fill = make_uint4(uf, uf, uf, uf);
         if (PF) {
-            // ping-pong: batch q's vectors in (a0, b0) while q + kBT's load into
-            // (a1, b1) and the other way round -- no register moves per batch
-            uint4 a0v = zero, b0v = zero, a1v, b1v;
+            // ping-pong: batch q's rows in (u0, v0) while q + kBT's load into
+            // (u1, v1) and the other way round -- no register moves per batch
+            lab_t u0[4] = {uf, uf, uf, uf}, v0[4] = {0, 0, 0, 0}, u1[4], v1[4];
+            if (sizeof(DT) == 2) { v0[0] = v0[1] = v0[2] = v0[3] = base; }
             int64_t q = tid;
-            if (q < nvec) { a0v = __ldcs(s4 + q); b0v = __ldcs(d4 + q); }
+            if (q < nvec) {
+                const uint4 a = __ldcs(s4 + q);
+                u0[0] = a.x; u0[1] = a.y; u0[2] = a.z; u0[3] = a.w;
+                load_dst4(d0, q, base, v0);
+            }
             for (; q < nvec; q += 2 * kBT) {
-                a1v = zero;
-                b1v = zero;
-                if (q + kBT < nvec) { a1v = __ldcs(s4 + q + kBT); b1v = __ldcs(d4 + q + kBT); }
-                {
-                    lab_t u[4] = {a0v.x, a0v.y, a0v.z, a0v.w}, v[4] = {b0v.x, b0v.y, b0v.z, b0v.w};
-                    wrote |= slice_rows<SM, 4>(L, sl, base, len, u, v);
-                }
+                uint4 a = fill;
+                if (q + kBT < nvec) { a = __ldcs(s4 + q + kBT); load_dst4(d0, q + kBT, base, v1); }
+                else { v1[0] = v1[1] = v1[2] = v1[3] = uf; }
+                u1[0] = a.x; u1[1] = a.y; u1[2] = a.z; u1[3] = a.w;
+                wrote |= slice_rows<SM, 4>(L, sl, base, len, u0, v0);
                 if (q + kBT >= nvec) break;
-                a0v = zero;
-                b0v = zero;
-                if (q + 2 * kBT < nvec) {
-                    a0v = __ldcs(s4 + q + 2 * kBT);
-                    b0v = __ldcs(d4 + q + 2 * kBT);
-                }
-                lab_t u[4] = {a1v.x, a1v.y, a1v.z, a1v.w}, v[4] = {b1v.x, b1v.y, b1v.z, b1v.w};
-                wrote |= slice_rows<SM, 4>(L, sl, base, len, u, v);
+                a = fill;
+                if (q + 2 * kBT < nvec) { a = __ldcs(s4 + q + 2 * kBT); load_dst4(d0, q + 2 * kBT, base, v0); }
+                else { v0[0] = v0[1] = v0[2] = v0[3] = uf; }
+                u0[0] = a.x; u0[1] = a.y; u0[2] = a.z; u0[3] = a.w;
+                wrote |= slice_rows<SM, 4>(L, sl, base, len, u1, v1);
             }
         } else {
             for (int64_t q = tid; q < nvec; q += kBT) {
-                const uint4 a = __ldcs(s4 + q), b = __ldcs(d4 + q);
-                lab_t u[4] = {a.x, a.y, a.z, a.w}, v[4] = {b.x, b.y, b.z, b.w};
+                const uint4 a = __ldcs(s4 + q);
+                lab_t u[4] = {a.x, a.y, a.z, a.w}, v[4];
+                load_dst4(d0, q, base, v);
                 wrote |= slice_rows<SM, 4>(L, sl, base, len, u, v);
             }
         }
@@ -790,9 +815,9 @@ __global__ void __launch_bounds__(kBT, 1)
 // nothing or the check already failed; poll the failure word every 16 row
 // batches (one load per warp).
 // NV uint4 row vectors per thread per iteration (4*NV independent gathers).
-template <int NV>
+template <int NV, typename DT = lab_t>
 __global__ void __launch_bounds__(kBT, 1)
-    k_check_slice(const lab_t* __restrict__ src, const lab_t* __restrict__ dst,
+    k_check_slice(const lab_t* __restrict__ src, const DT* __restrict__ dst,
                   const lab_t* __restrict__ L, const BucketItem* __restrict__ items, int n_items,
                   int* flags, int wrote_idx, int check_idx) {
     extern __shared__ __align__(128) lab_t sl[];
@@ -826,28 +851,30 @@ __global__ void __launch_bounds__(kBT, 1)
         __syncthreads();
         const int64_t a0 = min((w.start + 3) & ~(int64_t)3, w.end);
         const int64_t a1 = max(a0, w.end & ~(int64_t)3);
-        if (tid < a0 - w.start) bad |= L[src[w.start + tid]] != sl[dst[w.start + tid] - base];
-        if (tid < w.end - a1) bad |= L[src[a1 + tid]] != sl[dst[a1 + tid] - base];
+        if (tid < a0 - w.start)
+            bad |= L[src[w.start + tid]] != sl[load_dst1(dst, w.start + tid, base) - base];
+        if (tid < w.end - a1) bad |= L[src[a1 + tid]] != sl[load_dst1(dst, a1 + tid, base) - base];
         const uint32_t sadj = slice_adj(sl, base);
         const uint4* s4 = reinterpret_cast<const uint4*>(src + a0);
-        const uint4* d4 = reinterpret_cast<const uint4*>(dst + a0);
+        const DT* d0 = dst + a0;
         const int64_t nvec = (a1 - a0) >> 2;
         int k = 0;
         for (int64_t q = tid; q < nvec && !bad; q += (int64_t)kBT * NV) {
             if ((++k & 7) == 0 && vf[check_idx]) break;
-            uint4 a[NV], b[NV];
+            uint4 a[NV];
+            lab_t b[NV][4];
 #pragma unroll
             for (int j = 0; j < NV; ++j) {
                 const int64_t i = q + (int64_t)j * kBT;
-                if (i < nvec) { a[j] = __ldcs(s4 + i); b[j] = __ldcs(d4 + i); }
+                if (i < nvec) { a[j] = __ldcs(s4 + i); load_dst4(d0, i, base, b[j]); }
             }
 #pragma unroll
             for (int j = 0; j < NV; ++j) {
                 if (q + (int64_t)j * kBT < nvec)
-                    bad |= (L[a[j].x] != lds_u32(sadj + 4u * b[j].x)) |
-                           (L[a[j].y] != lds_u32(sadj + 4u * b[j].y)) |
-                           (L[a[j].z] != lds_u32(sadj + 4u * b[j].z)) |
-                           (L[a[j].w] != lds_u32(sadj + 4u * b[j].w));
+                    bad |= (L[a[j].x] != lds_u32(sadj + 4u * b[j][0])) |
+                           (L[a[j].y] != lds_u32(sadj + 4u * b[j][1])) |
+                           (L[a[j].z] != lds_u32(sadj + 4u * b[j][2])) |
+                           (L[a[j].w] != lds_u32(sadj + 4u * b[j][3]));
             }
         }
         if (bad) vf[check_idx] = 1;
