@@ -52,7 +52,7 @@ def parse():
     p.add_argument("--early-check", default="auto", choices=["auto", "on", "off"],
                    help="the reference's early convergence check after each changing sweep "
                         "(engine.py:318-320), inside the device loop.  auto: on for the hybrid "
-                        "layout, whose shared-memory check (0.28 ms on RMAT-22) is cheaper "
+                        "layout, whose shared-memory check (0.18 ms on RMAT-22) is cheaper "
                         "than the confirming sweep it saves; off elsewhere, where the check "
                         "costs what that sweep costs (RMAT-22 1.19 vs 1.15 ms, RMAT-28 158 vs "
                         "122 ms, forest 842 vs 800 ms, measured)")
