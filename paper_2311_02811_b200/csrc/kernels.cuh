@@ -532,6 +532,10 @@ __device__ __forceinline__ bool bucket_rows(lab_t* L, const lab_t* sl, lab_t bas
     for (int k = 0; k < NE; ++k) {
         if (u[k] == v[k]) continue;
         const lab_t z = min(zu[k], zv[k]);
+        // z <= zu <= lu and z <= zv <= lv (every stored label is <= its
+        // cell's index), so nothing is lowered iff max(lu, lv) == z: one
+        // test on the common path of a converging sweep
+        if (max(lu[k], lv[k]) == z) continue;
         if (lu[k] > z) { lower<SM, false>(L, u[k], z); wrote = true; }
         if (lu[k] != u[k] && zu[k] > z) { lower<SM, true>(L, lu[k], z); wrote = true; }
         if (lv[k] > z) {
@@ -679,6 +683,10 @@ __device__ __forceinline__ bool slice_rows(lab_t* L, lab_t* sl, lab_t base, lab_
     for (int k = 0; k < NE; ++k) {
         if (u[k] == v[k]) continue;
         const lab_t z = min(zu[k], zv[k]);
+        // z <= zu <= lu and z <= zv <= lv (every stored label is <= its
+        // cell's index), so nothing is lowered iff max(lu, lv) == z: one
+        // test on the common path of a converging sweep
+        if (max(lu[k], lv[k]) == z) continue;
         if (lu[k] > z) { lower<SM, false>(L, u[k], z); wrote = true; }
         if (lu[k] != u[k] && zu[k] > z) { lower<SM, true>(L, lu[k], z); wrote = true; }
         if (lv[k] > z) {
