@@ -86,7 +86,7 @@ int cc_create(int device, void* stream, cc_ctx** out) {
     CUDA_TRY(cudaMalloc(&c->dflags, sizeof(int) * kNumFlags));
     CUDA_TRY(cudaMemset(c->dflags, 0, sizeof(int) * kNumFlags));
     CUDA_TRY(cudaMalloc(&c->dcount, sizeof(unsigned long long)));
-    CUDA_TRY(cudaHostAlloc(&c->hflags, sizeof(int) * kNumFlags, cudaHostAllocDefault));
+    CUDA_TRY(cudaHostAlloc(&c->hflags, sizeof(int) * kNumFlags, cudaHostAllocMapped));
     CUDA_TRY(cudaHostAlloc(&c->hcount, sizeof(unsigned long long), cudaHostAllocDefault));
     CUDA_TRY(cudaEventCreate(&c->ev0));
     CUDA_TRY(cudaEventCreate(&c->ev1));
