@@ -535,6 +535,34 @@ def run_multi(args, rank, world, device):
 
     ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
     clk = clocks.stop() if clocks else None
+
+    # ---- roofline of the per-rank sweep kernel: one order-2 sweep of this
+    # rank's shard on the converged replica (no lowerings, so no peer
+    # traffic), CUDA events on the launching stream, max over ranks
+    from paper_2311_02811_b200 import _lib
+    sctx = runner.shard.ctx
+    fused_now = isinstance(runner, distributed.FusedShardedContour)
+    sweep_ts = []
+    for _ in range(3):
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
+        _lib.check(sctx.lib.cc_sweep(sctx.handle, 2, 0, int(bool(args.atomic)), 0, None))
+        s1.record(stream)
+        torch.cuda.synchronize()
+        sweep_ts.append(s0.elapsed_time(s1) / 1e3)
+    t_sw = max_over_ranks(sum(sweep_ts) / len(sweep_ts))
+    m_g = max(hi_ - lo_ for lo_, hi_ in (distributed.shard_rows(m_total, r, world)
+                                          for r in range(world)))
+    b_sw = 8 * m_g + 4 * n
+    peak, peak_src = peak_hbm()
+    roofline = {"bound": "hbm", "achieved": b_sw / t_sw / 1e9, "peak": peak, "unit": "GB/s",
+                "frac": b_sw / t_sw / 1e9 / peak, "traffic": None,
+                "kernel": ("cck::k_sweep_o2_peers (fused sweep + peer red.min)" if fused_now
+                           else "cck::k_sweep<2, 3, 1, 1>") + ", one rank's shard",
+                "bytes_per_launch": b_sw, "avg_launch_s": t_sw,
+                "note": "per GPU: 8 B x the largest shard's rows + 4 B x n, over the slowest "
+                        "rank's confirming-sweep time",
+                "peak_source": peak_src}
     # certificate over all shards: every rank checks its edges on its replica
     bad = max_over_ranks(engine.verify_staged(runner.shard.ctx))
 
@@ -597,6 +625,7 @@ def run_multi(args, rank, world, device):
                        "l2": "inputs larger than L2"},
             "exchanges_per_run": rounds,
             "verified": int(bad) == 0,
+            "roofline": roofline,
             "e2e": e2e,
             "gpu_launches": launches,
             "clocks": clk,
