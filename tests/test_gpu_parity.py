@@ -412,6 +412,31 @@ def test_hybrid_layout_exact(pipe):
     ctx.close()
 
 
+@pytest.mark.parametrize("transpose", [0, 1])
+def test_warp_transposed_layouts_exact(transpose):
+    """Sorted layouts with and without the warp-block transposition (and so
+    the hybrid copy compact or not by pipe): labels exact, certificate clean,
+    on chunk sizes that are and are not multiples of 128 rows."""
+    for chunk in (1 << 14, 50000):
+        ctx = _lib.Context(0)
+        ctx.set_option(_lib.CC_OPT_WARP_TRANSPOSE, transpose)
+        ctx.set_option(_lib.CC_OPT_SORT_CHUNK, chunk)
+        ctx.set_option(_lib.CC_OPT_BUCKET_SHIFT, 12)
+        ctx.set_option(_lib.CC_OPT_ITEM_ROWS, 5000)
+        for n, e in (graphgen.rmat(14, 16, 3), graphgen.grid(150, 170, 0.55, 2)):
+            exp = oracle.rem_union_find(n, e)
+            for layout in ("chunk_sorted", "src_sorted", "dst_bucketed", "hybrid"):
+                engine.stage_graph(ctx, n, e, layout)
+                for early in (False, True):
+                    labels = np.empty(n, dtype=np.int64)
+                    _, st = engine.run_staged(ctx, make_schedule("c2"), count_changes=False,
+                                              early_check=early, labels_out=labels)
+                    assert np.array_equal(labels, exp), (chunk, n, layout, early)
+                    check_invariants(labels, st)
+                    assert engine.verify_staged(ctx) == 0
+        ctx.close()
+
+
 def test_random_graphs_every_layout_and_loop():
     """Seeded fuzz: random multigraphs (self loops, duplicates, isolated
     vertices, ragged sizes) through every layout, both loops, check on/off,
