@@ -160,9 +160,11 @@ int cc_reorder_edges(cc_ctx* ctx, int mode);
                                       gathers, 8 4 rows + evict-last dst gathers, 9 4 rows +
                                       evict-first edge stream, 10 = 9 + evict-last src and dst
                                       gathers, 11 = 9 + evict-last dst gathers, 12 auto: on
-                                      layout 4 13 if m < 4n else 11, elsewhere 1 (default 12),
+                                      layout 4 13 if m < 4n else 18, elsewhere 1 (default 12),
                                       13 = 11 with 16 rows/thread, 14 = 13 capped at 128 regs
-                                      (2 blocks/SM), 15 = 11 with 8 rows/thread, 3 blocks/SM */
+                                      (2 blocks/SM), 15 = 11 with 8 rows/thread, 3 blocks/SM,
+                                      16 L1-bypassing dst gathers, 17 = 16 + evict-first edges,
+                                      18 = 11 + evict-first src gathers */
 #define CC_OPT_BUCKET_PIPE 13      /* layout 3/5 sweep kernel: 0 general, 1 lean slice kernel,
                                       2 lean + edge prefetch (default), 3 bulk-copy (TMA)
                                       pipelined, 3-stage ring */
