@@ -672,9 +672,9 @@ int cc_set_option(cc_ctx* c, int option, int64_t value) {
             c->loop_key.m = -1;
             return CC_OK;
         case CC_OPT_ITEM_ORDER:
-            if (value < 0 || value > 2)
-                return fail(CC_EINVAL, "item order must be 0 (bucket-major), 1 (run-major) or "
-                                       "2 (run-major, staggered)");
+            if (value < 0 || value > 3)
+                return fail(CC_EINVAL, "item order must be 0 (bucket-major), 1 (run-major), "
+                                       "2 (run-major, staggered) or 3 (src-major)");
             c->item_order = (int)value;
             return CC_OK;
         case CC_OPT_TILE_SPLIT:
