@@ -227,11 +227,91 @@ def test_increasing_path_c1_sync_is_n_minus_1():
         assert st.sweeps_until_stable == n - 1
 
 
+def _acceptance_suite():
+    """Graph families and sizes of the reference's acceptance suite
+    (test_acceptance.py:40-64), built here with seeded numpy: paths, cycles,
+    stars, full grids, random forests, Erdos-Renyi from sub- to
+    super-critical density.  IDs in generation order, as the reference's."""
+    import math
+    rng = np.random.default_rng(20261020)
+    out = []
+
+    def add(name, n, pairs):
+        out.append((name, n, np.asarray(pairs, dtype=np.int64).reshape(-1, 2)))
+
+    for n in (1, 2, 3, 4, 5, 8, 13, 21, 34, 64, 128, 333, 1000, 10_000):
+        add(f"path{n}", n, np.stack([np.arange(n - 1), np.arange(1, n)], 1))
+    for n in (3, 4, 5, 6, 10, 17, 50, 128, 999, 10_000):
+        add(f"cycle{n}", n, np.stack([np.arange(n), (np.arange(n) + 1) % n], 1))
+    for n in (2, 3, 4, 9, 33, 100, 1001, 10_000):
+        add(f"star{n}", n, np.stack([np.zeros(n - 1, np.int64), np.arange(1, n)], 1))
+    for r, c in ((1, 1), (1, 5), (2, 2), (3, 3), (4, 5), (7, 6), (10, 10), (25, 40), (100, 100)):
+        v = np.arange(r * c).reshape(r, c)
+        e = np.concatenate([np.stack([v[:, :-1].ravel(), v[:, 1:].ravel()], 1),
+                            np.stack([v[:-1, :].ravel(), v[1:, :].ravel()], 1)])
+        add(f"grid{r}x{c}", r * c, e)
+    for n in (10, 50, 200, 1000, 10_000):
+        for trees in (1, 3, 8):
+            for _ in range(2):
+                roots = rng.choice(n, size=trees, replace=False)
+                rest = np.setdiff1d(np.arange(n), roots)
+                rng.shuffle(rest)
+                order = np.concatenate([roots, rest])
+                par = [(order[i], order[rng.integers(0, i)]) for i in range(trees, n)]
+                add(f"forest{n}t{trees}", n, par)
+    for n in (10, 100, 1000, 2000):
+        for p in (0.5 / n, 1.0 / n, 2.0 / n, math.log(n) / n, 2.0 * math.log(n) / n):
+            for _ in range(70 if n <= 100 else 25):
+                iu = np.triu_indices(n, 1)
+                keep = rng.random(iu[0].size) < min(p, 1.0)
+                add(f"er{n}p{p:.4f}", n, np.stack([iu[0][keep], iu[1][keep]], 1))
+    return out
+
+
+def test_acceptance_matrix_c1_c4_c6():
+    """Acceptance C1 (labels == rem_union_find), C4 (sync sweeps C-m <= C-2 <=
+    C-1) and C6 (every converged run passes the early check and is one star
+    per component) over the reference suite's graph families, every variant x
+    {sync, async} x {atomic, plain}, on the device path
+    (test_acceptance.py:122-129, 169-180, 208-215)."""
+    ctx = _lib.Context(0)
+    bad, order_bad, runs = [], [], 0
+    for name, n, e in _acceptance_suite():
+        exp = oracle.rem_union_find(n, e)
+        comps = int(np.count_nonzero(exp == np.arange(n)))
+        engine.stage_graph(ctx, n, e, "auto")
+        sweeps = {}
+        for variant, sync in ALL_MODES:
+            for atomic in (True, False):
+                labels = np.empty(n, dtype=np.int64)
+                _, st = engine.run_staged(ctx, make_schedule(variant, 1024, sync=sync,
+                                                             atomic=atomic),
+                                          count_changes=sync, early_check=True,
+                                          labels_out=labels)
+                runs += 1
+                if not np.array_equal(labels, exp):
+                    bad.append((name, variant, sync, atomic, "labels"))
+                    continue
+                d = engine.forest_diagnostics(labels)
+                if not engine.early_convergence_check((n, e), labels) or \
+                        d.roots.size != comps or any(h > 1 for h in d.heights.values()):
+                    bad.append((name, variant, sync, atomic, "structure"))
+                if sync and atomic:
+                    sweeps[variant] = st.sweeps_until_stable
+        if not (sweeps["C-m"] <= sweeps["C-2"] <= sweeps["C-1"]):
+            order_bad.append((name, sweeps))
+    ctx.close()
+    assert runs == 1021 * 2 * len(ALL_MODES)  # the reference suite's 1,021 graphs
+    assert not bad, bad[:10]
+    assert not order_bad, order_bad[:10]
+
+
 def test_race_tolerance_repeated_runs():
-    """Acceptance C5 analogue: racy async sweeps always give identical labels."""
+    """Acceptance C5 analogue: racy async sweeps always give identical labels
+    (20 runs, as test_acceptance.py:183-205 runs 20 seeds)."""
     n, e = graphgen.erdos_renyi(100_000, 400_000, 99)
     exp = oracle.rem_union_find(n, e)
-    for _ in range(10):
+    for _ in range(20):
         labels, _ = run_contour((n, e), make_schedule("c2", atomic=False))
         assert np.array_equal(labels, exp)
 
