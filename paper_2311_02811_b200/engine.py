@@ -137,7 +137,7 @@ def _unpack_graph(g):
 
 LAYOUTS = {"input": 0, "src_sorted": 1, "chunk_sorted": 2, "dst_bucketed": 3, "l2_tiled": 4,
            "hybrid": 5}
-AUTO_SORT_MIN_ROWS = 1 << 20
+AUTO_SORT_MIN_ROWS = 1 << 16
 
 
 AUTO_L2_LABEL_BYTES = 96 << 20  # the 126 MB L2 holds the labels plus the edge stream's lines
@@ -147,7 +147,8 @@ AUTO_HYBRID_MIN_DEGREE = 8  # rows per vertex from which the bucketed copy pays 
 
 
 def resolve_layout(layout: str, m: int, n: int = 0, resident: bool = True) -> str:
-    """"auto": input order below 2^20 rows; while the label array fits
+    """"auto": input order below 2^16 rows (ER n=65,536, 524,282 rows: 0.088 ms
+    per run chunk-sorted vs 0.11 ms in input order); while the label array fits
     comfortably in L2, chunk-sorted staging (it hides under the host->device
     copy, ~2x faster sweeps) -- plus, for graphs staged once and run from HBM
     (``resident``) with >= 8 rows per vertex and m < 2^31, the dst-bucketed

@@ -64,7 +64,8 @@ def test_auto_layout_policy():
     run from HBM (m >= 8n, m < 2^31), chunk_sorted otherwise and for one-shot
     host runs (sweep 1 streams behind the copy)."""
     from paper_2311_02811_b200.engine import resolve_layout
-    assert resolve_layout("auto", (1 << 20) - 1, 1000) == "input"
+    assert resolve_layout("auto", (1 << 16) - 1, 1000) == "input"
+    assert resolve_layout("auto", 524282, 65536) == "chunk_sorted"                 # ER config
     assert resolve_layout("auto", 134217728, 4194304) == "hybrid"               # RMAT-22
     assert resolve_layout("auto", 134217728, 4194304, resident=False) == "chunk_sorted"
     assert resolve_layout("auto", 18446634, 16777216) == "chunk_sorted"          # grid 4096^2
