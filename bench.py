@@ -53,9 +53,9 @@ def parse():
                    help="the reference's early convergence check after each changing sweep "
                         "(engine.py:318-320), inside the device loop.  auto: on for the hybrid "
                         "layout, whose shared-memory check (0.18 ms on RMAT-22) is cheaper "
-                        "than the confirming sweep it saves; off elsewhere, where the check "
-                        "costs what that sweep costs (RMAT-22 1.19 vs 1.15 ms, RMAT-28 158 vs "
-                        "122 ms, forest 842 vs 800 ms, measured)")
+                        "than the confirming sweep it saves, and for L2-window tiles (RMAT-28 "
+                        "78 vs 82 ms, forest 693 vs 701 ms); off on flat chunk-sorted rows, "
+                        "where the check costs what that sweep costs (RMAT-22 1.19 vs 1.15 ms)")
     p.add_argument("--seed", type=int, default=1)
     p.add_argument("--layout", default="auto",
                    choices=["auto", "input", "src_sorted", "chunk_sorted", "dst_bucketed",
@@ -308,7 +308,8 @@ def run_single(args, device):
     e2e_layout = engine.resolve_layout(layout_arg, m, n, resident=False)
 
     def early_for(layout):
-        return args.early_check == "on" or (args.early_check == "auto" and layout == "hybrid")
+        return args.early_check == "on" or (args.early_check == "auto" and
+                                            layout in ("hybrid", "l2_tiled"))
 
     args.early = early_for(args.layout)
     hybrid = args.layout == "hybrid"

@@ -27,7 +27,8 @@ def main():
         lay = engine.resolve_layout(layout, e.shape[0], n)
         engine.stage_graph(ctx, n, e, lay)
         del e
-    _, st = engine.run_staged(ctx, make_schedule("c2"), count_changes=False, early_check=False,
+    check = os.environ.get("CC_CHECK", "0") == "1"
+    _, st = engine.run_staged(ctx, make_schedule("c2"), count_changes=False, early_check=check,
                               host_loop=True)
     print(cfg, lay, st.sweeps_executed, [round(t * 1e3, 2) for t in st.sweep_seconds])
 
