@@ -175,6 +175,8 @@ int cc_reorder_edges(cc_ctx* ctx, int mode);
 #define CC_OPT_WARP_TRANSPOSE 15   /* sorted layouts: store each 128-row block transposed so a
                                       warp's k-th gather reads 32 consecutive sorted rows (default
                                       1; applied when the layout is built) */
+#define CC_OPT_SWEEP_CTAS 16       /* flat order-1/2/h sweeps: CTAs per SM (0 = auto, default:
+                                      3 on dense L2-window tiles, else the occupancy limit) */
 #define CC_OPT_STAGE_LAYOUT 4     /* layout applied while staging: 0 input order (default),
                                       2 chunk-sorted, each chunk sorted as soon as it lands,
                                       overlapped with the next chunk's host->device copy */

@@ -685,6 +685,11 @@ int cc_set_option(cc_ctx* c, int option, int64_t value) {
             if (value < 10 || value > 30) return fail(CC_EINVAL, "tile shift must be in [10, 30]");
             c->tile_shift = (int)value;
             return CC_OK;
+        case CC_OPT_SWEEP_CTAS:
+            if (value < 0 || value > 32) return fail(CC_EINVAL, "sweep CTAs per SM must be 0..32");
+            c->sweep_ctas = (int)value;
+            c->loop_key.m = -1;
+            return CC_OK;
         case CC_OPT_WARP_TRANSPOSE:
             c->warp_transpose = value != 0;
             return CC_OK;

@@ -40,9 +40,11 @@ def run(cfg, args):
     if args.store_mode >= 0:
         ctx.set_option(_lib.CC_OPT_STORE_MODE_ATOMIC, args.store_mode)
     ctx.set_option(_lib.CC_OPT_TILE_SHIFT, args.tshift)
+    ctx.set_option(_lib.CC_OPT_SWEEP_CTAS, args.sweep_ctas)
     rec = {"store_mode": args.store_mode, "first_scatter": args.first_scatter, "host_loop": args.host_loop,
            "shortcut": args.shortcut, "tsplit": args.tsplit, "tshift": args.tshift, "seed": args.seed, "early_check": args.early_check, "sort_chunk": args.sort_chunk, "bshift": args.bshift, "config": cfg, "variant": args.variant, "pipe": args.pipe,
-           "item_order": args.item_order, "item_rows": args.item_rows}
+           "item_order": args.item_order, "item_rows": args.item_rows,
+           "sweep_ctas": args.sweep_ctas}
     t0 = time.perf_counter()
     host = None
     if spec["kind"] == "rmat":
@@ -140,6 +142,7 @@ def main():
     ap.add_argument("--store-mode", type=int, default=-1)
     ap.add_argument("--host-loop", type=int, default=0)
     ap.add_argument("--tshift", type=int, default=24)
+    ap.add_argument("--sweep-ctas", type=int, default=0)
     ap.add_argument("--runs", type=int, default=0, help="bucketed run-major: runs (sets sort chunk)")
     args = ap.parse_args()
     for cfg in args.configs:
