@@ -26,6 +26,7 @@ def main():
     ap.add_argument("--nosmem", default="0", help="comma list: 1 = dst labels from global memory")
     ap.add_argument("--runs", default="1", help="comma list: input-order runs (item order 1/2)")
     ap.add_argument("--checks", default="0,1")
+    ap.add_argument("--bshifts", default="15")
     a = ap.parse_args()
     sched = make_schedule("c2")
     for scale in map(int, a.scales.split(",")):
@@ -34,12 +35,14 @@ def main():
             ctx = _lib.Context(0, stream)
             _, m = graphgen.rmat_device(ctx, scale, 16, seed)
             for layout in a.layouts.split(","):
-                for order, rows, nosmem, nruns in [
-                        (o, r, ns, ru) for o in map(int, a.orders.split(","))
+                for order, rows, nosmem, nruns, bsh in [
+                        (o, r, ns, ru, bs) for o in map(int, a.orders.split(","))
                         for r in map(int, a.item_rows.split(","))
                         for ns in map(int, a.nosmem.split(","))
-                        for ru in map(int, a.runs.split(","))]:
+                        for ru in map(int, a.runs.split(","))
+                        for bs in map(int, a.bshifts.split(","))]:
                     if True:
+                        ctx.set_option(_lib.CC_OPT_BUCKET_SHIFT, bsh)
                         ctx.set_option(_lib.CC_OPT_SORT_CHUNK, -(-m // nruns) if nruns > 1 else 1 << 23)
                         ctx.set_option(_lib.CC_OPT_BUCKET_NOSMEM, nosmem)
                         ctx.set_option(_lib.CC_OPT_ITEM_ORDER, order)
@@ -55,7 +58,7 @@ def main():
                             best = min(runs, key=lambda s: s.device_seconds)
                             ok = engine.verify_staged(ctx) == 0
                             print(f"scale={scale} seed={seed} {layout} order={order} "
-                                  f"item_rows={rows} nosmem={nosmem} runs={nruns} check={int(check)} "
+                                  f"item_rows={rows} nosmem={nosmem} runs={nruns} bshift={bsh} check={int(check)} "
                                   f"ms={best.device_seconds * 1e3:.3f} "
                                   f"sweeps={[s.sweeps_executed for s in runs]} "
                                   f"sweep_ms={[round(t * 1e3, 3) for t in best.sweep_seconds]} "
