@@ -343,6 +343,39 @@ def test_store_modes_layouts_and_first_scatter_are_exact():
     ctx.close()
 
 
+def test_sweep_ctas_and_item_orders_exact():
+    """CTAs per SM of the flat sweep (auto, 1, 3) and every bucketed item
+    order (incl. src-major 3) give exact labels; out-of-range values raise."""
+    n, e = graphgen.rmat(14, 16, 8)
+    exp = oracle.rem_union_find(n, e)
+    ctx = _lib.Context(0)
+    for ctas in (0, 1, 3):
+        ctx.set_option(_lib.CC_OPT_SWEEP_CTAS, ctas)
+        for layout in ("chunk_sorted", "l2_tiled"):
+            ctx.set_option(_lib.CC_OPT_TILE_SHIFT, 12)
+            engine.stage_graph(ctx, n, e, layout)
+            for early in (False, True):
+                labels = np.empty(n, dtype=np.int64)
+                _, st = engine.run_staged(ctx, make_schedule("c2"), count_changes=False,
+                                          early_check=early, labels_out=labels)
+                assert np.array_equal(labels, exp), (ctas, layout, early)
+                check_invariants(labels, st)
+    ctx.set_option(_lib.CC_OPT_SWEEP_CTAS, 0)
+    ctx.set_option(_lib.CC_OPT_BUCKET_SHIFT, 11)
+    ctx.set_option(_lib.CC_OPT_ITEM_ROWS, 4000)
+    for order in (0, 1, 2, 3):
+        ctx.set_option(_lib.CC_OPT_ITEM_ORDER, order)
+        engine.stage_graph(ctx, n, e, "dst_bucketed")
+        labels = np.empty(n, dtype=np.int64)
+        engine.run_staged(ctx, make_schedule("c2"), labels_out=labels)
+        assert np.array_equal(labels, exp), order
+    for opt, val in ((_lib.CC_OPT_SWEEP_CTAS, -1), (_lib.CC_OPT_SWEEP_CTAS, 33),
+                     (_lib.CC_OPT_ITEM_ORDER, 4)):
+        with pytest.raises(ValueError):
+            ctx.set_option(opt, val)
+    ctx.close()
+
+
 def test_sync_first_scatter_keeps_reference_stats(golden):
     """The load-free sweep 1 is exactly the reference's sync sweep 1."""
     for g in golden["graphs"][:80]:
