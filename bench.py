@@ -324,7 +324,12 @@ def run_single(args, device):
     # ---- timed region: K whole runs, CUDA events on the launching stream
     clocks = ClockSampler(device)
     clocks.start()
-    time.sleep(0.3)
+    # keep the GPU busy with untimed runs while the sampler warms up, so the
+    # sampled clocks are clocks under this load (the timed region itself is
+    # a few ms)
+    t_busy = time.perf_counter()
+    while time.perf_counter() - t_busy < 0.3:
+        engine.run_staged(ctx, sched, sweep_times=False, **kw)
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
@@ -516,7 +521,8 @@ def run_multi(args, rank, world, device):
     clocks = ClockSampler(device) if rank == 0 else None
     if clocks:
         clocks.start()
-        time.sleep(0.3)
+    for _ in range(16):  # untimed runs under the sampler; a fixed count (collectives inside)
+        runner.run()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     dist.barrier()
     torch.cuda.synchronize()
