@@ -554,10 +554,11 @@ def test_random_graphs_every_layout_and_loop():
     """Seeded fuzz: random multigraphs (self loops, duplicates, isolated
     vertices, ragged sizes) through every layout, both loops, check on/off,
     small buckets / items / chunks so every kernel path sees many items."""
-    rng = np.random.default_rng(20261020)
+    import os
+    rng = np.random.default_rng(int(os.environ.get("CC_FUZZ_SEED", "20261020")))
     ctx = _lib.Context(0)
     layouts = ("input", "src_sorted", "chunk_sorted", "dst_bucketed", "l2_tiled", "hybrid")
-    for t in range(120):
+    for t in range(int(os.environ.get("CC_FUZZ_ITERS", "120"))):
         n = int(rng.integers(1, 6000))
         m = int(rng.integers(0, 25000))
         e = rng.integers(0, n, size=(m, 2), dtype=np.int64)
@@ -569,9 +570,12 @@ def test_random_graphs_every_layout_and_loop():
         layout = layouts[t % len(layouts)]
         ctx.set_option(_lib.CC_OPT_BUCKET_SHIFT, int(rng.integers(8, 12)))
         ctx.set_option(_lib.CC_OPT_ITEM_ROWS, int(rng.integers(1024, 5000)))
-        ctx.set_option(_lib.CC_OPT_SORT_CHUNK, int(rng.integers(1, 9000)))
+        chunk = int(rng.integers(1, 9000))
+        ctx.set_option(_lib.CC_OPT_SORT_CHUNK, chunk if t % 2 else 128 * (chunk // 128 + 1))
         ctx.set_option(_lib.CC_OPT_TILE_SHIFT, 10)
-        ctx.set_option(_lib.CC_OPT_ITEM_ORDER, int(t % 3))
+        ctx.set_option(_lib.CC_OPT_ITEM_ORDER, int(t % 4))
+        ctx.set_option(_lib.CC_OPT_WARP_TRANSPOSE, int(rng.integers(0, 4) > 0))
+        ctx.set_option(_lib.CC_OPT_SWEEP_CTAS, int(rng.integers(0, 4)))
         ctx.set_option(_lib.CC_OPT_BUCKET_PIPE, int(rng.integers(0, 4)))
         engine.stage_graph(ctx, n, e, layout)
         for variant in ("C-2", "C-1", "C-m"):
