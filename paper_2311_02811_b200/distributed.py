@@ -341,3 +341,80 @@ class ShardedContour(_HostIO):
                 break
         self.shard.compress()
         return rounds
+
+
+def run_in_process(n: int, edges, schedule, devices, cadence: int = 1, layout: str = "auto",
+                   cap=None):
+    """``run_contour(..., devices=[...])``: the edge-sharded driver inside one
+    process -- one host thread per listed device (a device may repeat: two
+    shards on one GPU), each with its own context, stream and label replica;
+    the MIN exchange is a host barrier + element-wise minimum of the replicas
+    (gathered to the first device, copied back).  Asynchronous schedules only
+    (a sweep of a shard is an asynchronous sweep of the whole edge list once
+    the replicas are merged).  Returns (int64 labels, sweeps executed,
+    exchange rounds)."""
+    import threading
+
+    import numpy as np
+    import torch
+
+    from .engine import _host_edges, stage_graph
+
+    if schedule.sync:
+        raise ValueError("multi-device runs need an asynchronous schedule (sync=False)")
+    devices = [int(d) for d in devices]
+    world = len(devices)
+    e = edges if (hasattr(edges, "data_ptr") and getattr(edges, "is_cuda", False)) \
+        else _host_edges(edges)
+    m = int(e.shape[0])
+    slots = [None] * world
+    barrier = threading.Barrier(world)
+    out, errors, counts = {}, [], {}
+    dev0 = torch.device("cuda", devices[0])
+
+    def allreduce_for(r):
+        def reduce(t):
+            torch.cuda.synchronize(t.device)
+            slots[r] = t
+            barrier.wait()
+            if r == 0:
+                mn = slots[0].clone()
+                for x in slots[1:]:
+                    torch.minimum(mn, x.to(dev0), out=mn)
+                for x in slots:
+                    x.copy_(mn.to(x.device))
+                for x in slots:
+                    torch.cuda.synchronize(x.device)
+            barrier.wait()
+        return reduce
+
+    def work(r):
+        try:
+            dev = devices[r]
+            torch.cuda.set_device(dev)
+            ctx = _lib.Context(dev)
+            lo, hi = shard_rows(m, r, world)
+            stage_graph(ctx, n, e[lo:hi], layout)
+            shard = CudaShard(ctx, n, atomic=schedule.atomic)
+            runner = ShardedContour(shard, n, m, order_for=schedule.order_for, cadence=cadence,
+                                    allreduce=allreduce_for(r), cap=cap)
+            rounds = runner.run()
+            torch.cuda.synchronize(dev)
+            counts[r] = rounds
+            if r == 0:
+                out[0] = shard.labels[:n].cpu().numpy().astype(np.int64)
+            ctx.close()
+        except Exception as exc:  # surfaced below; release the other threads
+            errors.append(exc)
+            barrier.abort()
+
+    threads = [threading.Thread(target=work, args=(r,)) for r in range(world)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    if errors:  # the first real failure, not the barrier breaks it caused
+        real = [x for x in errors if not isinstance(x, threading.BrokenBarrierError)]
+        raise (real or errors)[0]
+    rounds = counts[0]
+    return out[0], rounds * max(1, int(cadence)), rounds

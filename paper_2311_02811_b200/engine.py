@@ -325,7 +325,8 @@ def run_contour(g, schedule: Schedule, threads: int = 1, seed: Optional[int] = N
                 device: int = 0, count_changes: bool = True, early_check: bool = True,
                 sweep_times: bool = True, layout: str = "auto",
                 first_scatter: bool = False,
-                host_loop: bool = False) -> tuple[LabelArray, IterationStats]:
+                host_loop: bool = False, devices=None,
+                cadence: int = 1) -> tuple[LabelArray, IterationStats]:
     """Run minimum-mapping sweeps to convergence on the GPU (engine.py:248-328).
 
     ``g`` is anything with ``.n`` and ``.edges`` ((m, 2) int32/int64 pairs,
@@ -334,12 +335,32 @@ def run_contour(g, schedule: Schedule, threads: int = 1, seed: Optional[int] = N
     semantics (every sweep already runs on all SMs).  Returns int64 labels
     (every entry the minimum vertex ID of its component) and IterationStats.
     Raises IterationCapExceeded after n+2 sweeps, ValueError on bad input.
+
+    ``devices`` (a list of CUDA device ordinals, more than one) shards the
+    edge rows over those GPUs inside this process -- label replicas merged by
+    an element-wise MIN every ``cadence`` local sweeps (distributed.py; one
+    process per GPU with torch.distributed is the multi-node-ready form).
+    Asynchronous schedules only; ``changed_per_sweep`` holds -1 for the
+    sweeps of changing rounds and 0 for the last round's (with ``cadence`` k
+    > 1 the last round has k no-write sweeps, so executed = until_stable + k).
     """
     if threads < 1:
         raise ValueError("threads must be >= 1")
     n, edges = _unpack_graph(g)
     if n < 0:
         raise ValueError("vertex count must be non-negative")
+    if devices is not None and len(devices) > 1:
+        from .distributed import run_in_process
+        labels, sweeps, rounds = run_in_process(n, edges, schedule, devices, cadence=cadence,
+                                                layout=layout)
+        k = max(1, int(cadence))
+        changed = [-1] * (rounds - 1) + [0]
+        return labels, IterationStats(
+            sweeps_executed=sweeps, sweeps_until_stable=max(0, sweeps - k),
+            changed_per_sweep=[c for c in changed for _ in range(k)],
+            converged_by="change-flag", sweep_seconds=[0.0] * sweeps, device_seconds=0.0)
+    if devices is not None and len(devices) == 1:
+        device = int(devices[0])
     ctx = _context(device)
     labels = np.empty(n, dtype=np.int64)
     if hasattr(edges, "data_ptr") and getattr(edges, "is_cuda", False):

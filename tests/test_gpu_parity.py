@@ -770,3 +770,22 @@ def test_staged_chunk_sort_from_host_matches_device_reorder():
     for layout in ("chunk_sorted", "src_sorted", "auto"):
         labels, st = run_contour((n, e), make_schedule("c2"), layout=layout)
         assert np.array_equal(labels, exp), layout
+
+
+@pytest.mark.parametrize("cadence", [1, 2])
+def test_run_contour_devices_in_process(cadence):
+    """run_contour(..., devices=[...]): the edge-sharded driver in one process
+    (shards as host threads; here all on cuda:0, which exercises the same
+    exchange logic as distinct GPUs) -- exact labels, async variants."""
+    for n, e in (graphgen.rmat(15, 16, 5), graphgen.grid(200, 230, 0.55, 3),
+                 graphgen.forest(60, 2), (5, np.zeros((0, 2), np.int64))):
+        exp = oracle.rem_union_find(n, e)
+        for devs in ([0, 0], [0, 0, 0]):
+            for variant in ("C-2", "C-1", "C-m"):
+                labels, st = run_contour((n, e), make_schedule(variant, 6), devices=devs,
+                                         cadence=cadence)
+                assert np.array_equal(labels, exp), (n, devs, variant)
+                assert st.sweeps_executed == st.sweeps_until_stable + cadence
+                assert st.changed_per_sweep[-1] == 0
+    with pytest.raises(ValueError):
+        run_contour((n, e), make_schedule("c2", sync=True), devices=[0, 0])
