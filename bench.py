@@ -439,6 +439,24 @@ def run_single(args, device):
                          f"async atomic={bool(args.atomic)}, {threads} threads): {t_cpu:.2f} s, "
                          f"sweeps_executed={st_cpu.sweeps_executed}"}
         ref_sweeps = {"executed": st_cpu.sweeps_executed, "until_stable": st_cpu.sweeps_until_stable}
+        # the reference's 1-thread time and its synchronous C-2
+        # counts (deterministic: the device's sync run must match them)
+        from oracle import oracle
+        t1 = time.perf_counter()
+        _, st1 = oracle.run_contour(n, host_edges, "C-2", atomic=bool(args.atomic), threads=1,
+                                    seed=0)
+        t1 = time.perf_counter() - t1
+        cpu["threads_1"] = {"value": m / t1, "seconds": t1, "sweeps_executed": st1.sweeps_executed}
+        _, sts = oracle.run_contour(n, host_edges, "C-2", sync=True, threads=threads, seed=0)
+        ref_sweeps["sync_c2"] = {"executed": sts.sweeps_executed,
+                                 "until_stable": sts.sweeps_until_stable,
+                                 "changed_per_sweep": list(sts.changed_per_sweep)}
+        _, stg = engine.run_staged(ctx, make_schedule("c2", sync=True), count_changes=True,
+                                   early_check=True, sweep_times=False)
+        ref_sweeps["sync_c2_device"] = {"executed": stg.sweeps_executed,
+                                        "until_stable": stg.sweeps_until_stable,
+                                        "changed_per_sweep": stg.changed_per_sweep,
+                                        "equal": stg.changed_per_sweep == list(sts.changed_per_sweep)}
     else:
         ref_sweeps = None
 
