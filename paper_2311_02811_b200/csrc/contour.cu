@@ -13,6 +13,9 @@
 #include <string.h>
 
 #include <algorithm>
+#include <condition_variable>
+#include <functional>
+#include <memory>
 #include <mutex>
 #include <thread>
 #include <vector>
@@ -50,6 +53,8 @@ static int fail(int code, const char* fmt, ...) {
     } while (0)
 
 #include "device_aux.inc"
+
+#include "hostpool.inc"
 
 #include "ctx.inc"
 
@@ -112,6 +117,8 @@ void cc_destroy(cc_ctx* c) {
     cudaFree(c->bsrc);
     cudaFree(c->bdst);
     cudaFree(c->bdst16);
+    for (int b = 0; b < 2; ++b) cudaFreeHost(c->hstage[b]);
+    cudaFreeHost(c->hlab);
     if (c->own_labels) cudaFree(c->labels);
     cudaFree(c->wide);
     cudaFree(c->shadow);
@@ -476,7 +483,11 @@ int cc_run_host(cc_ctx* c, const void* edges_host, int elem_bytes, int64_t m, in
     const bool spec_valid = rounds == 0 && (k == 1 || (k == 2 && by == 0));
     if (labels_out && c->n > 0) {
         CUDA_TRY(cudaEventSynchronize(c->spec_done));  // before the buffer is reused
-        if (spec_valid) labels_out = nullptr;
+        if (spec_valid) {
+            if (c->pend_out) finish_pageable(c, c->pend_out, c->pend_eb);  // pinned -> caller
+            c->pend_out = nullptr;
+            labels_out = nullptr;
+        }
     }
     if (st) {
         st->sweeps_executed = k;

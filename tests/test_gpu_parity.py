@@ -789,3 +789,44 @@ def test_run_contour_devices_in_process(cadence):
                 assert st.changed_per_sweep[-1] == 0
     with pytest.raises(ValueError):
         run_contour((n, e), make_schedule("c2", sync=True), devices=[0, 0])
+
+
+def test_pinned_and_pageable_host_buffers():
+    """Host edges and labels in pinned (cudaHostAlloc, via torch) and pageable
+    (numpy) memory, int32 and int64: the copy engine reads pinned buffers
+    directly, pageable ones go through the context's narrowing threads and
+    pinned staging -- same labels, same range errors, both read-back paths
+    (speculative after sweep 1, and after later sweeps)."""
+    import torch
+    for n, e in (graphgen.rmat(16, 16, 2), graphgen.grid(300, 280, 0.55, 4),
+                 graphgen.forest(80, 3)):
+        exp = oracle.rem_union_find(n, e)
+        for dt in (np.int32, np.int64):
+            pageable = np.ascontiguousarray(e, dtype=dt)
+            pinned_t = torch.empty(e.shape, dtype=torch.int32 if dt == np.int32 else torch.int64,
+                                   pin_memory=True)
+            pinned_t.numpy()[:] = pageable
+            for src in (pageable, pinned_t.numpy()):
+                for out_pinned in (False, True):
+                    if out_pinned:
+                        lt = torch.empty(n, dtype=torch.int64, pin_memory=True)
+                        labels = lt.numpy()
+                    else:
+                        labels = np.empty(n, dtype=np.int64)
+                    ctx = engine._context(0)
+                    for early in (False, True):
+                        _, st = engine.run_host(ctx, n, src, make_schedule("c2"),
+                                                count_changes=False, early_check=early,
+                                                labels_out=labels)
+                        assert np.array_equal(labels, exp), (n, dt, early, out_pinned)
+                    got, _ = run_contour((n, src), make_schedule("c2"))
+                    assert np.array_equal(got, exp)
+                    l32 = np.empty(n, dtype=np.int32)
+                    engine.run_host(ctx, n, src, make_schedule("c1"), count_changes=False,
+                                    labels_out=l32)
+                    assert np.array_equal(l32, exp)
+    bad = np.array([[0, 1], [2, 5]], dtype=np.int64)
+    for arr in (bad, np.array([[0, -1]], dtype=np.int64), np.array([[0, 1 << 33]], np.int64),
+                np.array([[0, -3]], dtype=np.int32)):
+        with pytest.raises(ValueError):
+            run_contour((4, arr), make_schedule("c2"))
