@@ -303,9 +303,27 @@ int cc_write_labels(cc_ctx* c, const void* in, int eb) {
         CUDA_TRY(cudaMalloc((void**)&c->wide, sizeof(int64_t) * c->n));
         c->wide_cap = c->n;
     }
-    CUDA_TRY(cudaMemcpyAsync(c->wide, in, (size_t)eb * c->n, cudaMemcpyHostToDevice, c->stream));
+    const bool pageable = !host_pinned(in);
+    if (pageable) {  // narrowed by the context's threads into pinned memory (hostpool.inc)
+        CC_TRY(ensure_hlab(c));
+        uint32_t* h = c->hlab;
+        ensure_pool(c)->run(c->n, [&](int64_t lo, int64_t hi) {
+            for (int64_t i = lo; i < hi; ++i) {
+                const int64_t x = eb == 8 ? ((const int64_t*)in)[i] : ((const int32_t*)in)[i];
+                h[i] = (x < 0 || x > 0xFFFFFFFFll) ? 0xFFFFFFFFu : (uint32_t)x;
+            }
+        });
+        CUDA_TRY(cudaMemcpyAsync(c->wide, h, sizeof(uint32_t) * c->n, cudaMemcpyHostToDevice,
+                                 c->stream));
+    } else {
+        CUDA_TRY(cudaMemcpyAsync(c->wide, in, (size_t)eb * c->n, cudaMemcpyHostToDevice,
+                                 c->stream));
+    }
     CUDA_TRY(cudaMemsetAsync(c->dflags + kFlagBad, 0, sizeof(int), c->stream));
-    if (eb == 8)
+    if (pageable)
+        k_labels_in<uint32_t><<<grid_for(c, c->n), kThreads, 0, c->stream>>>(
+            (const uint32_t*)c->wide, c->n, c->labels, c->dflags);
+    else if (eb == 8)
         k_labels_in<int64_t><<<grid_for(c, c->n), kThreads, 0, c->stream>>>(
             (const int64_t*)c->wide, c->n, c->labels, c->dflags);
     else
