@@ -303,7 +303,7 @@ int cc_write_labels(cc_ctx* c, const void* in, int eb) {
         CUDA_TRY(cudaMalloc((void**)&c->wide, sizeof(int64_t) * c->n));
         c->wide_cap = c->n;
     }
-    const bool pageable = !host_pinned(in);
+    const bool pageable = host_pageable(in);
     if (pageable) {  // narrowed by the context's threads into pinned memory (hostpool.inc)
         CC_TRY(ensure_hlab(c));
         uint32_t* h = c->hlab;
