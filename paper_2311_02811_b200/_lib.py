@@ -157,6 +157,7 @@ class Context:
         check(self.lib.cc_create(device, ctypes.c_void_p(stream or 0), ctypes.byref(h)),
               "cc_create")
         self.handle = h
+        self.staged = None  # run_contour's resident-graph key (engine._resident)
         self.n = 0
         self.m = 0
 

@@ -199,6 +199,7 @@ def stage_graph(ctx: _lib.Context, n: int, edges, layout: str = "auto") -> None:
     "input" keeps the caller's order, "chunk_sorted" radix-sorts every 2^23-row
     chunk by src as it lands (overlapped with the next chunk's copy),
     "src_sorted" sorts all rows by src afterwards, "auto" picks."""
+    ctx.staged = None  # the context's edges change: no resident graph to reuse
     m_rows = int(edges.shape[0]) if hasattr(edges, "shape") and len(edges.shape) == 2 \
         else len(edges)
     layout = resolve_layout(layout, m_rows, n)
@@ -282,6 +283,7 @@ def run_host(ctx: _lib.Context, n: int, edges, schedule: Schedule, *, layout: st
     behind the host-to-device copy, so the transfer hides it; every other
     case stages, then runs, exactly as stage_graph + run_staged.  Returns
     (labels_out, IterationStats)."""
+    ctx.staged = None
     e = _host_edges(edges)
     m = e.shape[0]
     layout = resolve_layout(layout, m, n, resident=False)
@@ -363,6 +365,21 @@ def run_contour(g, schedule: Schedule, threads: int = 1, seed: Optional[int] = N
         device = int(devices[0])
     ctx = _context(device)
     labels = np.empty(n, dtype=np.int64)
+    # A read-only edge array (the reference's Graph freezes its arrays,
+    # graph.py:82-83) cannot change between calls: the graph staged by the
+    # previous call on this context stays resident and is reused -- as the
+    # device layout for resident graphs (resolve_layout(resident=True)).
+    frozen = isinstance(edges, np.ndarray) and not edges.flags.writeable
+    if frozen and ctx.staged is not None and ctx.staged[0] is edges and \
+            ctx.staged[1:3] == (n, layout):
+        if ctx.staged[3]:  # upgrade the streamed layout once (+ the hybrid's bucketed copy)
+            _lib.check(ctx.lib.cc_reorder_edges(ctx.handle, LAYOUTS[ctx.staged[3]]))
+            ctx.staged = ctx.staged[:3] + (None,)
+        _, stats = run_staged(ctx, schedule, count_changes=count_changes,
+                              early_check=early_check, sweep_times=sweep_times,
+                              labels_out=labels, first_scatter=first_scatter,
+                              host_loop=host_loop)
+        return labels, stats
     if hasattr(edges, "data_ptr") and getattr(edges, "is_cuda", False):
         stage_graph(ctx, n, edges, layout)
         _, stats = run_staged(ctx, schedule, count_changes=count_changes,
@@ -373,6 +390,15 @@ def run_contour(g, schedule: Schedule, threads: int = 1, seed: Optional[int] = N
         _, stats = run_host(ctx, n, edges, schedule, layout=layout, count_changes=count_changes,
                             early_check=early_check, sweep_times=sweep_times, labels_out=labels,
                             first_scatter=first_scatter, host_loop=host_loop)
+        if frozen:
+            m = int(edges.shape[0])
+            staged = resolve_layout(layout, m, n, resident=False)
+            want = resolve_layout(layout, m, n, resident=True)
+            upgrade = None
+            if want != staged:
+                # only layouts reachable from the staged order in place
+                upgrade = want if (staged, want) in (("chunk_sorted", "hybrid"),) else None
+            ctx.staged = (edges, n, layout, upgrade)
     return labels, stats
 
 

@@ -830,3 +830,35 @@ def test_pinned_and_pageable_host_buffers():
                 np.array([[0, -3]], dtype=np.int32)):
         with pytest.raises(ValueError):
             run_contour((4, arr), make_schedule("c2"))
+
+
+def test_frozen_edges_stay_resident():
+    """run_contour on a read-only edge array (the reference's Graph freezes
+    its arrays) reuses the graph staged by the previous call on the context,
+    upgraded to the resident layout; any other staging on the context, a
+    different array object or a writeable array restages."""
+    from paper_2311_02811_b200 import early_convergence_check
+    n, e = graphgen.rmat(16, 16, 6)
+    e = np.ascontiguousarray(e)
+    exp = oracle.rem_union_find(n, e)
+    e.flags.writeable = False
+    ctx = engine._context(0)
+    for i in range(4):
+        labels, st = run_contour((n, e), make_schedule("c2"))
+        assert np.array_equal(labels, exp), i
+        check_invariants(labels, st)
+        assert ctx.staged is not None and ctx.staged[0] is e
+    labels, st = run_contour((n, e), make_schedule("c2", sync=True))  # any schedule
+    assert np.array_equal(labels, exp)
+    n2, e2 = graphgen.grid(120, 130, 0.55, 1)
+    e2 = np.ascontiguousarray(e2)
+    e2.flags.writeable = False
+    assert np.array_equal(run_contour((n2, e2), make_schedule("c2"))[0],
+                          oracle.rem_union_find(n2, e2))
+    assert ctx.staged[0] is e2
+    assert early_convergence_check((n2, e2), oracle.rem_union_find(n2, e2))
+    assert ctx.staged is None  # the check staged its own copy
+    assert np.array_equal(run_contour((n, e), make_schedule("c2"))[0], exp)
+    w = np.array(e)  # writeable copy: never cached
+    assert np.array_equal(run_contour((n, w), make_schedule("cm"))[0], exp)
+    assert ctx.staged is None

@@ -21,7 +21,10 @@ def main():
                       ("count_changes=False, early_check=True", dict(count_changes=False)),
                       ("count_changes=False, early_check=False",
                        dict(count_changes=False, early_check=False))):
-        for src, arr in (("pinned", pe.numpy()), ("pageable int64", e.astype(np.int64))):
+        frozen = e.astype(np.int64)
+        frozen.flags.writeable = False  # as the reference's Graph.edges (graph.py:82-83)
+        for src, arr in (("pinned", pe.numpy()), ("pageable int64", e.astype(np.int64)),
+                         ("frozen int64, repeat", frozen)):
             for _ in range(2):
                 run_contour((n, arr), make_schedule("c2"), **kw)
             ts = []
