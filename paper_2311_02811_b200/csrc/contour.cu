@@ -8,6 +8,7 @@
 // from a one-word device flag instead of an n-sized label diff.
 #include <cuda_runtime.h>
 #include <cub/cub.cuh>
+#include <emmintrin.h>
 #include <stdarg.h>
 #include <stdio.h>
 #include <string.h>
@@ -363,19 +364,21 @@ int check_run_args(cc_ctx* c, const cc_schedule* s, void* labels_out, int out_eb
 }
 
 // run_contour (engine.py:248-328) over the device kernels; caller holds c->mu.
+// start > 0: sweeps 1..start already ran (cc_run_host's streamed, counted
+// sweep 1) and changed something; the host loop continues from start + 1.
 int run_impl(cc_ctx* c, const cc_schedule* s, int flags, int64_t cap, void* labels_out,
-             int out_eb, cc_stats* st) {
+             int out_eb, cc_stats* st, int64_t start = 0) {
     const bool sync = s->sync != 0;
     const bool count = (flags & CC_RUN_COUNT_CHANGES) != 0;
     const bool check = (flags & CC_RUN_EARLY_CHECK) != 0;
     const bool times = (flags & CC_RUN_SWEEP_TIMES) != 0;
     const bool first_scatter = (flags & CC_RUN_FIRST_SCATTER) != 0;
     if (!sync && !count && !first_scatter && !(flags & CC_RUN_HOST_LOOP) && c->n > 0 &&
-        c->peers.n == 0)
+        c->peers.n == 0 && start == 0)
         return run_graph(c, s, cap, labels_out, out_eb, st, check ? 1 : 0);
     CUDA_TRY(cudaEventRecord(c->evs, c->stream));
-    CC_TRY(enqueue_init(c, sync));
-    int64_t sweep = 0, until_stable = 0;
+    if (start == 0) CC_TRY(enqueue_init(c, sync));
+    int64_t sweep = start, until_stable = start;
     int converged_by = 0;
     while (true) {
         ++sweep;
@@ -433,7 +436,7 @@ int run_impl(cc_ctx* c, const cc_schedule* s, int flags, int64_t cap, void* labe
 // exact counting / first scatter / host loop / peers, staged in input or
 // chunk-sorted order (the orders a sweep can follow while rows arrive).
 bool streamable(const cc_ctx* c, const cc_schedule* s, int flags) {
-    return !s->sync && !(flags & (CC_RUN_COUNT_CHANGES | CC_RUN_FIRST_SCATTER | CC_RUN_HOST_LOOP)) &&
+    return !s->sync && !(flags & (CC_RUN_FIRST_SCATTER | CC_RUN_HOST_LOOP)) &&
            c->peers.n == 0 && (c->stage_layout == 0 || c->stage_layout == 2);
 }
 
@@ -464,8 +467,10 @@ int cc_run_host(cc_ctx* c, const void* edges_host, int elem_bytes, int64_t m, in
         return run_impl(c, s, flags, cap, labels_out, out_eb, st);
     }
     const bool check = (flags & CC_RUN_EARLY_CHECK) != 0;
-    CC_TRY(stage(c, edges_host, elem_bytes, m, n, true, s, check, labels_out, out_eb));
+    const bool count = (flags & CC_RUN_COUNT_CHANGES) != 0;
+    CC_TRY(stage(c, edges_host, elem_bytes, m, n, true, s, check, labels_out, out_eb, count));
     const bool wrote = c->hflags[kFlagWrote] != 0;
+    const int64_t changed1 = count ? (int64_t)*c->hcount : (wrote ? -1 : 0);
     const bool passed = check && wrote && c->hflags[kFlagCheck] == 0;
     float sweep1_ms = 0.f;
     cudaEventElapsedTime(&sweep1_ms, c->ev0, c->ev1);
@@ -477,7 +482,8 @@ int cc_run_host(cc_ctx* c, const void* edges_host, int elem_bytes, int64_t m, in
         CUDA_TRY(cudaMemsetAsync(c->dflags, 0, sizeof(int) * kNumFlags, c->stream));
         cc_stats local = {};
         cc_stats* gs = st ? st : &local;
-        const int rc = run_graph(c, s, cap, nullptr, out_eb, gs, check ? 1 : 0, 1);
+        const int rc = count ? run_impl(c, s, flags, cap, nullptr, out_eb, gs, 1)
+                             : run_graph(c, s, cap, nullptr, out_eb, gs, check ? 1 : 0, 1);
         if (rc) {  // (e.g. the cap) -- no read-back may still be writing the caller's buffer
             if (labels_out) cudaEventSynchronize(c->spec_done);
             return rc;
@@ -514,7 +520,7 @@ int cc_run_host(cc_ctx* c, const void* edges_host, int elem_bytes, int64_t m, in
         st->compress_rounds = rounds;
         st->converge_seconds = seconds;
         if (st->capacity >= 1) {
-            if (st->changed_per_sweep) st->changed_per_sweep[0] = wrote ? -1 : 0;
+            if (st->changed_per_sweep) st->changed_per_sweep[0] = changed1;
             if (st->sweep_seconds) st->sweep_seconds[0] = sweep1_ms * 1e-3;
         }
     }

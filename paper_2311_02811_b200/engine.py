@@ -280,9 +280,10 @@ def run_host(ctx: _lib.Context, n: int, edges, schedule: Schedule, *, layout: st
              first_scatter: bool = False, host_loop: bool = False):
     """Stage host edges and run in ONE call (cc_run_host): for asynchronous
     runs in input / chunk-sorted order, sweep 1 runs chunk by chunk right
-    behind the host-to-device copy, so the transfer hides it; every other
-    case stages, then runs, exactly as stage_graph + run_staged.  Returns
-    (labels_out, IterationStats)."""
+    behind the host-to-device copy, so the transfer hides it (with exact
+    counts too: sweep 1 started from the identity, so its change count is the
+    number of cells with L[x] != x); every other case stages, then runs,
+    exactly as stage_graph + run_staged.  Returns (labels_out, IterationStats)."""
     ctx.staged = None
     e = _host_edges(edges)
     m = e.shape[0]
