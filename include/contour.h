@@ -83,8 +83,10 @@ int cc_version(void);
  * edges: (m, 2) row-major pairs, elem_bytes 4 (int32) or 8 (int64), as the
  * reference's g.edges.  Converted on device to packed uint32 SoA src[]/dst[]
  * with the endpoint range check of graph.py:73-79 (-> CC_EINVAL).
- * Host variant: the buffer is borrowed for the call only (pinned memory
- * gives full PCIe rate; pageable works).  Device variant: device pointer. */
+ * Host variant: the buffer is borrowed for the call only.  Pinned memory is
+ * read by the copy engine directly; pageable memory (a numpy array) is
+ * narrowed to uint32 pairs by the context's host threads into pinned staging
+ * chunks, pipelined with the copy.  Device variant: device pointer. */
 int cc_stage_edges(cc_ctx* ctx, const void* edges_host, int elem_bytes, int64_t m, int64_t n);
 int cc_stage_edges_device(cc_ctx* ctx, const void* edges_dev, int elem_bytes, int64_t m, int64_t n);
 /* Borrow caller-owned device SoA arrays (must outlive their use). */
@@ -98,18 +100,22 @@ int cc_labels_device(cc_ctx* ctx, uint32_t** labels_dev);
  * lowers nothing (ballot/OR flag) or the early check passes, then
  * pointer-jump compress.  cap: sweeps allowed (the reference uses n+2,
  * engine.py:275) -> CC_ECAP.  labels_out: host buffer of n elements of
- * out_elem_bytes (4 or 8), or NULL to leave labels on device. */
+ * out_elem_bytes (4 or 8), or NULL to leave labels on device (a pageable
+ * buffer is filled from a pinned read-back buffer by the context's threads). */
 int cc_run(cc_ctx* ctx, const cc_schedule* sched, int flags, int64_t cap,
            void* labels_out, int out_elem_bytes, cc_stats* stats);
 
 /* Stage host edges (as cc_stage_edges) AND run (as cc_run) in one call --
  * run_contour(g, ...) for a graph in host memory.  Asynchronous runs without
- * COUNT_CHANGES / FIRST_SCATTER / HOST_LOOP, staged in input or chunk-sorted
+ * FIRST_SCATTER / HOST_LOOP, staged in input or chunk-sorted
  * order (CC_OPT_STAGE_LAYOUT 0 or 2), run sweep 1 chunk by chunk right behind
  * the host-to-device copy (each chunk is swept as soon as it is staged, while
  * the next one is in flight), then its shortcut pass and early check, then
  * the device-side loop from sweep 2 if needed; sweep_seconds[0] is the span
- * of the streamed sweep.  Every other case stages, then runs. */
+ * of the streamed sweep.  With COUNT_CHANGES, sweep 1's exact count is the
+ * number of cells it moved off the identity (no shortcut pass then) and the
+ * counted host loop continues from sweep 2.  Every other case stages, then
+ * runs. */
 int cc_run_host(cc_ctx* ctx, const void* edges_host, int elem_bytes, int64_t m, int64_t n,
                 const cc_schedule* sched, int flags, int64_t cap, void* labels_out,
                 int out_elem_bytes, cc_stats* stats);
