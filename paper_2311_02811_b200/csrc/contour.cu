@@ -21,6 +21,8 @@
 #include <thread>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "contour.h"
 #include "gen_rng.cuh"
 #include "kernels.cuh"
@@ -52,6 +54,13 @@ static int fail(int code, const char* fmt, ...) {
         int rc_ = (x);           \
         if (rc_ != CC_OK) return rc_; \
     } while (0)
+
+// NVTX ranges around the C-ABI entry points (SURVEY §5 tracing): visible to
+// ncu --nvtx / nsys; a no-op without a tool attached.
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
 
 #include "device_aux.inc"
 
@@ -157,6 +166,7 @@ void cc_destroy(cc_ctx* c) {
 }
 
 int cc_stage_edges(cc_ctx* c, const void* edges, int eb, int64_t m, int64_t n) {
+    NvtxRange nvtx_("cc_stage_edges");
     if (!c) return fail(CC_EINVAL, "null context");
     std::lock_guard<std::mutex> lk(c->mu);
     DeviceGuard g(c->device);
@@ -164,6 +174,7 @@ int cc_stage_edges(cc_ctx* c, const void* edges, int eb, int64_t m, int64_t n) {
 }
 
 int cc_stage_edges_device(cc_ctx* c, const void* edges, int eb, int64_t m, int64_t n) {
+    NvtxRange nvtx_("cc_stage_edges_device");
     if (!c) return fail(CC_EINVAL, "null context");
     std::lock_guard<std::mutex> lk(c->mu);
     DeviceGuard g(c->device);
@@ -210,6 +221,7 @@ int cc_init_labels(cc_ctx* c) {
 }
 
 int cc_sweep(cc_ctx* c, int order, int sync, int atomic, int first, int* wrote_out) {
+    NvtxRange nvtx_("cc_sweep");
     if (!c) return fail(CC_EINVAL, "null context");
     std::lock_guard<std::mutex> lk(c->mu);
     DeviceGuard g(c->device);
@@ -446,6 +458,7 @@ extern "C" {
 
 int cc_run(cc_ctx* c, const cc_schedule* s, int flags, int64_t cap, void* labels_out, int out_eb,
            cc_stats* st) {
+    NvtxRange nvtx_("cc_run");
     CC_TRY(check_run_args(c, s, labels_out, out_eb));
     std::lock_guard<std::mutex> lk(c->mu);
     DeviceGuard g(c->device);
@@ -459,6 +472,7 @@ int cc_run(cc_ctx* c, const cc_schedule* s, int flags, int64_t cap, void* labels
 int cc_run_host(cc_ctx* c, const void* edges_host, int elem_bytes, int64_t m, int64_t n,
                 const cc_schedule* s, int flags, int64_t cap, void* labels_out, int out_eb,
                 cc_stats* st) {
+    NvtxRange nvtx_("cc_run_host");
     CC_TRY(check_run_args(c, s, labels_out, out_eb));
     std::lock_guard<std::mutex> lk(c->mu);
     DeviceGuard g(c->device);
@@ -573,6 +587,7 @@ int cc_set_peers(cc_ctx* c, const uint64_t* ptrs, int npeers) {
 // stats: changed_per_sweep = cells changed per iteration (exact, equal to the
 // reference's), converged_by = 2 ("grandparent-stable").
 int cc_fastsv(cc_ctx* c, int64_t cap, void* labels_out, int out_eb, cc_stats* st, int flags) {
+    NvtxRange nvtx_("cc_fastsv");
     if (!c) return fail(CC_EINVAL, "null context");
     if (labels_out && out_eb != 4 && out_eb != 8)
         return fail(CC_EINVAL, "label element size must be 4 or 8");
@@ -743,6 +758,7 @@ int cc_set_option(cc_ctx* c, int option, int64_t value) {
 extern "C" {
 
 int cc_reorder_edges(cc_ctx* c, int mode) {
+    NvtxRange nvtx_("cc_reorder_edges");
     if (!c) return fail(CC_EINVAL, "null context");
     if (mode == 0) return CC_OK;
     if (mode < 1 || mode > 5) return fail(CC_EINVAL, "unknown edge layout mode %d", mode);
