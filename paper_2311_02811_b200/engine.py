@@ -12,6 +12,7 @@ from __future__ import annotations
 
 import ctypes
 import threading
+import weakref
 from dataclasses import dataclass, field
 from typing import Optional
 
@@ -371,7 +372,7 @@ def run_contour(g, schedule: Schedule, threads: int = 1, seed: Optional[int] = N
     # previous call on this context stays resident and is reused -- as the
     # device layout for resident graphs (resolve_layout(resident=True)).
     frozen = isinstance(edges, np.ndarray) and not edges.flags.writeable
-    if frozen and ctx.staged is not None and ctx.staged[0] is edges and \
+    if frozen and ctx.staged is not None and ctx.staged[0]() is edges and \
             ctx.staged[1:3] == (n, layout):
         if ctx.staged[3]:  # upgrade the streamed layout once (+ the hybrid's bucketed copy)
             _lib.check(ctx.lib.cc_reorder_edges(ctx.handle, LAYOUTS[ctx.staged[3]]))
@@ -399,7 +400,8 @@ def run_contour(g, schedule: Schedule, threads: int = 1, seed: Optional[int] = N
             if want != staged:
                 # only layouts reachable from the staged order in place
                 upgrade = want if (staged, want) in (("chunk_sorted", "hybrid"),) else None
-            ctx.staged = (edges, n, layout, upgrade)
+            # a weak reference: the cache must not keep the caller's array alive
+            ctx.staged = (weakref.ref(edges), n, layout, upgrade)
     return labels, stats
 
 

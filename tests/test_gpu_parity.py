@@ -847,7 +847,7 @@ def test_frozen_edges_stay_resident():
         labels, st = run_contour((n, e), make_schedule("c2"))
         assert np.array_equal(labels, exp), i
         check_invariants(labels, st)
-        assert ctx.staged is not None and ctx.staged[0] is e
+        assert ctx.staged is not None and ctx.staged[0]() is e
     labels, st = run_contour((n, e), make_schedule("c2", sync=True))  # any schedule
     assert np.array_equal(labels, exp)
     n2, e2 = graphgen.grid(120, 130, 0.55, 1)
@@ -855,10 +855,17 @@ def test_frozen_edges_stay_resident():
     e2.flags.writeable = False
     assert np.array_equal(run_contour((n2, e2), make_schedule("c2"))[0],
                           oracle.rem_union_find(n2, e2))
-    assert ctx.staged[0] is e2
+    assert ctx.staged[0]() is e2
     assert early_convergence_check((n2, e2), oracle.rem_union_find(n2, e2))
     assert ctx.staged is None  # the check staged its own copy
     assert np.array_equal(run_contour((n, e), make_schedule("c2"))[0], exp)
     w = np.array(e)  # writeable copy: never cached
     assert np.array_equal(run_contour((n, w), make_schedule("cm"))[0], exp)
     assert ctx.staged is None
+    import gc
+    e3 = np.array(e)
+    e3.flags.writeable = False
+    assert np.array_equal(run_contour((n, e3), make_schedule("c2"))[0], exp)
+    del e3
+    gc.collect()
+    assert ctx.staged[0]() is None  # the cache holds no reference to a dropped array
