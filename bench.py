@@ -335,7 +335,7 @@ def run_single(args, device):
     ev0.record(stream)
     stats = []
     for _ in range(args.steps):
-        _, st = engine.run_staged(ctx, sched, sweep_times=True, **kw)
+        _, st = engine.run_staged(ctx, sched, sweep_times=False, **kw)
         stats.append(st)
     ev1.record(stream)
     torch.cuda.synchronize()
@@ -493,7 +493,9 @@ def run_single(args, device):
                    "parallelism": "single GPU",
                    "l2": "inputs larger than L2 (edge stream 8m B > 126 MB); no flush"},
         "sweeps_per_run": sweeps,
-        "sweep_ms": [round(t * 1e3, 4) for t in stats[-1].sweep_seconds],
+        # per-sweep device times of one untimed run (the timed runs skip the records)
+        "sweep_ms": [round(t * 1e3, 4) for t in
+                     engine.run_staged(ctx, sched, sweep_times=True, **kw)[1].sweep_seconds],
         "reference_sweeps": ref_sweeps,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
