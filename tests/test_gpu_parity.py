@@ -869,3 +869,36 @@ def test_frozen_edges_stay_resident():
     del e3
     gc.collect()
     assert ctx.staged[0]() is None  # the cache holds no reference to a dropped array
+
+
+def test_concurrent_callers_reentrant():
+    """Reentrancy (the reference's SPEC.md:212: independent runs on shared
+    immutable graphs from several threads): every caller thread gets its own
+    context; concurrent run_contour calls on a shared frozen graph and on
+    private graphs all return exact labels."""
+    import threading
+    n, e = graphgen.rmat(14, 16, 11)
+    e = np.ascontiguousarray(e)
+    e.flags.writeable = False
+    exp = oracle.rem_union_find(n, e)
+    privates = [graphgen.grid(100 + 10 * i, 90, 0.55, i) for i in range(4)]
+    pexp = [oracle.rem_union_find(pn, pe) for pn, pe in privates]
+    errors = []
+
+    def work(i):
+        try:
+            for it in range(5):
+                labels, st = run_contour((n, e), make_schedule("c2" if it % 2 else "cm"))
+                assert np.array_equal(labels, exp), (i, it)
+                pn, pe = privates[i]
+                labels, st = run_contour((pn, pe), make_schedule("c2", sync=bool(it % 2)))
+                assert np.array_equal(labels, pexp[i]), (i, it)
+        except Exception as exc:  # pragma: no cover - reported below
+            errors.append(exc)
+
+    threads = [threading.Thread(target=work, args=(i,)) for i in range(4)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors[:3]
