@@ -17,8 +17,7 @@ def main():
         spec = graphgen.CONFIGS[cfg]
         if spec["kind"] == "rmat":
             n, m = graphgen.rmat_device(ctx, spec["scale"], spec["edgefactor"], 1)
-            lay = engine.resolve_layout("auto", m, n)
-            _lib.check(ctx.lib.cc_reorder_edges(ctx.handle, engine.LAYOUTS[lay]))
+            engine.apply_layout(ctx, engine.resolve_layout("auto", m, n))
         else:
             n, e = graphgen.make(spec, 1, elem_bytes=4)
             engine.stage_graph(ctx, n, e)
