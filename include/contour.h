@@ -197,11 +197,23 @@ int cc_compress(cc_ctx* ctx, int* rounds_out);
 int cc_shortcut(cc_ctx* ctx, int passes);
 /* early_convergence_check(g, labels) (engine.py:331-365) on device. */
 int cc_early_check(cc_ctx* ctx, int* ok_out);
+/* The same check as the device convergence loop runs it after a changing
+ * sweep (layout-aware: shared-memory slices on the bucketed layouts, the
+ * cache-hinted pass on L2-window tiles) on the current device labels. */
+int cc_loop_check(cc_ctx* ctx, int* ok_out);
 /* Size-independent certificate of the device labels: *result bit 0 = some
  * edge has L[u] != L[v], bit 1 = some L[L[x]] != L[x], bit 2 = some
  * L[x] > x; 0 means every component carries one root label <= its IDs. */
 int cc_verify(cc_ctx* ctx, int* result);
 int cc_read_labels(cc_ctx* ctx, void* out_host, int elem_bytes);
+/* The staged rows [row_lo, row_hi) back to host memory as (rows, 2) pairs of
+ * elem_bytes (4 or 8), in their current device order (input order until a
+ * layout is applied; with layout 3 the bucketed order).  The inverse of
+ * cc_stage_edges -- e.g. to hand a graph generated on the device
+ * (cc_gen_rmat_device) to host-side callers such as the reference's own
+ * Graph type.  Pageable destinations are filled by the context's threads
+ * from pinned chunks, overlapped with the next chunk's copy. */
+int cc_read_edges(cc_ctx* ctx, void* out_host, int elem_bytes, int64_t row_lo, int64_t row_hi);
 /* Load caller labels (n int64 or int32 host values, each in 0..n-1, else
  * CC_EINVAL) as the device labels -- e.g. before cc_early_check on labels
  * from elsewhere (early_convergence_check(g, labels), engine.py:331-348). */

@@ -76,7 +76,10 @@ SIGNATURES = {
     "cc_shortcut": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
     "cc_early_check": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_int)]),
     "cc_read_labels": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]),
+    "cc_read_edges": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int,
+                                     ctypes.c_int64, ctypes.c_int64]),
     "cc_write_labels": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]),
+    "cc_loop_check": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_int)]),
     "cc_verify": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_int)]),
     "cc_synchronize": (ctypes.c_int, [ctypes.c_void_p]),
     "cc_mm_order": (ctypes.c_int, [_I64P, _I64P, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,

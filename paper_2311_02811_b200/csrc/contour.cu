@@ -272,6 +272,24 @@ int cc_early_check(cc_ctx* c, int* ok) {
     return early_check(c, ok);
 }
 
+// The early check exactly as the convergence loop runs it after a changing
+// sweep (layout-aware halves: shared-memory slices on bucketed layouts,
+// cache-hinted few-CTA pass on L2-window tiles) on the current labels.
+int cc_loop_check(cc_ctx* c, int* ok) {
+    if (!c || !ok) return fail(CC_EINVAL, "null argument");
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard g(c->device);
+    *ok = 1;
+    if (c->n == 0) return CC_OK;
+    CUDA_TRY(cudaMemsetAsync(c->dflags + kFlagCheck, 0, sizeof(int), c->stream));
+    CUDA_TRY(cudaMemsetAsync(c->dflags + kFlagWrote, 1, 1, c->stream));  // "the sweep changed"
+    CC_TRY(enqueue_loop_check(c, c->stream));
+    CUDA_TRY(cudaMemsetAsync(c->dflags + kFlagWrote, 0, sizeof(int), c->stream));
+    CC_TRY(read_flags(c));
+    *ok = c->hflags[kFlagCheck] == 0;
+    return CC_OK;
+}
+
 // Size-independent certificate of a final labelling (used where the host
 // oracle cannot run): bit 0 some edge has L[u] != L[v], bit 1 some label is
 // not a root (L[L[x]] != L[x]), bit 2 some L[x] > x.  0 = every component
@@ -353,6 +371,91 @@ int cc_read_labels(cc_ctx* c, void* out, int eb) {
     std::lock_guard<std::mutex> lk(c->mu);
     DeviceGuard g(c->device);
     return copy_out(c, out, eb);
+}
+
+}  // extern "C"
+
+namespace {
+
+// The staged rows back in host memory, in their current device order, as the
+// reference's (m, 2) pair array: device AoS conversion per chunk, then the
+// copy engine into pinned buffers that the context's threads hand over to a
+// pageable destination while the next chunk is in flight (or straight into
+// a pinned destination).
+template <typename T>
+int read_edges_impl(cc_ctx* c, T* out, int64_t lo, int64_t hi) {
+    const int64_t chunk = (int64_t)1 << 23;
+    const bool pageable = host_pageable(out);
+    T* dbuf[2] = {nullptr, nullptr};
+    T* hbuf[2] = {nullptr, nullptr};
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    int rc = CC_OK;
+    auto cleanup = [&]() {
+        for (int b = 0; b < 2; ++b) {
+            if (ev[b]) { cudaEventSynchronize(ev[b]); cudaEventDestroy(ev[b]); }
+            cudaFree(dbuf[b]);
+            cudaFreeHost(hbuf[b]);
+        }
+    };
+    auto step = [&]() -> int {
+        for (int b = 0; b < 2; ++b) {
+            CUDA_TRY(cudaMalloc(&dbuf[b], sizeof(T) * 2 * chunk));
+            if (pageable) CUDA_TRY(cudaHostAlloc(&hbuf[b], sizeof(T) * 2 * chunk, cudaHostAllocDefault));
+            CUDA_TRY(cudaEventCreateWithFlags(&ev[b], cudaEventDisableTiming));
+        }
+        int64_t prev_off = -1, prev_rows = 0;
+        int k = 0;
+        for (int64_t off = lo; off < hi; off += chunk, ++k) {
+            const int b = k & 1;
+            const int64_t rows = std::min<int64_t>(chunk, hi - off);
+            k_unstage<T><<<grid_for(c, rows), kThreads, 0, c->stream>>>(c->src + off, c->dst + off,
+                                                                        rows, dbuf[b]);
+            CUDA_TRY(cudaGetLastError());
+            T* target = pageable ? hbuf[b] : out + 2 * (off - lo);
+            CUDA_TRY(cudaMemcpyAsync(target, dbuf[b], sizeof(T) * 2 * rows, cudaMemcpyDeviceToHost,
+                                     c->stream));
+            CUDA_TRY(cudaEventRecord(ev[b], c->stream));
+            if (pageable && prev_off >= 0) {  // hand over the previous chunk meanwhile
+                CUDA_TRY(cudaEventSynchronize(ev[b ^ 1]));
+                const T* h = hbuf[b ^ 1];
+                T* o = out + 2 * (prev_off - lo);
+                ensure_pool(c)->run(prev_rows, [&](int64_t a, int64_t e) {
+                    memcpy(o + 2 * a, h + 2 * a, sizeof(T) * 2 * (e - a));
+                });
+            }
+            prev_off = off;
+            prev_rows = rows;
+        }
+        CUDA_TRY(cudaStreamSynchronize(c->stream));
+        if (pageable && prev_off >= 0) {
+            const T* h = hbuf[(k - 1) & 1];
+            T* o = out + 2 * (prev_off - lo);
+            ensure_pool(c)->run(prev_rows, [&](int64_t a, int64_t e) {
+                memcpy(o + 2 * a, h + 2 * a, sizeof(T) * 2 * (e - a));
+            });
+        }
+        return CC_OK;
+    };
+    rc = step();
+    cleanup();
+    return rc;
+}
+
+}  // namespace
+
+extern "C" {
+
+int cc_read_edges(cc_ctx* c, void* out, int eb, int64_t lo, int64_t hi) {
+    NvtxRange nvtx_("cc_read_edges");
+    if (!c) return fail(CC_EINVAL, "null context");
+    if (eb != 4 && eb != 8) return fail(CC_EINVAL, "edge element size must be 4 or 8");
+    std::lock_guard<std::mutex> lk(c->mu);
+    if (lo < 0 || hi > c->m || lo > hi) return fail(CC_EINVAL, "bad row range");
+    if (hi > lo && !out) return fail(CC_EINVAL, "null output buffer");
+    if (hi == lo) return CC_OK;
+    DeviceGuard g(c->device);
+    if (eb == 4) return read_edges_impl<int32_t>(c, (int32_t*)out, lo, hi);
+    return read_edges_impl<int64_t>(c, (int64_t*)out, lo, hi);
 }
 
 int cc_synchronize(cc_ctx* c) {

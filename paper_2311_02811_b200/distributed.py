@@ -148,10 +148,15 @@ class FusedShardedContour(_HostIO):
         self.m_total = m_total
         self.cap = n + 2 if cap is None else cap
         self.layout = "input"
+        self.host_edges = None  # host copy of the shard (from_rmat keep_host)
 
     @classmethod
     def from_rmat(cls, scale: int, edgefactor: int, seed: int, rank: int, world: int,
-                  device: int, layout: str = "auto", atomic: bool = True, group=None):
+                  device: int, layout: str = "auto", atomic: bool = True, group=None,
+                  keep_host: bool = False):
+        """This rank's contiguous row shard of the symmetrised RMAT list,
+        generated on its GPU and laid out; ``keep_host``: also keep a host
+        int64 copy of the shard in input order (``host_edges``, the e2e leg)."""
         import torch
 
         from .engine import LAYOUTS, resolve_layout
@@ -160,11 +165,13 @@ class FusedShardedContour(_HostIO):
         total = 2 * edgefactor * n
         lo, hi = shard_rows(total, rank, world)
         graphgen.rmat_device(ctx, scale, edgefactor, seed, row_lo=lo, row_hi=hi)
+        host = graphgen.read_edges(ctx, 8) if keep_host else None  # input order, pre-layout
         layout = resolve_layout(layout, hi - lo, n, resident=False)  # no bucketed copy
         if LAYOUTS[layout]:
             _lib.check(ctx.lib.cc_reorder_edges(ctx.handle, LAYOUTS[layout]))
         runner = cls(PeerShard(ctx, n, atomic, group), n, total)
         runner.layout = layout
+        runner.host_edges = host
         return runner
 
     def _flag_any(self, wrote: int) -> bool:
@@ -215,17 +222,21 @@ class HybridShardedContour(_HostIO):
         self.m_total = m_total
         self.cap = n + 2 if cap is None else cap
         self.layout = "input"
+        self.host_edges = None  # host copy of the shard (from_rmat keep_host)
         self.first_sweeps = max(1, int(first_sweeps))
         self.labels = shard.labels_tensor()
         self.allreduce = allreduce or nccl_allreduce_min(shard.group)
 
     @classmethod
     def from_rmat(cls, scale: int, edgefactor: int, seed: int, rank: int, world: int,
-                  device: int, layout: str = "auto", atomic: bool = True, group=None):
+                  device: int, layout: str = "auto", atomic: bool = True, group=None,
+                  keep_host: bool = False):
         base = FusedShardedContour.from_rmat(scale, edgefactor, seed, rank, world, device,
-                                             layout=layout, atomic=atomic, group=group)
+                                             layout=layout, atomic=atomic, group=group,
+                                             keep_host=keep_host)
         runner = cls(base.shard, base.n, base.m_total)
         runner.layout = base.layout
+        runner.host_edges = base.host_edges
         return runner
 
     def run(self) -> int:
@@ -299,13 +310,16 @@ class ShardedContour(_HostIO):
         self.allreduce = allreduce or nccl_allreduce_min(group)
         self.cap = n + 2 if cap is None else cap
         self.layout = "input"
+        self.host_edges = None  # host copy of the shard (from_rmat keep_host)
         self.first_scatter = False  # load-free sweep 1 (exact, but adds a sweep on RMAT)
 
     @classmethod
     def from_rmat(cls, scale: int, edgefactor: int, seed: int, rank: int, world: int,
-                  device: int, layout: str = "auto", atomic: bool = True, **kw):
+                  device: int, layout: str = "auto", atomic: bool = True,
+                  keep_host: bool = False, **kw):
         """Generate this rank's contiguous row shard of the symmetrised RMAT
-        list on its GPU and lay it out (engine.resolve_layout)."""
+        list on its GPU and lay it out (engine.resolve_layout); ``keep_host``
+        keeps a host int64 copy of the shard in input order (``host_edges``)."""
         import torch
 
         from .engine import LAYOUTS, resolve_layout
@@ -314,11 +328,13 @@ class ShardedContour(_HostIO):
         total = 2 * edgefactor * n
         lo, hi = shard_rows(total, rank, world)
         graphgen.rmat_device(ctx, scale, edgefactor, seed, row_lo=lo, row_hi=hi)
+        host = graphgen.read_edges(ctx, 8) if keep_host else None  # input order, pre-layout
         layout = resolve_layout(layout, hi - lo, n, resident=False)  # no bucketed copy
         if LAYOUTS[layout]:
             _lib.check(ctx.lib.cc_reorder_edges(ctx.handle, LAYOUTS[layout]))
         runner = cls(CudaShard(ctx, n, atomic), n, total, **kw)
         runner.layout = layout
+        runner.host_edges = host
         return runner
 
     def run(self) -> int:

@@ -325,6 +325,14 @@ def verify_staged(ctx: _lib.Context) -> int:
     return r.value
 
 
+def loop_check(ctx: _lib.Context) -> bool:
+    """The early convergence check (engine.py:331-348) exactly as the device
+    loop runs it after a changing sweep, on the context's current labels."""
+    ok = ctypes.c_int(0)
+    _lib.check(ctx.lib.cc_loop_check(ctx.handle, ctypes.byref(ok)))
+    return bool(ok.value)
+
+
 def run_contour(g, schedule: Schedule, threads: int = 1, seed: Optional[int] = None, *,
                 device: int = 0, count_changes: bool = True, early_check: bool = True,
                 sweep_times: bool = True, layout: str = "auto",

@@ -126,6 +126,21 @@ def rmat_device(ctx: _lib.Context, scale: int, edgefactor: int = 16, seed: int =
     return n, hi - row_lo
 
 
+def read_edges(ctx: _lib.Context, elem_bytes: int = 8, row_lo: int = 0, row_hi=None,
+               out: np.ndarray | None = None) -> np.ndarray:
+    """The context's staged rows [row_lo, row_hi) as a host (rows, 2) array
+    (cc_read_edges) -- e.g. an RMAT-28 edge list generated on the device in a
+    second, handed to host-side callers as the reference's int64 pairs."""
+    hi = ctx.m if row_hi is None else int(row_hi)
+    e = _alloc(hi - row_lo, elem_bytes) if out is None else out
+    if e.shape != (hi - row_lo, 2) or e.dtype.itemsize != elem_bytes or \
+            not e.flags.c_contiguous:
+        raise ValueError("out must be a C-contiguous (rows, 2) array of elem_bytes")
+    _lib.check(ctx.lib.cc_read_edges(ctx.handle, ctypes.c_void_p(e.ctypes.data), elem_bytes,
+                                     row_lo, hi))
+    return e
+
+
 # BASELINE.json configs (DESIGN.md "Inputs" documents every deviation)
 CONFIGS = {
     "er": dict(kind="er", n=65536, pairs=524288),
