@@ -143,7 +143,12 @@ int cc_sweep(cc_ctx* ctx, int order, int sync, int atomic, int first, int* wrote
  * time -- for label arrays larger than L2 (RMAT-28: 1 GB); mode 5 (hybrid)
  * keeps the current row order for sweep 1 and builds a mode-3 copy of the
  * rows (8m more bytes) that the later order-2 sweeps and checks walk with
- * shared-memory dst slices. */
+ * shared-memory dst slices; mode 6 is mode 4 plus a copy of the rows for the
+ * early check (8m more bytes): inside each L2 window the rows regrouped by
+ * 2^CC_OPT_CHECK_SHIFT-vertex dst buckets and src-sorted, walked with a
+ * component bitmap (one bit per vertex: "labelled like the giant
+ * component") whose dst part sits in shared memory -- the check then
+ * streams rows instead of gathering labels. */
 int cc_reorder_edges(cc_ctx* ctx, int mode);
 
 /* Tuning knobs of a context.  Store modes for async sweeps:
@@ -183,6 +188,11 @@ int cc_reorder_edges(cc_ctx* ctx, int mode);
                                       1; applied when the layout is built) */
 #define CC_OPT_SWEEP_CTAS 16       /* flat order-1/2/h sweeps: CTAs per SM (0 = auto, default:
                                       3 on dense L2-window tiles, else the occupancy limit) */
+#define CC_OPT_CHECK_SHIFT 17      /* layout 6: 2^shift-vertex dst buckets of the check copy
+                                      (7..20, default 20 = 128 KB of bitmap per CTA) */
+#define CC_OPT_FLAT_BITS 18        /* early check on flat rows with the component bitmap:
+                                      0 never, 1 always, 2 auto (default: labels beyond L2
+                                      and m >= 4n, e.g. one-shot RMAT-28) */
 #define CC_OPT_STAGE_LAYOUT 4     /* layout applied while staging: 0 input order (default),
                                       2 chunk-sorted, each chunk sorted as soon as it lands,
                                       overlapped with the next chunk's host->device copy */

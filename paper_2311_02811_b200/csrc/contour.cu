@@ -14,6 +14,9 @@
 #include <string.h>
 
 #include <algorithm>
+#include <atomic>
+#include <map>
+#include <tuple>
 #include <condition_variable>
 #include <functional>
 #include <memory>
@@ -127,6 +130,8 @@ void cc_destroy(cc_ctx* c) {
     cudaFree(c->bsrc);
     cudaFree(c->bdst);
     cudaFree(c->bdst16);
+    cudaFree(c->bits);
+    cudaFree(c->dr0);
     for (int b = 0; b < 2; ++b) cudaFreeHost(c->hstage[b]);
     cudaFreeHost(c->hlab);
     if (c->own_labels) cudaFree(c->labels);
@@ -843,6 +848,16 @@ int cc_set_option(cc_ctx* c, int option, int64_t value) {
             c->sweep_ctas = (int)value;
             c->loop_key.m = -1;
             return CC_OK;
+        case CC_OPT_FLAT_BITS:
+            if (value < 0 || value > 2) return fail(CC_EINVAL, "flat bits must be 0, 1 or 2");
+            c->flat_bits = (int)value;
+            c->loop_key.m = -1;
+            return CC_OK;
+        case CC_OPT_CHECK_SHIFT:
+            if (value < 7 || value > 20)
+                return fail(CC_EINVAL, "check shift must be in [7, 20] (<= 128 KB of bits)");
+            c->check_shift = (int)value;
+            return CC_OK;
         case CC_OPT_WARP_TRANSPOSE:
             c->warp_transpose = value != 0;
             return CC_OK;
@@ -864,12 +879,12 @@ int cc_reorder_edges(cc_ctx* c, int mode) {
     NvtxRange nvtx_("cc_reorder_edges");
     if (!c) return fail(CC_EINVAL, "null context");
     if (mode == 0) return CC_OK;
-    if (mode < 1 || mode > 5) return fail(CC_EINVAL, "unknown edge layout mode %d", mode);
+    if (mode < 1 || mode > 6) return fail(CC_EINVAL, "unknown edge layout mode %d", mode);
     std::lock_guard<std::mutex> lk(c->mu);
     DeviceGuard g(c->device);
     if (c->m < 2) return CC_OK;
     if (mode == 3 || mode == 5) return reorder_bucketed(c, mode);
-    if (mode == 4) return reorder_l2tiles(c);
+    if (mode == 4 || mode == 6) return reorder_l2tiles(c, mode);
     c->layout = mode;
     // mode 1: one global sort by src; mode 2: independent sorts of
     // consecutive chunks of c->sort_chunk rows (each chunk's label gathers

@@ -166,7 +166,7 @@ class FusedShardedContour(_HostIO):
         lo, hi = shard_rows(total, rank, world)
         graphgen.rmat_device(ctx, scale, edgefactor, seed, row_lo=lo, row_hi=hi)
         host = graphgen.read_edges(ctx, 8) if keep_host else None  # input order, pre-layout
-        layout = resolve_layout(layout, hi - lo, n, resident=False)  # no bucketed copy
+        layout = resolve_layout(layout, hi - lo, n, copies=False)  # one row array
         if LAYOUTS[layout]:
             _lib.check(ctx.lib.cc_reorder_edges(ctx.handle, LAYOUTS[layout]))
         runner = cls(PeerShard(ctx, n, atomic, group), n, total)
@@ -329,7 +329,7 @@ class ShardedContour(_HostIO):
         lo, hi = shard_rows(total, rank, world)
         graphgen.rmat_device(ctx, scale, edgefactor, seed, row_lo=lo, row_hi=hi)
         host = graphgen.read_edges(ctx, 8) if keep_host else None  # input order, pre-layout
-        layout = resolve_layout(layout, hi - lo, n, resident=False)  # no bucketed copy
+        layout = resolve_layout(layout, hi - lo, n, copies=False)  # one row array
         if LAYOUTS[layout]:
             _lib.check(ctx.lib.cc_reorder_edges(ctx.handle, LAYOUTS[layout]))
         runner = cls(CudaShard(ctx, n, atomic), n, total, **kw)

@@ -137,7 +137,7 @@ def _unpack_graph(g):
 
 
 LAYOUTS = {"input": 0, "src_sorted": 1, "chunk_sorted": 2, "dst_bucketed": 3, "l2_tiled": 4,
-           "hybrid": 5}
+           "hybrid": 5, "l2_tiled_check": 6}
 AUTO_SORT_MIN_ROWS = 1 << 16
 
 
@@ -147,7 +147,8 @@ AUTO_L2_LABEL_BYTES = 96 << 20  # the 126 MB L2 holds the labels plus the edge s
 AUTO_HYBRID_MIN_DEGREE = 8  # rows per vertex from which the bucketed copy pays (measured)
 
 
-def resolve_layout(layout: str, m: int, n: int = 0, resident: bool = True) -> str:
+def resolve_layout(layout: str, m: int, n: int = 0, resident: bool = True,
+                   copies: bool = True) -> str:
     """"auto": input order below 2^16 rows (ER n=65,536, 524,282 rows: 0.088 ms
     per run chunk-sorted vs 0.11 ms in input order); while the label array fits
     comfortably in L2, chunk-sorted staging (it hides under the host->device
@@ -155,15 +156,21 @@ def resolve_layout(layout: str, m: int, n: int = 0, resident: bool = True) -> st
     (``resident``) with >= 8 rows per vertex and m < 2^31, the dst-bucketed
     copy of the hybrid layout (later sweeps and the early check gather dst
     labels from shared memory: RMAT-20..23 12-17 % faster per run; grid and
-    ER are slower with it); L2-window tiles (layout 4) for larger label
-    arrays.  One-shot runs from host memory (run_host) keep chunk_sorted so
-    sweep 1 streams behind the copy."""
+    ER are slower with it).  Label arrays beyond L2: L2-window tiles, with
+    the bitmap check copy for resident dense graphs (m >= 4n, RMAT-28: 57 vs
+    77-83 ms per run, DESIGN 5.19); one-shot runs from host memory
+    (``resident=False``) of dense graphs stay chunk-sorted, so sweep 1
+    streams behind the copy and the tiling (0.5 s at RMAT-28) is skipped
+    (DESIGN 5.20).  ``copies=False``: no extra copy of the rows (the
+    multi-GPU shards: their fused exchange walks one row array)."""
     if layout == "auto":
         if m < AUTO_SORT_MIN_ROWS:
             return "input"
         if 4 * n > AUTO_L2_LABEL_BYTES:
-            return "l2_tiled"
-        if resident and m < (1 << 31) and m >= AUTO_HYBRID_MIN_DEGREE * n:
+            if not resident:
+                return "chunk_sorted" if m >= 4 * n else "l2_tiled"
+            return "l2_tiled_check" if copies and m >= 4 * n else "l2_tiled"
+        if resident and copies and m < (1 << 31) and m >= AUTO_HYBRID_MIN_DEGREE * n:
             return "hybrid"
         return "chunk_sorted"
     if layout not in LAYOUTS:
@@ -220,7 +227,7 @@ def stage_graph(ctx: _lib.Context, n: int, edges, layout: str = "auto") -> None:
         _lib.check(lib.cc_stage_edges(ctx.handle, ctypes.c_void_p(e.ctypes.data),
                                       e.dtype.itemsize, m, n))
     ctx.n, ctx.m = n, m
-    if layout in ("src_sorted", "dst_bucketed", "l2_tiled", "hybrid"):
+    if layout in ("src_sorted", "dst_bucketed", "l2_tiled", "hybrid", "l2_tiled_check"):
         _lib.check(lib.cc_reorder_edges(ctx.handle, LAYOUTS[layout]))
 
 

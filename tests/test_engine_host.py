@@ -69,10 +69,14 @@ def test_auto_layout_policy():
     assert resolve_layout("auto", 134217728, 4194304) == "hybrid"               # RMAT-22
     assert resolve_layout("auto", 134217728, 4194304, resident=False) == "chunk_sorted"
     assert resolve_layout("auto", 18446634, 16777216) == "chunk_sorted"          # grid 4096^2
-    assert resolve_layout("auto", 8589934592, 268435456) == "l2_tiled"           # RMAT-28
+    assert resolve_layout("auto", 8589934592, 268435456) == "l2_tiled_check"     # RMAT-28
+    assert resolve_layout("auto", 8589934592, 268435456, resident=False) == "chunk_sorted"
+    assert resolve_layout("auto", 8589934592 // 8, 268435456, copies=False) == "l2_tiled"
+    assert resolve_layout("auto", 1845476017, 2307095021, resident=False) == "l2_tiled"
     assert resolve_layout("auto", 1845476017, 2307095021) == "l2_tiled"          # forest
     assert resolve_layout("auto", 1 << 31, 1 << 24) == "chunk_sorted"            # m >= 2^31
-    for lay in ("input", "src_sorted", "chunk_sorted", "dst_bucketed", "l2_tiled", "hybrid"):
+    for lay in ("input", "src_sorted", "chunk_sorted", "dst_bucketed", "l2_tiled", "hybrid",
+                "l2_tiled_check"):
         assert resolve_layout(lay, 10, 10) == lay
     with pytest.raises(ValueError):
         resolve_layout("bogus", 10, 10)

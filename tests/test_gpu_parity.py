@@ -557,7 +557,8 @@ def test_random_graphs_every_layout_and_loop():
     import os
     rng = np.random.default_rng(int(os.environ.get("CC_FUZZ_SEED", "20261020")))
     ctx = _lib.Context(0)
-    layouts = ("input", "src_sorted", "chunk_sorted", "dst_bucketed", "l2_tiled", "hybrid")
+    layouts = ("input", "src_sorted", "chunk_sorted", "dst_bucketed", "l2_tiled", "hybrid",
+               "l2_tiled_check")
     for t in range(int(os.environ.get("CC_FUZZ_ITERS", "120"))):
         n = int(rng.integers(1, 6000))
         m = int(rng.integers(0, 25000))
@@ -573,6 +574,8 @@ def test_random_graphs_every_layout_and_loop():
         chunk = int(rng.integers(1, 9000))
         ctx.set_option(_lib.CC_OPT_SORT_CHUNK, chunk if t % 2 else 128 * (chunk // 128 + 1))
         ctx.set_option(_lib.CC_OPT_TILE_SHIFT, 10)
+        ctx.set_option(_lib.CC_OPT_CHECK_SHIFT, int(rng.integers(7, 11)))
+        ctx.set_option(_lib.CC_OPT_FLAT_BITS, int(rng.integers(0, 3)))
         ctx.set_option(_lib.CC_OPT_ITEM_ORDER, int(t % 4))
         ctx.set_option(_lib.CC_OPT_WARP_TRANSPOSE, int(rng.integers(0, 4) > 0))
         ctx.set_option(_lib.CC_OPT_SWEEP_CTAS, int(rng.integers(0, 4)))
@@ -715,22 +718,75 @@ def test_dst_bucketed_layout_exact(bshift, item_rows, threads, pipe, order):
     ctx.close()
 
 
+@pytest.mark.parametrize("layout", ["l2_tiled", "l2_tiled_check"])
 @pytest.mark.parametrize("tile_shift", [10, 14])
-def test_l2_tiled_layout_exact(tile_shift):
+def test_l2_tiled_layout_exact(tile_shift, layout):
     ctx = _lib.Context(0)
     ctx.set_option(_lib.CC_OPT_TILE_SHIFT, tile_shift)
+    ctx.set_option(_lib.CC_OPT_CHECK_SHIFT, tile_shift - 2)
     for n, e in (graphgen.rmat(16, 16, 6), graphgen.grid(400, 300, 0.55, 9),
                  graphgen.forest(60, 7), spec.erdos_renyi(5000, 20001, 2)):
         if (n + (1 << tile_shift) - 1) >> tile_shift > 1024:
             continue
         exp = oracle.rem_union_find(n, e)
-        engine.stage_graph(ctx, n, e, "l2_tiled")
+        engine.stage_graph(ctx, n, e, layout)
         for sched in (make_schedule("c2"), make_schedule("cm", 16), make_schedule("c2", sync=True)):
+            for early in (False, True):
+                labels = np.empty(n, dtype=np.int64)
+                engine.run_staged(ctx, sched, labels_out=labels, count_changes=False,
+                                  early_check=early)
+                assert np.array_equal(labels, exp), (n, sched, early)
+                assert engine.verify_staged(ctx) == 0
+    ctx.close()
+
+
+@pytest.mark.parametrize("check_shift", [7, 9, 12])
+def test_bitmap_check_equals_oracle_early_check(check_shift):
+    """The layout-6 early check (component bitmap + check copy) decides
+    exactly as early_convergence_check (engine.py:331-348) -- on converged
+    labels, on labels after a partial run, and on single-cell perturbations
+    inside and outside the giant component's class."""
+    rng = np.random.default_rng(7)
+    ctx = _lib.Context(0)
+    ctx.set_option(_lib.CC_OPT_TILE_SHIFT, 12)
+    ctx.set_option(_lib.CC_OPT_CHECK_SHIFT, check_shift)
+    ctx.set_option(_lib.CC_OPT_ITEM_ROWS, 3000)
+    for n, e in (graphgen.rmat(15, 16, 3), graphgen.grid(300, 200, 0.55, 4),
+                 graphgen.forest(40, 5), spec.erdos_renyi(9000, 40000, 6)):
+        exp = oracle.rem_union_find(n, e)
+        engine.stage_graph(ctx, n, e, "l2_tiled_check")  # (for the partial-run labels below)
+        cases = [exp.copy()]
+        for _ in range(6):  # one cell moved to another valid value (<= itself)
+            lab = exp.copy()
+            x = int(rng.integers(1, n))
+            lab[x] = int(rng.integers(0, x))
+            cases.append(lab)
+        _lib.check(ctx.lib.cc_init_labels(ctx.handle))  # labels after one C-1 sweep
+        _lib.check(ctx.lib.cc_sweep(ctx.handle, 1, 0, 1, 0, None))
+        part = np.empty(n, dtype=np.int64)
+        _lib.check(ctx.lib.cc_read_labels(ctx.handle, part.ctypes.data, 8))
+        cases.append(part)
+        lab = np.arange(n, dtype=np.int64)  # identity: every non-loop edge disagrees
+        cases.append(lab)
+        for layout in ("l2_tiled_check", "chunk_sorted"):  # check copy / flat bitmap check
+            ctx.set_option(_lib.CC_OPT_FLAT_BITS, 1)
+            engine.stage_graph(ctx, n, e, layout)
+            for lab in cases:
+                lab = np.ascontiguousarray(lab, dtype=np.int64)
+                _lib.check(ctx.lib.cc_write_labels(ctx.handle, lab.ctypes.data, 8))
+                want = oracle.early_convergence_check(n, e, lab)
+                assert engine.loop_check(ctx) == want, (n, check_shift, layout)
+            # whole runs through the bitmap check, incl. the streamed one-shot path
             labels = np.empty(n, dtype=np.int64)
-            engine.run_staged(ctx, sched, labels_out=labels, count_changes=False,
-                              early_check=False)
-            assert np.array_equal(labels, exp), (n, sched)
-            assert engine.verify_staged(ctx) == 0
+            engine.run_staged(ctx, make_schedule("c2"), count_changes=False, labels_out=labels)
+            assert np.array_equal(labels, exp), (n, layout)
+        for count in (False, True):
+            labels = np.empty(n, dtype=np.int64)
+            _, st = engine.run_host(ctx, n, e, make_schedule("c2"), layout="chunk_sorted",
+                                    count_changes=count, labels_out=labels)
+            assert np.array_equal(labels, exp), (n, "run_host", count)
+            check_invariants(labels, st)
+        ctx.set_option(_lib.CC_OPT_FLAT_BITS, 2)
     ctx.close()
 
 
