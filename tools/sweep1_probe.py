@@ -24,13 +24,19 @@ def main():
     ap.add_argument("--layout", default="l2_tiled_check")
     ap.add_argument("--split", default="2")
     ap.add_argument("--ctas", default="0")
+    ap.add_argument("--seeds", default="1")
+    ap.add_argument("--scales", default=None)
     args = ap.parse_args()
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
     ctx = _lib.Context(0, stream.cuda_stream)
-    for split in [int(x) for x in args.split.split(",")]:
+    scales = [int(x) for x in (args.scales or str(args.scale)).split(",")]
+    combos = [(sc_, sd, sp) for sc_ in scales for sd in [int(x) for x in args.seeds.split(",")]
+              for sp in [int(x) for x in args.split.split(",")]]
+    for scale, seed, split in combos:
+        args.scale = scale
         ctx.set_option(_lib.CC_OPT_TILE_SPLIT, split)
-        n, m = graphgen.rmat_device(ctx, args.scale, 16, 1)
+        n, m = graphgen.rmat_device(ctx, args.scale, 16, seed)
         engine.apply_layout(ctx, args.layout)
         for ctas in [int(x) for x in args.ctas.split(",")]:
             ctx.set_option(_lib.CC_OPT_SWEEP_CTAS, ctas)
@@ -45,7 +51,8 @@ def main():
                                               sweep_times=False)
                     sweeps.append(st.sweeps_executed)
                     dev.append(st.device_seconds)
-                print(json.dumps({"scale": args.scale, "layout": args.layout, "split": split,
+                print(json.dumps({"scale": args.scale, "seed": seed, "layout": args.layout,
+                                  "split": split,
                                   "ctas": ctas, "shortcut": sc, "sweeps": sweeps,
                                   "ms": [round(x * 1e3, 2) for x in dev],
                                   "verify": engine.verify_staged(ctx)}), flush=True)
