@@ -444,6 +444,7 @@ def run_single(args, device):
     early = args.early_check == "on" or (args.early_check == "auto" and
                                          layout in ("hybrid", "l2_tiled", "l2_tiled_check"))
     hybrid = layout == "hybrid"
+    two_kernel = layout in ("hybrid", "l2_tiled_check")  # sweep 1 and later sweeps differ
     sched = make_schedule("c2", atomic=atomic)
     kw = dict(count_changes=False, early_check=early, first_scatter=args.first_scatter,
               host_loop=args.host_loop)
@@ -475,6 +476,13 @@ def run_single(args, device):
     check = 2 if early else 0  # edge-agreement + idempotence kernels
     if args.host_loop:  # iota + (sweep + shortcut + check) per sweep + compress
         launches = sum(2 + s.sweeps_executed * (1 + shortcut + check) for s in stats)
+    elif layout == "l2_tiled_check":
+        # per loop iteration: tiled sweep (guarded) + root pick + bitmap pass + bitmap
+        # sweep (guarded) + shortcut + control; the bitmap sweep that passes as the
+        # early check is one iteration more than the sweeps it books
+        per = 1 + 3 + shortcut + 1
+        launches = sum(3 + (s.sweeps_executed + (s.converged_by == "early-check")) * per
+                       for s in stats)
     else:  # loop_init + (guarded sweeps + shortcut + check + control) per sweep + compress + publish
         per = (2 if hybrid else 1) + shortcut + check + 1
         launches = sum(3 + s.sweeps_executed * per for s in stats)
@@ -493,7 +501,7 @@ def run_single(args, device):
     for _ in range(max(1, min(args.steps, 3))):
         _, st = engine.run_staged(ctx, sched, sweep_times=True, count_changes=False,
                                   early_check=False, host_loop=True)
-        if hybrid:
+        if two_kernel:
             rt1.append(st.sweep_seconds[0])
             rt2.extend(st.sweep_seconds[1:])
         else:
@@ -527,13 +535,23 @@ def run_single(args, device):
             "avg_launch_s": t_chk, "bytes_per_launch": b_sweep,
             "achieved": b_sweep / t_chk / 1e9, "frac": b_sweep / t_chk / 1e9 / peak,
             "traffic": traffic.get("check_dram_bytes_per_launch")}
-    if rt2:  # hybrid layout: later sweeps run the shared-memory slice kernel
+    if rt2 and hybrid:  # hybrid layout: later sweeps run the shared-memory slice kernel
         t2 = sum(rt2) / len(rt2)
         b2 = 6 * m + 4 * n  # compact bucketed copy: 4 B src + 2 B dst offset per row
         roofline["slice_kernel"] = {
             "kernel": "cck::k_sweep_slice (dst-bucketed copy, dst labels in shared memory)",
             "avg_launch_s": t2, "frac_of_B_sweep": b_sweep / t2 / 1e9 / peak,
             "streamed_bytes_per_launch": b2, "frac_streamed": b2 / t2 / 1e9 / peak}
+    elif rt2:  # layout 6: later sweeps are the bitmap sweep over the check copy
+        t2 = sum(rt2) / len(rt2)
+        b2 = 8 * m + n // 8 + 4 * n  # copy rows + bitmap + the vertex pass's label read
+        roofline["bitmap_sweep_kernel"] = {
+            "kernel": "k_pick_root + k_bits_idem + k_sweep_bits (dst-bucketed check copy, "
+                      "component bitmap; rows both of whose ends carry the root label are "
+                      "decided without label gathers)",
+            "avg_launch_s": t2, "frac_of_B_sweep": b_sweep / t2 / 1e9 / peak,
+            "streamed_bytes_per_launch": b2, "frac_streamed": b2 / t2 / 1e9 / peak,
+            "launch_ms": [round(t * 1e3, 4) for t in rt2]}
 
     # ---- the paper's comparison baseline on the same device and staged edges
     fsv = None

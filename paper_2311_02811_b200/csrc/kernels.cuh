@@ -171,8 +171,12 @@ __device__ __forceinline__ void lower_bcast(lab_t* T, const PeerSet& ps, lab_t t
     constexpr bool check = HOT && (SM == kStoreCheckPlain || SM == kStoreCheckRed);
     // a local value already <= z came from a lowering that was broadcast too
     if (check && __ldcg(T + t) <= z) return;
-    if (SM == kStoreRed || SM == kStoreCheckRed) atomicMin(T + t, z);
-    else T[t] = z;
+    // always an atomic min locally: peers red.min into this replica at any
+    // time, and a plain store could overwrite a smaller value a peer just
+    // wrote -- the replicas would then diverge for good (the peer's min was
+    // already sent, so nothing would bring it back).  Atomic min is one legal
+    // interleaving of the plain-store schedule (atomic=False) too.
+    atomicMin(T + t, z);
     for (int i = 0; i < ps.n; ++i) atomicMin(ps.p[i] + t, z);
 }
 

@@ -214,10 +214,20 @@ def stage_graph(ctx: _lib.Context, n: int, edges, layout: str = "auto") -> None:
     ctx.set_option(_lib.CC_OPT_STAGE_LAYOUT, 2 if layout in ("chunk_sorted", "hybrid") else 0)
     lib = ctx.lib
     if hasattr(edges, "data_ptr") and getattr(edges, "is_cuda", False):
-        e = edges.reshape(-1, 2).contiguous()
-        eb = e.element_size()
-        if eb not in (4, 8):
+        import torch
+        if edges.dtype not in (torch.int32, torch.int64):
             raise ValueError("edges must be int32 or int64")
+        e = edges.reshape(-1, 2)
+        if e.device.index != ctx.device:  # a tensor on another GPU: copy it over first
+            e = e.to(torch.device("cuda", ctx.device))
+        e = e.contiguous()
+        # the library stages on its own stream: wait for the work that produced
+        # the tensor (torch's current stream of its device, e.g. a
+        # torch.randint just before this call) before it reads the rows
+        torch.cuda.current_stream(e.device).synchronize()
+        if e.data_ptr() != edges.data_ptr():
+            torch.cuda.current_stream(edges.device).synchronize()
+        eb = e.element_size()
         _lib.check(lib.cc_stage_edges_device(ctx.handle, ctypes.c_void_p(e.data_ptr()), eb,
                                              e.shape[0], n))
         m = e.shape[0]
@@ -340,6 +350,25 @@ def loop_check(ctx: _lib.Context) -> bool:
     return bool(ok.value)
 
 
+def _frozen(edges) -> bool:
+    """True only for an edge array that cannot change behind our back: not
+    writeable itself and every array it views is read-only and owns its
+    memory (a read-only view of a writeable base, or a read-only memory map
+    of a file, can still change)."""
+    if not isinstance(edges, np.ndarray) or edges.flags.writeable:
+        return False
+    a = edges
+    while isinstance(a, np.ndarray) and a.base is not None:
+        a = a.base
+        if not isinstance(a, np.ndarray) or a.flags.writeable:
+            return False  # a foreign buffer (mmap, bytes, ...) or a writeable base
+    return True
+
+
+def _array_key(edges):
+    return (edges.ctypes.data, edges.shape, edges.strides, edges.dtype.str)
+
+
 def run_contour(g, schedule: Schedule, threads: int = 1, seed: Optional[int] = None, *,
                 device: int = 0, count_changes: bool = True, early_check: bool = True,
                 sweep_times: bool = True, layout: str = "auto",
@@ -386,12 +415,12 @@ def run_contour(g, schedule: Schedule, threads: int = 1, seed: Optional[int] = N
     # graph.py:82-83) cannot change between calls: the graph staged by the
     # previous call on this context stays resident and is reused -- as the
     # device layout for resident graphs (resolve_layout(resident=True)).
-    frozen = isinstance(edges, np.ndarray) and not edges.flags.writeable
+    frozen = _frozen(edges)
     if frozen and ctx.staged is not None and ctx.staged[0]() is edges and \
-            ctx.staged[1:3] == (n, layout):
+            ctx.staged[1:3] == (n, layout) and ctx.staged[4] == _array_key(edges):
         if ctx.staged[3]:  # upgrade the streamed layout once (+ the hybrid's bucketed copy)
             _lib.check(ctx.lib.cc_reorder_edges(ctx.handle, LAYOUTS[ctx.staged[3]]))
-            ctx.staged = ctx.staged[:3] + (None,)
+            ctx.staged = ctx.staged[:3] + (None,) + ctx.staged[4:]
         _, stats = run_staged(ctx, schedule, count_changes=count_changes,
                               early_check=early_check, sweep_times=sweep_times,
                               labels_out=labels, first_scatter=first_scatter,
@@ -416,7 +445,7 @@ def run_contour(g, schedule: Schedule, threads: int = 1, seed: Optional[int] = N
                 # only layouts reachable from the staged order in place
                 upgrade = want if (staged, want) in (("chunk_sorted", "hybrid"),) else None
             # a weak reference: the cache must not keep the caller's array alive
-            ctx.staged = (weakref.ref(edges), n, layout, upgrade)
+            ctx.staged = (weakref.ref(edges), n, layout, upgrade, _array_key(edges))
     return labels, stats
 
 

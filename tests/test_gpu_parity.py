@@ -918,6 +918,11 @@ def test_frozen_edges_stay_resident():
     w = np.array(e)  # writeable copy: never cached
     assert np.array_equal(run_contour((n, w), make_schedule("cm"))[0], exp)
     assert ctx.staged is None
+    base = np.array(e)  # a read-only VIEW of a writeable base can still change: never cached
+    v = base[:]
+    v.flags.writeable = False
+    assert np.array_equal(run_contour((n, v), make_schedule("c2"))[0], exp)
+    assert ctx.staged is None
     import gc
     e3 = np.array(e)
     e3.flags.writeable = False
@@ -925,6 +930,22 @@ def test_frozen_edges_stay_resident():
     del e3
     gc.collect()
     assert ctx.staged[0]() is None  # the cache holds no reference to a dropped array
+
+
+def test_cuda_tensor_edges_fresh_from_another_stream():
+    """Edges produced on the device by torch right before the call (on torch's
+    current stream, which the library's own stream does not follow) are
+    staged only after that work is done."""
+    import torch
+    n = 1 << 20
+    for i in range(3):
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            e = torch.randint(0, n, (1 << 22, 2), device="cuda", dtype=torch.int64)
+            e[:, 1] = (e[:, 0] * 7 + 3) % n  # more work queued behind the draw
+            labels, st = run_contour((n, e), make_schedule("c2"))
+        exp = oracle.rem_union_find(n, e.cpu().numpy())
+        assert np.array_equal(labels, exp), i
 
 
 def test_concurrent_callers_reentrant():
