@@ -202,6 +202,17 @@ int cc_set_option(cc_ctx* ctx, int option, int64_t value);
  * labels[n] = min(labels[n], wrote ? 0 : 1).  Clears the flag. */
 int cc_fold_flag(cc_ctx* ctx, int first);
 int cc_compress(cc_ctx* ctx, int* rounds_out);
+/* Deterministic multi-GPU synchronous sweeps (last bullet),
+ * replacing engine.py:288-291,309-311 across devices: cc_sync_sweep copies
+ * labels -> shadow and lowers the shadow from this context's edges (read the
+ * labels, atomic min into the shadow); the caller all-reduces the n shadow
+ * entries with MIN over all ranks (cc_shadow_device gives the buffer, n+1
+ * uint32); cc_sync_commit then counts the cells that changed and copies the
+ * shadow into the labels.  Every sweep equals the single-device synchronous
+ * sweep, so changed_per_sweep equals the reference's. */
+int cc_sync_sweep(cc_ctx* ctx, int order, int* wrote_out);
+int cc_sync_commit(cc_ctx* ctx, int64_t* changed_out);
+int cc_shadow_device(cc_ctx* ctx, uint32_t** shadow_dev);
 /* `passes` pointer-jumping passes L[v] = L[L[v]] without reading back (the
  * between-sweep shortcut of CC_OPT_SHORTCUT for drivers using cc_sweep). */
 int cc_shortcut(cc_ctx* ctx, int passes);

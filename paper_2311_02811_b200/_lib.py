@@ -74,6 +74,9 @@ SIGNATURES = {
     "cc_reorder_edges": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
     "cc_set_option": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int64]),
     "cc_fold_flag": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
+    "cc_sync_sweep": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.POINTER(ctypes.c_int)]),
+    "cc_sync_commit": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_int64)]),
+    "cc_shadow_device": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_void_p)]),
     "cc_compress": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_int)]),
     "cc_shortcut": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
     "cc_early_check": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_int)]),

@@ -243,6 +243,57 @@ int cc_sweep(cc_ctx* c, int order, int sync, int atomic, int first, int* wrote_o
     return CC_OK;
 }
 
+// Synchronous sweep split in two for the multi-GPU sync mode (SURVEY 8(e)
+// last bullet): phase 1 lowers a shadow copy of the labels from this
+// context's edge shard (read L, atomic min into the shadow); the caller then
+// all-reduces the shadows with MIN across ranks -- min is associative, so
+// the result is the single-device synchronous sweep's shadow exactly -- and
+// phase 2 commits it (count cells changed, L = shadow; engine.py:309-311).
+int cc_sync_sweep(cc_ctx* c, int order, int* wrote_out) {
+    NvtxRange nvtx_("cc_sync_sweep");
+    if (!c) return fail(CC_EINVAL, "null context");
+    if (order < 1) return fail(CC_EINVAL, "operator order must be >= 1");
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard g(c->device);
+    CC_TRY(ensure_aux(c, true, false));
+    if (c->n > 0)
+        CUDA_TRY(cudaMemcpyAsync(c->shadow, c->labels, sizeof(lab_t) * c->n,
+                                 cudaMemcpyDeviceToDevice, c->stream));
+    CUDA_TRY(cudaMemsetAsync(c->dflags + kFlagWrote, 0, sizeof(int), c->stream));
+    if (c->m > 0) CC_TRY(launch_order(c, c->labels, c->shadow, order, cck::kStoreCheckAllRed));
+    if (wrote_out) {
+        CC_TRY(read_flags(c));
+        *wrote_out = c->hflags[kFlagWrote] != 0;
+    }
+    return CC_OK;
+}
+
+int cc_sync_commit(cc_ctx* c, int64_t* changed_out) {
+    if (!c) return fail(CC_EINVAL, "null context");
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard g(c->device);
+    CC_TRY(ensure_aux(c, true, false));
+    CUDA_TRY(cudaMemsetAsync(c->dcount, 0, sizeof(unsigned long long), c->stream));
+    CUDA_TRY(cudaMemsetAsync(c->dflags + kFlagWrote, 0, sizeof(int), c->stream));
+    if (c->n > 0) {
+        k_commit<<<grid_for(c, c->n), kThreads, 0, c->stream>>>(c->labels, c->shadow, c->n,
+                                                                c->dcount, c->dflags);
+        CUDA_TRY(cudaGetLastError());
+    }
+    CC_TRY(read_flags(c));
+    if (changed_out) *changed_out = (int64_t)*c->hcount;
+    return CC_OK;
+}
+
+int cc_shadow_device(cc_ctx* c, uint32_t** out) {
+    if (!c || !out) return fail(CC_EINVAL, "null argument");
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard g(c->device);
+    CC_TRY(ensure_aux(c, true, false));
+    *out = c->shadow;
+    return CC_OK;
+}
+
 int cc_fold_flag(cc_ctx* c, int first) {
     if (!c) return fail(CC_EINVAL, "null context");
     std::lock_guard<std::mutex> lk(c->mu);

@@ -26,6 +26,16 @@ import ctypes
 from . import _lib, graphgen
 
 
+def _device_view(ptr: int, count: int, device: int):
+    """A torch int32 view (no copy) of `count` entries of a device buffer."""
+    import torch
+
+    class _View:
+        __cuda_array_interface__ = {"shape": (count,), "typestr": "<i4", "data": (ptr, False),
+                                    "version": 3}
+    return torch.as_tensor(_View(), device=f"cuda:{device}")
+
+
 class CudaShard:
     """A rank's edge shard + label replica on its GPU (libcontour.so)."""
 
@@ -58,6 +68,29 @@ class CudaShard:
         r = ctypes.c_int(0)
         _lib.check(self.ctx.lib.cc_compress(self.ctx.handle, ctypes.byref(r)))
         return r.value
+
+    # ---- synchronous mode (SyncShardedContour)
+    def sync_sweep(self, order: int) -> None:
+        _lib.check(self.ctx.lib.cc_sync_sweep(self.ctx.handle, order, None))
+
+    def shadow(self):
+        """The context's shadow labels (n entries) as a torch view, for the
+        MIN all-reduce between the two halves of a synchronous sweep."""
+        ptr = ctypes.c_void_p(0)
+        _lib.check(self.ctx.lib.cc_shadow_device(self.ctx.handle, ctypes.byref(ptr)))
+        return _device_view(ptr.value, self.n, self.ctx.device)
+
+    def commit(self) -> int:
+        c = ctypes.c_int64(0)
+        _lib.check(self.ctx.lib.cc_sync_commit(self.ctx.handle, ctypes.byref(c)))
+        return c.value
+
+    def check(self) -> bool:
+        """early_convergence_check on this shard's edges (and every label's
+        idempotence) -- all ranks' results AND-ed give the whole graph's."""
+        ok = ctypes.c_int(0)
+        _lib.check(self.ctx.lib.cc_early_check(self.ctx.handle, ctypes.byref(ok)))
+        return bool(ok.value)
 
 
 class PeerShard:
@@ -359,16 +392,67 @@ class ShardedContour(_HostIO):
         return rounds
 
 
+class SyncShardedContour:
+    """Deterministic synchronous mode across ranks (last bullet):
+    every sweep each rank lowers a shadow of the (identical) label replicas
+    from its edge shard, the shadows are all-reduced with MIN -- min is
+    associative, so the result is exactly the single-device synchronous
+    sweep's shadow -- and committed; the change count is then the
+    reference's (engine.py:288-291,309-311), identical on every rank.  The
+    early check (engine.py:318-320) runs per shard and is AND-ed across
+    ranks (a MIN all-reduce of the 0/1 results).  ``run`` returns
+    (sweeps_executed, sweeps_until_stable, changed_per_sweep, converged_by)."""
+
+    def __init__(self, shard, n: int, m_total: int, *, order_for=lambda k: 2,
+                 early_check: bool = True, allreduce=None, group=None, cap=None):
+        self.shard = shard
+        self.n = n
+        self.m_total = m_total
+        self.order_for = order_for
+        self.early_check = early_check
+        self.allreduce = allreduce or nccl_allreduce_min(group)
+        self.cap = n + 2 if cap is None else cap
+
+    def run(self):
+        import torch
+        shard = self.shard
+        shard.init()
+        flag = torch.zeros(1, dtype=torch.int32, device=shard.labels.device)
+        sweep, until, changed, by = 0, 0, [], "change-flag"
+        while True:
+            sweep += 1
+            if sweep > self.cap:
+                from .errors import IterationCapExceeded
+                raise IterationCapExceeded(f"no convergence after {self.cap} sweeps")
+            shard.sync_sweep(self.order_for(sweep))
+            self.allreduce(shard.shadow())
+            c = shard.commit()
+            changed.append(int(c))
+            if c == 0:
+                break
+            until = sweep
+            if self.early_check:
+                flag.fill_(int(shard.check()))
+                self.allreduce(flag)
+                if int(flag.item()) == 1:
+                    by = "early-check"
+                    break
+        shard.compress()
+        return sweep, until, changed, by
+
+
 def run_in_process(n: int, edges, schedule, devices, cadence: int = 1, layout: str = "auto",
-                   cap=None):
+                   cap=None, early_check: bool = True):
     """``run_contour(..., devices=[...])``: the edge-sharded driver inside one
     process -- one host thread per listed device (a device may repeat: two
     shards on one GPU), each with its own context, stream and label replica;
     the MIN exchange is a host barrier + element-wise minimum of the replicas
-    (gathered to the first device, copied back).  Asynchronous schedules only
-    (a sweep of a shard is an asynchronous sweep of the whole edge list once
-    the replicas are merged).  Returns (int64 labels, sweeps executed,
-    exchange rounds)."""
+    (gathered to the first device, copied back).  Asynchronous schedules:
+    ShardedContour (a sweep of a shard is an asynchronous sweep of the whole
+    edge list once the replicas are merged); returns (int64 labels, sweeps
+    executed, exchange rounds).  Synchronous schedules: SyncShardedContour
+    (per-sweep results identical to one device); returns (int64 labels,
+    (sweeps, until_stable, changed_per_sweep, converged_by))."""
     import threading
 
     import numpy as np
@@ -376,8 +460,6 @@ def run_in_process(n: int, edges, schedule, devices, cadence: int = 1, layout: s
 
     from .engine import _host_edges, stage_graph
 
-    if schedule.sync:
-        raise ValueError("multi-device runs need an asynchronous schedule (sync=False)")
     devices = [int(d) for d in devices]
     world = len(devices)
     e = edges if (hasattr(edges, "data_ptr") and getattr(edges, "is_cuda", False)) \
@@ -412,8 +494,13 @@ def run_in_process(n: int, edges, schedule, devices, cadence: int = 1, layout: s
             lo, hi = shard_rows(m, r, world)
             stage_graph(ctx, n, e[lo:hi], layout)
             shard = CudaShard(ctx, n, atomic=schedule.atomic)
-            runner = ShardedContour(shard, n, m, order_for=schedule.order_for, cadence=cadence,
-                                    allreduce=allreduce_for(r), cap=cap)
+            if schedule.sync:
+                runner = SyncShardedContour(shard, n, m, order_for=schedule.order_for,
+                                            early_check=early_check,
+                                            allreduce=allreduce_for(r), cap=cap)
+            else:
+                runner = ShardedContour(shard, n, m, order_for=schedule.order_for,
+                                        cadence=cadence, allreduce=allreduce_for(r), cap=cap)
             rounds = runner.run()
             torch.cuda.synchronize(dev)
             counts[r] = rounds
@@ -433,4 +520,6 @@ def run_in_process(n: int, edges, schedule, devices, cadence: int = 1, layout: s
         real = [x for x in errors if not isinstance(x, threading.BrokenBarrierError)]
         raise (real or errors)[0]
     rounds = counts[0]
+    if schedule.sync:  # (sweeps, until_stable, changed_per_sweep, converged_by)
+        return out[0], rounds
     return out[0], rounds * max(1, int(cadence)), rounds

@@ -388,9 +388,12 @@ def run_contour(g, schedule: Schedule, threads: int = 1, seed: Optional[int] = N
     edge rows over those GPUs inside this process -- label replicas merged by
     an element-wise MIN every ``cadence`` local sweeps (distributed.py; one
     process per GPU with torch.distributed is the multi-node-ready form).
-    Asynchronous schedules only; ``changed_per_sweep`` holds -1 for the
-    sweeps of changing rounds and 0 for the last round's (with ``cadence`` k
-    > 1 the last round has k no-write sweeps, so executed = until_stable + k).
+    Asynchronous schedules: ``changed_per_sweep`` holds -1 for the sweeps of
+    changing rounds and 0 for the last round's (with ``cadence`` k > 1 the
+    last round has k no-write sweeps, so executed = until_stable + k).
+    Synchronous schedules shard deterministically (shadow lowering per
+    shard, MIN all-reduce of the shadows, commit): every IterationStats
+    field equals the single-device run's.
     """
     if threads < 1:
         raise ValueError("threads must be >= 1")
@@ -399,6 +402,12 @@ def run_contour(g, schedule: Schedule, threads: int = 1, seed: Optional[int] = N
         raise ValueError("vertex count must be non-negative")
     if devices is not None and len(devices) > 1:
         from .distributed import run_in_process
+        if schedule.sync:  # deterministic: the same per-sweep results as one device
+            labels, (k, until, changed, by) = run_in_process(
+                n, edges, schedule, devices, layout=layout, early_check=early_check)
+            return labels, IterationStats(
+                sweeps_executed=k, sweeps_until_stable=until, changed_per_sweep=changed,
+                converged_by=by, sweep_seconds=[0.0] * k, device_seconds=0.0)
         labels, sweeps, rounds = run_in_process(n, edges, schedule, devices, cadence=cadence,
                                                 layout=layout)
         k = max(1, int(cadence))

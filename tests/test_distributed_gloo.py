@@ -14,7 +14,7 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 from oracle import gen, oracle
-from paper_2311_02811_b200.distributed import ShardedContour, shard_rows
+from paper_2311_02811_b200.distributed import ShardedContour, SyncShardedContour, shard_rows
 
 
 class OracleShard:
@@ -42,6 +42,28 @@ class OracleShard:
         f = 0 if self.wrote else 1
         self.labels[self.n] = f if first else min(int(self.labels[self.n]), f)
         self.wrote = False
+
+    # synchronous mode (SyncShardedContour): lower a shadow from this shard
+    def sync_sweep(self, order):
+        lab = self.labels[: self.n].numpy().astype(np.int64)
+        sh = lab.copy()
+        L = oracle.lib()
+        L.oc_sweep_edges(lab.ctypes.data_as(oracle._I64P), sh.ctypes.data_as(oracle._I64P),
+                         self.edges.ctypes.data, 8, 0, self.edges.shape[0], 0, order, 1)
+        self._shadow = torch.from_numpy(sh.astype(np.int32))
+
+    def shadow(self):
+        return self._shadow
+
+    def commit(self):
+        lab = self.labels[: self.n]
+        changed = int((self._shadow != lab).sum())
+        lab.copy_(self._shadow)
+        return changed
+
+    def check(self):
+        return oracle.early_convergence_check(self.n, self.edges,
+                                              self.labels[: self.n].numpy().astype(np.int64))
 
     def compress(self):
         lab = self.labels[: self.n].numpy()
@@ -100,6 +122,47 @@ def test_two_rank_gloo_matches_union_find(graph, cadence):
     assert len(rounds) == 1  # every rank agrees when to stop
     for _, labels, _ in results:
         assert np.array_equal(labels, exp)
+
+
+def _sync_worker(rank, world, port, cfg, variant, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        n, e = cfg
+        lo, hi = shard_rows(e.shape[0], rank, world)
+        runner = SyncShardedContour(OracleShard(n, e[lo:hi]), n, e.shape[0],
+                                    order_for=lambda k: oracle.order_for(variant, k, 8))
+        stats = runner.run()
+        q.put((rank, runner.shard.labels[:n].numpy().astype(np.int64), stats))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("graph,variant,world", [("rmat", "C-2", 2), ("grid", "C-2", 3),
+                                                 ("grid", "C-1", 2), ("forest", "C-m", 2)])
+def test_sync_mode_shards_reproduce_single_device_counts(graph, variant, world):
+    """Synchronous sweeps sharded over ranks (shadow per shard, MIN all-reduce
+    of the shadows, commit) give per-sweep results identical to the
+    one-device synchronous run -- the reference's."""
+    cfg = {"rmat": gen.rmat(10, 8, 3), "grid": gen.grid(40, 40, 0.55, 2),
+           "forest": gen.forest(6, 4)}[graph]
+    n, e = cfg
+    exp_labels, exp = oracle.run_contour(n, e, variant, high_order=8, sync=True)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_sync_worker, args=(r, world, port, cfg, variant, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    results = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for _, labels, (k, until, changed, by) in results:
+        assert np.array_equal(labels, exp_labels)
+        assert (k, until, changed, by) == (exp.sweeps_executed, exp.sweeps_until_stable,
+                                           list(exp.changed_per_sweep), exp.converged_by)
 
 
 def test_shard_rows_cover_and_align():

@@ -843,8 +843,57 @@ def test_run_contour_devices_in_process(cadence):
                 assert np.array_equal(labels, exp), (n, devs, variant)
                 assert st.sweeps_executed == st.sweeps_until_stable + cadence
                 assert st.changed_per_sweep[-1] == 0
-    with pytest.raises(ValueError):
-        run_contour((n, e), make_schedule("c2", sync=True), devices=[0, 0])
+    # synchronous schedules shard deterministically: stats equal one device's
+    for n, e in (graphgen.rmat(14, 16, 5), graphgen.grid(150, 170, 0.55, 3)):
+        for variant in ("C-2", "C-Syn", "C-1", "C-m"):
+            sched = make_schedule(variant, 6, sync=True)
+            lab1, st1 = run_contour((n, e), sched)
+            for devs in ([0, 0], [0, 0, 0]):
+                labels, st = run_contour((n, e), sched, devices=devs)
+                assert np.array_equal(labels, lab1), (devs, variant)
+                assert (st.sweeps_executed, st.sweeps_until_stable, st.changed_per_sweep,
+                        st.converged_by) == (st1.sweeps_executed, st1.sweeps_until_stable,
+                                             st1.changed_per_sweep, st1.converged_by)
+
+
+def _gpus():
+    import torch
+    return torch.cuda.device_count()
+
+
+@pytest.mark.skipif("_gpus() < 2")
+def test_two_distinct_gpus_in_process_and_bench():
+    """run_contour(devices=[0, 1]) on two real GPUs (the per-device smem
+    opt-in / occupancy caches, peer copies of the exchange) and the bench's
+    2-rank launch; skipped on a one-GPU box."""
+    import json
+    import subprocess
+    import sys
+    n, e = graphgen.rmat(18, 16, 2)
+    exp = oracle.rem_union_find(n, e)
+    for sched in (make_schedule("c2"), make_schedule("c2", sync=True)):
+        labels, st = run_contour((n, e), sched, devices=[0, 1])
+        assert np.array_equal(labels, exp)
+    out = subprocess.run([sys.executable, "bench.py", "--gpus", "2", "--config", "rmat22",
+                          "--steps", "2", "--warmup", "1", "--no-cpu-baseline", "--no-e2e"],
+                         capture_output=True, text=True, timeout=900, check=True).stdout
+    line = json.loads([x for x in out.splitlines() if x.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["verified"]
+
+
+def test_bench_two_ranks_share_one_gpu():
+    """bench.py --gpus 2 without torchrun starts 2 ranks itself (here sharing
+    cuda:0 -- the plumbing check: gloo for the host exchange) and rank 0
+    prints one line with n_gpus = 2 and verified labels."""
+    import json
+    import subprocess
+    import sys
+    out = subprocess.run([sys.executable, "bench.py", "--gpus", "2", "--config", "rmat22",
+                          "--steps", "2", "--warmup", "1", "--no-cpu-baseline"],
+                         capture_output=True, text=True, timeout=900)
+    assert out.returncode == 0, out.stderr[-3000:]
+    line = json.loads([x for x in out.stdout.splitlines() if x.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["verified"] and line["e2e"]["value"] > 0
 
 
 def test_pinned_and_pageable_host_buffers():
