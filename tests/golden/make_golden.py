@@ -219,7 +219,42 @@ def ingest_cases():
     return out
 
 
+def forest_diag_cases(rng):
+    """forest_diagnostics (engine.py:373-405) on pointer graphs: the
+    reference's own examples (test_engine.py:281-309), converged run labels,
+    random parent forests (labels[x] <= x), deep chains, and the two error
+    cases (a cycle -> IterationCapExceeded, out of range -> ValueError)."""
+    arrays = [[0, 0, 1, 2], [0, 1, 2], [0, 0, 0, 1], [0, 0, 1, 0, 3], [], [0],
+              list(range(0, 1)) + list(range(0, 29)), [1, 0], [0, 5], [0, -1]]
+    for n in (5, 17, 60, 200, 1000):
+        for _ in range(4):
+            arrays.append([int(rng.integers(0, x + 1)) for x in range(n)])
+    for n, e in (gen.rmat(9, 8, 2), gen.grid(12, 12, 0.55, 3), gen.forest(5, 2)):
+        ns = SimpleNamespace(n=n, m=e.shape[0], edges=e)
+        lab, _ = ref.run_contour(ns, ref.make_schedule("C-2", sync=True), threads=1)
+        arrays.append(lab.tolist())
+    out = []
+    for arr in arrays:
+        try:
+            d = ref.forest_diagnostics(np.asarray(arr, dtype=np.int64))
+            res = {"roots": d.roots.tolist(),
+                   "heights": [[k, v] for k, v in sorted(d.heights.items())],
+                   "class_sizes": [[k, v] for k, v in sorted(d.class_sizes.items())],
+                   "merged_min_count": d.merged_min_count}
+        except Exception as exc:  # noqa: BLE001 - recording the reference's error
+            res = {"error": type(exc).__name__}
+        out.append({"labels": arr, "result": res})
+    return out
+
+
 def main():
+    if "--forest-diag" in sys.argv:  # only the forest_diagnostics fixture (forest_diag.json)
+        with open(os.path.join(HERE, "forest_diag.json"), "w") as fh:
+            json.dump({"generator": "tests/golden/make_golden.py --forest-diag",
+                       "reference": "minmapcc " + ref.__version__,
+                       "cases": forest_diag_cases(np.random.default_rng(405))}, fh,
+                      separators=(",", ":"))
+        return
     rng = np.random.default_rng(20261020)
     data = {"generator": "tests/golden/make_golden.py", "reference": "minmapcc " + ref.__version__,
             "mm_order": mm_cases(rng), "graphs": small_graphs(rng), "configs": configs(),

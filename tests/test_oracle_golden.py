@@ -124,3 +124,33 @@ def test_normalize_and_stars():
         oracle.normalize_labels(np.array([0, 5]))
     assert oracle.is_star_forest(np.array([0, 0, 2, 0]))
     assert not oracle.is_star_forest(np.array([0, 0, 1]))
+
+
+def test_forest_diagnostics_equal_reference():
+    """engine.forest_diagnostics (pointer doubling) equals the reference's
+    forest_diagnostics (engine.py:373-405) on the committed fixture, errors
+    included (cycle -> IterationCapExceeded, out of range -> ValueError)."""
+    import json
+    import os
+
+    import numpy as np
+
+    from paper_2311_02811_b200 import IterationCapExceeded
+    from paper_2311_02811_b200.engine import forest_diagnostics
+    with open(os.path.join(os.path.dirname(__file__), "golden", "forest_diag.json")) as fh:
+        cases = json.load(fh)["cases"]
+    errors = {"IterationCapExceeded": IterationCapExceeded, "ValueError": ValueError}
+    for case in cases:
+        lab = np.asarray(case["labels"], dtype=np.int64)
+        want = case["result"]
+        if "error" in want:
+            try:
+                forest_diagnostics(lab)
+            except errors[want["error"]]:
+                continue
+            raise AssertionError(f"expected {want['error']} for {case['labels'][:10]}")
+        d = forest_diagnostics(lab)
+        assert d.roots.tolist() == want["roots"]
+        assert sorted(d.heights.items()) == [tuple(x) for x in want["heights"]]
+        assert sorted(d.class_sizes.items()) == [tuple(x) for x in want["class_sizes"]]
+        assert d.merged_min_count == want["merged_min_count"]
