@@ -193,6 +193,11 @@ int cc_reorder_edges(cc_ctx* ctx, int mode);
 #define CC_OPT_FLAT_BITS 18        /* early check on flat rows with the component bitmap:
                                       0 never, 1 always, 2 auto (default: labels beyond L2
                                       and m >= 4n, e.g. one-shot RMAT-28) */
+#define CC_OPT_HOST_SUB 19         /* pageable host edges: rows narrowed per pinned sub-chunk
+                                      (default 2^20; small enough to stay in the host's LLC
+                                      until the copy engine reads it) */
+#define CC_OPT_HOST_NT 20          /* 1: streaming (non-temporal) stores into the pinned
+                                      sub-chunks (default 0: cached stores) */
 #define CC_OPT_STAGE_LAYOUT 4     /* layout applied while staging: 0 input order (default),
                                       2 chunk-sorted, each chunk sorted as soon as it lands,
                                       overlapped with the next chunk's host->device copy */

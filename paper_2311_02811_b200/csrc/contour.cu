@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 #include <cub/cub.cuh>
 #include <emmintrin.h>
+#include <immintrin.h>
 #include <stdarg.h>
 #include <stdio.h>
 #include <string.h>
@@ -132,7 +133,10 @@ void cc_destroy(cc_ctx* c) {
     cudaFree(c->bdst16);
     cudaFree(c->bits);
     cudaFree(c->dr0);
-    for (int b = 0; b < 2; ++b) cudaFreeHost(c->hstage[b]);
+    for (int b = 0; b < kNSub; ++b) {
+        cudaFreeHost(c->hsub[b]);
+        if (c->subdone[b]) cudaEventDestroy(c->subdone[b]);
+    }
     cudaFreeHost(c->hlab);
     if (c->own_labels) cudaFree(c->labels);
     cudaFree(c->wide);
@@ -903,6 +907,14 @@ int cc_set_option(cc_ctx* c, int option, int64_t value) {
             if (value < 0 || value > 2) return fail(CC_EINVAL, "flat bits must be 0, 1 or 2");
             c->flat_bits = (int)value;
             c->loop_key.m = -1;
+            return CC_OK;
+        case CC_OPT_HOST_SUB:
+            if (value < 4096 || value > ((int64_t)1 << 26))
+                return fail(CC_EINVAL, "host sub-chunk must be in [4096, 2^26] rows");
+            c->host_sub = value & ~(int64_t)15;
+            return CC_OK;
+        case CC_OPT_HOST_NT:
+            c->host_nt = value != 0;
             return CC_OK;
         case CC_OPT_CHECK_SHIFT:
             if (value < 7 || value > 20)

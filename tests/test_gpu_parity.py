@@ -776,10 +776,15 @@ def test_bitmap_check_equals_oracle_early_check(check_shift):
                 _lib.check(ctx.lib.cc_write_labels(ctx.handle, lab.ctypes.data, 8))
                 want = oracle.early_convergence_check(n, e, lab)
                 assert engine.loop_check(ctx) == want, (n, check_shift, layout)
-            # whole runs through the bitmap check, incl. the streamed one-shot path
-            labels = np.empty(n, dtype=np.int64)
-            engine.run_staged(ctx, make_schedule("c2"), count_changes=False, labels_out=labels)
-            assert np.array_equal(labels, exp), (n, layout)
+            # whole runs through the bitmap check / bitmap sweeps (graph loop and
+            # counted host loop), incl. the streamed one-shot path below
+            for count in (False, True):
+                for early in (False, True):
+                    labels = np.empty(n, dtype=np.int64)
+                    _, st = engine.run_staged(ctx, make_schedule("c2"), count_changes=count,
+                                              early_check=early, labels_out=labels)
+                    assert np.array_equal(labels, exp), (n, layout, count, early)
+                    check_invariants(labels, st)
         for count in (False, True):
             labels = np.empty(n, dtype=np.int64)
             _, st = engine.run_host(ctx, n, e, make_schedule("c2"), layout="chunk_sorted",
@@ -935,6 +940,28 @@ def test_pinned_and_pageable_host_buffers():
                 np.array([[0, -3]], dtype=np.int32)):
         with pytest.raises(ValueError):
             run_contour((4, arr), make_schedule("c2"))
+
+
+def test_pageable_narrowing_range_checks_in_the_vector_body():
+    """Pageable host edges are narrowed by the context's threads (AVX-512 when
+    the host has it): out-of-range endpoints anywhere in a large array -- not
+    only in the scalar head/tail -- still raise ValueError, valid ones stage
+    exactly (int64 and int32)."""
+    n, e = graphgen.rmat(16, 16, 4)
+    exp = oracle.rem_union_find(n, e)
+    for dt in (np.int64, np.int32):
+        a = np.ascontiguousarray(e, dtype=dt)
+        labels, _ = run_contour((n, a), make_schedule("c2"))
+        assert np.array_equal(labels, exp), dt
+        for pos, val in ((123457, -1), (777777, n), (1000003, -(1 << 30))):
+            b = a.copy()
+            b.flat[pos] = val
+            with pytest.raises(ValueError):
+                run_contour((n, b), make_schedule("c2"))
+    b = np.ascontiguousarray(e, dtype=np.int64)
+    b.flat[555555] = 1 << 33  # beyond uint32: must not wrap to a valid ID
+    with pytest.raises(ValueError):
+        run_contour((n, b), make_schedule("c2"))
 
 
 def test_frozen_edges_stay_resident():

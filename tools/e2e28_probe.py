@@ -24,6 +24,8 @@ def main():
     ap.add_argument("--scale", type=int, default=28)
     ap.add_argument("--reps", type=int, default=2)
     ap.add_argument("--cases", default="stage_input,stage_chunk,auto,chunk_sorted,auto_nocount,chunk_nocount")
+    ap.add_argument("--host-sub", default="0", help="comma list of CC_OPT_HOST_SUB (0: default)")
+    ap.add_argument("--host-nt", default="0", help="comma list of CC_OPT_HOST_NT")
     args = ap.parse_args()
     ctx = _lib.Context(0)
     n, m = graphgen.rmat_device(ctx, args.scale, 16, 1)
@@ -39,12 +41,27 @@ def main():
     ctx.close()
     del ctx
     sched = make_schedule("c2")
-    for case in args.cases.split(","):
+    combos = [(case, hs, nt) for hs in args.host_sub.split(",") for nt in args.host_nt.split(",")
+              for case in args.cases.split(",")]
+    for case, hs, nt in combos:
+        c0 = engine._context(0)
+        if int(hs):
+            c0.set_option(_lib.CC_OPT_HOST_SUB, int(hs))
+        c0.set_option(_lib.CC_OPT_HOST_NT, int(nt))
         ts, extra = [], {}
         for _ in range(args.reps):
             c2 = engine._context(0)
             t = time.perf_counter()
-            if case == "stage_input":
+            if case in ("host_nolabels", "host_labels", "host_labels32"):
+                out = None
+                if case == "host_labels":
+                    out = np.empty(n, dtype=np.int64)
+                elif case == "host_labels32":
+                    out = np.empty(n, dtype=np.int32)
+                t = time.perf_counter()
+                _, st = engine.run_host(c2, n, e, sched, count_changes=False, labels_out=out)
+                extra = {"sweeps": st.sweeps_executed, "device_s": round(st.device_seconds, 3)}
+            elif case == "stage_input":
                 engine.stage_graph(c2, n, e, "input")
             elif case == "stage_chunk":
                 engine.stage_graph(c2, n, e, "chunk_sorted")
@@ -59,7 +76,8 @@ def main():
                 del lab
             torch.cuda.synchronize()
             ts.append(round(time.perf_counter() - t, 3))
-        print(json.dumps({"case": case, "s": ts, **extra}), flush=True)
+        print(json.dumps({"case": case, "host_sub": int(hs), "host_nt": int(nt), "s": ts,
+                          **extra}), flush=True)
 
 
 if __name__ == "__main__":
