@@ -198,6 +198,9 @@ int cc_reorder_edges(cc_ctx* ctx, int mode);
                                       until the copy engine reads it) */
 #define CC_OPT_HOST_NT 20          /* 1: streaming (non-temporal) stores into the pinned
                                       sub-chunks (default 0: cached stores) */
+#define CC_OPT_CHECK_PACK 21       /* layout 6: 1 (default) = 6-byte check-copy rows (uint32
+                                      src + high offset bits, uint16 low offset bits) when
+                                      log2(n) + shift - 16 <= 32; 0 = 8-byte rows */
 #define CC_OPT_STAGE_LAYOUT 4     /* layout applied while staging: 0 input order (default),
                                       2 chunk-sorted, each chunk sorted as soon as it lands,
                                       overlapped with the next chunk's host->device copy */

@@ -30,6 +30,7 @@ CC_OPT_CHECK_SHIFT = 17
 CC_OPT_FLAT_BITS = 18
 CC_OPT_HOST_SUB = 19
 CC_OPT_HOST_NT = 20
+CC_OPT_CHECK_PACK = 21
 STORE_PLAIN, STORE_RED, STORE_CHECK_PLAIN, STORE_CHECK_RED = 0, 1, 2, 3
 
 _I64P = ctypes.POINTER(ctypes.c_int64)

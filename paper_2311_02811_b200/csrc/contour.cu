@@ -908,6 +908,9 @@ int cc_set_option(cc_ctx* c, int option, int64_t value) {
             c->flat_bits = (int)value;
             c->loop_key.m = -1;
             return CC_OK;
+        case CC_OPT_CHECK_PACK:
+            c->check_pack = value != 0;
+            return CC_OK;
         case CC_OPT_HOST_SUB:
             if (value < 4096 || value > ((int64_t)1 << 26))
                 return fail(CC_EINVAL, "host sub-chunk must be in [4096, 2^26] rows");

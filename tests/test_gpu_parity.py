@@ -740,6 +740,39 @@ def test_l2_tiled_layout_exact(tile_shift, layout):
     ctx.close()
 
 
+@pytest.mark.parametrize("check_shift,pack", [(16, 1), (17, 1), (17, 0)])
+def test_packed_check_copy_exact(check_shift, pack):
+    """The 6-byte packed check copy (src | high offset bits, uint16 low bits;
+    used when log2(n) + check_shift - 16 <= 32, e.g. RMAT-28) against the
+    oracle: the bitmap check's verdicts and whole runs through the bitmap
+    sweep."""
+    rng = np.random.default_rng(17)
+    ctx = _lib.Context(0)
+    ctx.set_option(_lib.CC_OPT_TILE_SHIFT, 18)
+    ctx.set_option(_lib.CC_OPT_CHECK_SHIFT, check_shift)
+    ctx.set_option(_lib.CC_OPT_CHECK_PACK, pack)
+    ctx.set_option(_lib.CC_OPT_ITEM_ROWS, 50000)
+    for n, e in (graphgen.rmat(19, 16, 2), graphgen.grid(700, 900, 0.55, 5),
+                 graphgen.forest(300, 3)):
+        exp = oracle.rem_union_find(n, e)
+        engine.stage_graph(ctx, n, e, "l2_tiled_check")
+        for count in (False, True):
+            labels = np.empty(n, dtype=np.int64)
+            _, st = engine.run_staged(ctx, make_schedule("c2"), count_changes=count,
+                                      labels_out=labels)
+            assert np.array_equal(labels, exp), (n, count)
+            check_invariants(labels, st)
+        for _ in range(4):
+            lab = exp.copy()
+            x = int(rng.integers(1, n))
+            lab[x] = int(rng.integers(0, x))
+            _lib.check(ctx.lib.cc_write_labels(ctx.handle, lab.ctypes.data, 8))
+            assert engine.loop_check(ctx) == oracle.early_convergence_check(n, e, lab)
+        _lib.check(ctx.lib.cc_write_labels(ctx.handle, exp.ctypes.data, 8))
+        assert engine.loop_check(ctx)
+    ctx.close()
+
+
 @pytest.mark.parametrize("check_shift", [7, 9, 12])
 def test_bitmap_check_equals_oracle_early_check(check_shift):
     """The layout-6 early check (component bitmap + check copy) decides
