@@ -544,7 +544,10 @@ def run_single(args, device):
             "streamed_bytes_per_launch": b2, "frac_streamed": b2 / t2 / 1e9 / peak}
     elif rt2:  # layout 6: later sweeps are the bitmap sweep over the check copy
         t2 = sum(rt2) / len(rt2)
-        b2 = 8 * m + n // 8 + 4 * n  # copy rows + bitmap + the vertex pass's label read
+        # copy rows (6 B packed when log2(n) + check_shift(20) - 16 <= 32, else 8 B)
+        # + the bitmap + the vertex pass's label read
+        packed = max(1, (n - 1).bit_length()) + 4 <= 32
+        b2 = (6 if packed else 8) * m + n // 8 + 4 * n
         roofline["bitmap_sweep_kernel"] = {
             "kernel": "k_pick_root + k_bits_idem + k_sweep_bits (dst-bucketed check copy, "
                       "component bitmap; rows both of whose ends carry the root label are "
