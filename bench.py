@@ -89,7 +89,7 @@ def parse(argv=None):
     p.add_argument("--seed", type=int, default=1)
     p.add_argument("--layout", default="auto",
                    choices=["auto", "input", "src_sorted", "chunk_sorted", "dst_bucketed",
-                            "l2_tiled", "hybrid", "l2_tiled_check"],
+                            "l2_tiled", "hybrid", "l2_tiled_check", "relabel"],
                    help="staging-time edge layout of the device-resident runs")
     p.add_argument("--e2e-layout", default="auto",
                    help="layout= of the e2e drop-in run_contour call")
@@ -442,7 +442,8 @@ def run_single(args, device):
     prep_s = time.perf_counter() - t_prep
 
     early = args.early_check == "on" or (args.early_check == "auto" and
-                                         layout in ("hybrid", "l2_tiled", "l2_tiled_check"))
+                                         layout in ("hybrid", "l2_tiled", "l2_tiled_check",
+                                                    "relabel"))
     hybrid = layout == "hybrid"
     two_kernel = layout in ("hybrid", "l2_tiled_check")  # sweep 1 and later sweeps differ
     sched = make_schedule("c2", atomic=atomic)

@@ -148,7 +148,14 @@ int cc_sweep(cc_ctx* ctx, int order, int sync, int atomic, int first, int* wrote
  * 2^CC_OPT_CHECK_SHIFT-vertex dst buckets and src-sorted, walked with a
  * component bitmap (one bit per vertex: "labelled like the giant
  * component") whose dst part sits in shared memory -- the check then
- * streams rows instead of gathering labels. */
+ * streams rows instead of gathering labels; mode 7 relabels the vertices
+ * that appear in edges by first appearance in the row order and keeps a copy
+ * of the rows in those IDs (sparse graphs whose labels exceed L2, e.g. a
+ * forest written tree by tree: the rows a sweep processes together then touch
+ * nearby labels); asynchronous runs without exact counts sweep the copy and
+ * map the labels back to the minimum original ID per component, every other
+ * run uses the rows in input order; without locality in the input order the
+ * build falls back to mode 4. */
 int cc_reorder_edges(cc_ctx* ctx, int mode);
 
 /* Tuning knobs of a context.  Store modes for async sweeps:

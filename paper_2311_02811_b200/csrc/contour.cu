@@ -78,6 +78,8 @@ struct NvtxRange {
 
 #include "staging.inc"
 
+#include "relabel.inc"
+
 // ------------------------------------------------------------------ C-ABI
 extern "C" {
 
@@ -133,6 +135,9 @@ void cc_destroy(cc_ctx* c) {
     cudaFree(c->bdst16);
     cudaFree(c->bits);
     cudaFree(c->dr0);
+    cudaFree(c->rlab);
+    cudaFree(c->rorig);
+    cudaFree(c->rmin);
     for (int b = 0; b < kNSub; ++b) {
         cudaFreeHost(c->hsub[b]);
         if (c->subdone[b]) cudaEventDestroy(c->subdone[b]);
@@ -548,6 +553,12 @@ int run_impl(cc_ctx* c, const cc_schedule* s, int flags, int64_t cap, void* labe
     const bool check = (flags & CC_RUN_EARLY_CHECK) != 0;
     const bool times = (flags & CC_RUN_SWEEP_TIMES) != 0;
     const bool first_scatter = (flags & CC_RUN_FIRST_SCATTER) != 0;
+    // layout 7: asynchronous runs without exact counts on the relabeled rows
+    // (the dynamics differ from the original IDs', so parity modes use the
+    // original rows in input order)
+    if (c->layout == 7 && c->rlab && !sync && !count && !first_scatter && c->peers.n == 0 &&
+        start == 0)
+        return run_relabeled(c, s, flags, cap, labels_out, out_eb, st);
     if (!sync && !count && !first_scatter && !(flags & CC_RUN_HOST_LOOP) && c->n > 0 &&
         c->peers.n == 0 && start == 0)
         return run_graph(c, s, cap, labels_out, out_eb, st, check ? 1 : 0);
@@ -945,12 +956,13 @@ int cc_reorder_edges(cc_ctx* c, int mode) {
     NvtxRange nvtx_("cc_reorder_edges");
     if (!c) return fail(CC_EINVAL, "null context");
     if (mode == 0) return CC_OK;
-    if (mode < 1 || mode > 6) return fail(CC_EINVAL, "unknown edge layout mode %d", mode);
+    if (mode < 1 || mode > 7) return fail(CC_EINVAL, "unknown edge layout mode %d", mode);
     std::lock_guard<std::mutex> lk(c->mu);
     DeviceGuard g(c->device);
     if (c->m < 2) return CC_OK;
     if (mode == 3 || mode == 5) return reorder_bucketed(c, mode);
     if (mode == 4 || mode == 6) return reorder_l2tiles(c, mode);
+    if (mode == 7) return reorder_relabel(c);
     c->layout = mode;
     // mode 1: one global sort by src; mode 2: independent sorts of
     // consecutive chunks of c->sort_chunk rows (each chunk's label gathers

@@ -137,7 +137,7 @@ def _unpack_graph(g):
 
 
 LAYOUTS = {"input": 0, "src_sorted": 1, "chunk_sorted": 2, "dst_bucketed": 3, "l2_tiled": 4,
-           "hybrid": 5, "l2_tiled_check": 6}
+           "hybrid": 5, "l2_tiled_check": 6, "relabel": 7}
 AUTO_SORT_MIN_ROWS = 1 << 16
 
 
@@ -169,7 +169,11 @@ def resolve_layout(layout: str, m: int, n: int = 0, resident: bool = True,
         if 4 * n > AUTO_L2_LABEL_BYTES:
             if not resident:
                 return "chunk_sorted" if m >= 4 * n else "l2_tiled"
-            return "l2_tiled_check" if copies and m >= 4 * n else "l2_tiled"
+            if m >= 4 * n:
+                return "l2_tiled_check" if copies else "l2_tiled"
+            # sparse (the forest): first-appearance relabeling, which falls
+            # back to the tiles when the input order carries no locality
+            return "relabel" if copies and m < (1 << 31) else "l2_tiled"
         if resident and copies and m < (1 << 31) and m >= AUTO_HYBRID_MIN_DEGREE * n:
             return "hybrid"
         return "chunk_sorted"
@@ -237,7 +241,8 @@ def stage_graph(ctx: _lib.Context, n: int, edges, layout: str = "auto") -> None:
         _lib.check(lib.cc_stage_edges(ctx.handle, ctypes.c_void_p(e.ctypes.data),
                                       e.dtype.itemsize, m, n))
     ctx.n, ctx.m = n, m
-    if layout in ("src_sorted", "dst_bucketed", "l2_tiled", "hybrid", "l2_tiled_check"):
+    if layout in ("src_sorted", "dst_bucketed", "l2_tiled", "hybrid", "l2_tiled_check",
+                  "relabel"):
         _lib.check(lib.cc_reorder_edges(ctx.handle, LAYOUTS[layout]))
 
 

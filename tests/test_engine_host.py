@@ -73,10 +73,11 @@ def test_auto_layout_policy():
     assert resolve_layout("auto", 8589934592, 268435456, resident=False) == "chunk_sorted"
     assert resolve_layout("auto", 8589934592 // 8, 268435456, copies=False) == "l2_tiled"
     assert resolve_layout("auto", 1845476017, 2307095021, resident=False) == "l2_tiled"
-    assert resolve_layout("auto", 1845476017, 2307095021) == "l2_tiled"          # forest
+    assert resolve_layout("auto", 1845476017, 2307095021) == "relabel"           # forest
+    assert resolve_layout("auto", 1845476017, 2307095021, copies=False) == "l2_tiled"
     assert resolve_layout("auto", 1 << 31, 1 << 24) == "chunk_sorted"            # m >= 2^31
     for lay in ("input", "src_sorted", "chunk_sorted", "dst_bucketed", "l2_tiled", "hybrid",
-                "l2_tiled_check"):
+                "l2_tiled_check", "relabel"):
         assert resolve_layout(lay, 10, 10) == lay
     with pytest.raises(ValueError):
         resolve_layout("bogus", 10, 10)

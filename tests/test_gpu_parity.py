@@ -558,7 +558,7 @@ def test_random_graphs_every_layout_and_loop():
     rng = np.random.default_rng(int(os.environ.get("CC_FUZZ_SEED", "20261020")))
     ctx = _lib.Context(0)
     layouts = ("input", "src_sorted", "chunk_sorted", "dst_bucketed", "l2_tiled", "hybrid",
-               "l2_tiled_check")
+               "l2_tiled_check", "relabel")
     for t in range(int(os.environ.get("CC_FUZZ_ITERS", "120"))):
         n = int(rng.integers(1, 6000))
         m = int(rng.integers(0, 25000))
@@ -737,6 +737,38 @@ def test_l2_tiled_layout_exact(tile_shift, layout):
                                   early_check=early)
                 assert np.array_equal(labels, exp), (n, sched, early)
                 assert engine.verify_staged(ctx) == 0
+    ctx.close()
+
+
+def test_relabel_layout_exact():
+    """Layout 7 (first-appearance relabeling + map back to the minimum
+    original ID): exact labels for asynchronous runs on the relabeled rows
+    (graph loop and host loop, early check on/off) and for the parity modes
+    that run on the original rows (exact counts, synchronous); isolated
+    vertices keep their own ID; the device certificate holds on the
+    original rows after the map back."""
+    rng = np.random.default_rng(77)
+    ctx = _lib.Context(0)
+    cases = [graphgen.forest(60, 3), graphgen.grid(300, 200, 0.55, 2), graphgen.rmat(14, 16, 9),
+             (5, np.zeros((0, 2), np.int64))]
+    for _ in range(6):
+        n = int(rng.integers(10, 40000))
+        m = int(rng.integers(1, 30000))
+        cases.append((n, rng.integers(0, n, size=(m, 2), dtype=np.int64)))
+    for n, e in cases:
+        exp = oracle.rem_union_find(n, e)
+        engine.stage_graph(ctx, n, e, "relabel")
+        for sched, count in ((make_schedule("c2"), False), (make_schedule("cm", 6), False),
+                             (make_schedule("c2", atomic=False), False),
+                             (make_schedule("c2"), True), (make_schedule("c2", sync=True), True)):
+            for early in (False, True):
+                for host_loop in (False, True):
+                    labels = np.empty(n, dtype=np.int64)
+                    _, st = engine.run_staged(ctx, sched, count_changes=count, early_check=early,
+                                              host_loop=host_loop, labels_out=labels)
+                    assert np.array_equal(labels, exp), (n, sched, count, early, host_loop)
+                    check_invariants(labels, st)
+                    assert engine.verify_staged(ctx) == 0
     ctx.close()
 
 
