@@ -160,7 +160,8 @@ class _HostIO:
         """Stage this rank's host edge shard on its GPU (own PCIe link); the
         label buffer -- and so any peer mapping of it -- is kept."""
         from .engine import stage_graph
-        stage_graph(self.shard.ctx, self.n, edges, layout)
+        # one row array: the exchange kernels walk the primary rows only
+        stage_graph(self.shard.ctx, self.n, edges, layout, copies=False)
 
     def read_labels(self, out) -> None:
         """Copy the (converged) label replica into a host array of n
@@ -492,7 +493,7 @@ def run_in_process(n: int, edges, schedule, devices, cadence: int = 1, layout: s
             torch.cuda.set_device(dev)
             ctx = _lib.Context(dev)
             lo, hi = shard_rows(m, r, world)
-            stage_graph(ctx, n, e[lo:hi], layout)
+            stage_graph(ctx, n, e[lo:hi], layout, copies=False)
             shard = CudaShard(ctx, n, atomic=schedule.atomic)
             if schedule.sync:
                 runner = SyncShardedContour(shard, n, m, order_for=schedule.order_for,

@@ -202,7 +202,8 @@ def apply_layout(ctx: _lib.Context, layout: str) -> None:
         _lib.check(ctx.lib.cc_reorder_edges(ctx.handle, LAYOUTS[layout]))
 
 
-def stage_graph(ctx: _lib.Context, n: int, edges, layout: str = "auto") -> None:
+def stage_graph(ctx: _lib.Context, n: int, edges, layout: str = "auto",
+                copies: bool = True) -> None:
     """Stage an (m, 2) edge array (numpy int32/int64 on the host, or a CUDA
     tensor) as packed uint32 SoA in HBM, with the graph.py:73-79 range check.
 
@@ -214,7 +215,7 @@ def stage_graph(ctx: _lib.Context, n: int, edges, layout: str = "auto") -> None:
     ctx.staged = None  # the context's edges change: no resident graph to reuse
     m_rows = int(edges.shape[0]) if hasattr(edges, "shape") and len(edges.shape) == 2 \
         else len(edges)
-    layout = resolve_layout(layout, m_rows, n)
+    layout = resolve_layout(layout, m_rows, n, copies=copies)
     ctx.set_option(_lib.CC_OPT_STAGE_LAYOUT, 2 if layout in ("chunk_sorted", "hybrid") else 0)
     lib = ctx.lib
     if hasattr(edges, "data_ptr") and getattr(edges, "is_cuda", False):

@@ -30,9 +30,9 @@ import numpy as np
 from oracle import gen
 from minmapcc import Graph, bench, run_contour, make_schedule
 graphs = {{
-    "rmat14": gen.rmat(14, 16, 3),
-    "grid200": gen.grid(200, 200, 0.55, 2),
-    "forest": gen.forest(40, 5),
+    "rmat12": gen.rmat(12, 16, 3),
+    "grid120": gen.grid(120, 120, 0.55, 2),
+    "forest": gen.forest(12, 5),
 }}
 plan = []
 for name, (n, e) in graphs.items():
@@ -46,7 +46,7 @@ out = [dict(graph=r.graph, variant=r.variant, sync=r.sync, match=r.oracle_match,
             checksum=r.label_checksum, executed=r.sweeps_executed,
             until=r.sweeps_until_stable, components=r.components, error=r.error)
        for r in recs]
-n, e = graphs["rmat14"]
+n, e = graphs["rmat12"]
 g = Graph.from_edges(n, e)
 labels, st = run_contour(g, make_schedule("c2"))
 rep = bench.verify_labels(g, labels)
