@@ -561,6 +561,8 @@ def run_single(args, device):
     fsv = None
     if args.fastsv > 0:
         from paper_2311_02811_b200.baselines import fastsv_staged
+        fastsv_staged(ctx, sweep_times=False)  # untimed: scratch allocation, module load
+        torch.cuda.synchronize()
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         f0.record(stream)
         fst = None
@@ -595,6 +597,8 @@ def run_single(args, device):
         e2e = {"value": m / e2e_s, "unit": UNIT,
                "h2d_bytes_per_step": int(host_edges.nbytes), "d2h_bytes_per_step": int(n * 8),
                "seconds_per_step": e2e_s, "seconds_min": min(walls),
+               "seconds_median": statistics.median(walls),
+               "step_seconds": [round(w, 3) for w in walls],
                "path": f"run_contour((n, edges), make_schedule('c2', atomic={atomic}), "
                        f"layout={args.e2e_layout!r}) -- the drop-in with the reference's defaults "
                        f"(exact change counts, early check), pageable {host_edges.dtype} (m, 2) "
