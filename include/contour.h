@@ -320,6 +320,38 @@ int cc_parse_edges(const char* buf, int64_t len, int mode, int64_t* out, int64_t
                    int64_t* m_out, int64_t* err_line, int* err_code, int* err_tokens,
                    int threads, int64_t bound, int64_t* err_vals);
 
+/* ---- ingestion on the device ----
+ * The reference loaders load_edge_list (graph.py:149-197) and the Matrix
+ * Market body of load_matrix_market (graph.py:252-274) with the text moved to
+ * HBM once: newline split, tokenising (the line semantics of cc_parse_edges,
+ * one shared definition), canonical (min, max) rows, densification by
+ * ascending original ID (np.unique + np.searchsorted, graph.py:186-194) and
+ * sorted de-duplication (np.unique(axis=0), graph.py:142-146) run on the
+ * device.  A handle owns its device buffers; results stay valid until the
+ * next parse on it or cc_ingest_destroy.  Calls on one handle serialise. */
+typedef struct cc_ingest cc_ingest;
+int cc_ingest_create(int device, cc_ingest** out);
+void cc_ingest_destroy(cc_ingest* h);
+/* Parse host text buf[0, len) (pageable or pinned); errors as cc_parse_edges
+ * (first malformed line in file order, 1-based).  canonical != 0 stores every
+ * row as (min, max) (graph.py:133-139).  *m_out = rows kept. */
+int cc_ingest_parse(cc_ingest* h, const char* buf, int64_t len, int mode, int64_t bound,
+                    int canonical, int64_t* m_out, int64_t* err_line, int* err_code,
+                    int* err_tokens, int64_t* err_vals);
+/* The same for text already in device memory (on the handle's device). */
+int cc_ingest_parse_device(cc_ingest* h, const char* text_dev, int64_t len, int mode,
+                           int64_t bound, int canonical, int64_t* m_out, int64_t* err_line,
+                           int* err_code, int* err_tokens, int64_t* err_vals);
+/* remap != 0: densify IDs (*has_map = 1 when the IDs were not already 0..k-1);
+ * dedupe != 0: sorted unique rows.  n_given >= 0 fixes n (Matrix Market
+ * size line); else n = #distinct IDs (remap) or max ID + 1 (0 when empty). */
+int cc_ingest_finish(cc_ingest* h, int remap, int dedupe, int64_t n_given, int64_t* n_out,
+                     int64_t* m_out, int* has_map);
+/* Device pointers of the result: edges (m, 2) int64, id map (n) int64 or NULL. */
+int cc_ingest_result(cc_ingest* h, const int64_t** edges_dev, const int64_t** id_map_dev);
+/* Copy the result to host or device memory (either pointer may be NULL). */
+int cc_ingest_copy(cc_ingest* h, int64_t* edges_out, int64_t* id_map_out);
+
 #ifdef __cplusplus
 }
 #endif

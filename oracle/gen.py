@@ -197,3 +197,72 @@ def forest(components: int, seed: int = 1, isolated_frac: float = 0.2,
     u = permute_ids(u.astype(np.uint64), n, pk).astype(np.int64)
     v = permute_ids(v.astype(np.uint64), n, pk).astype(np.int64)
     return n, np.stack([u, v], axis=1)
+
+
+# ---------------------------------------------------------------- ingestion
+INGEST_TEXT_CASES = ("edgelist_sparse", "edgelist_dense", "edgelist_err_nonint",
+                     "edgelist_err_tokens", "edgelist_err_negative", "mtx_symmetric_real",
+                     "mtx_general_pattern", "mtx_err_range", "mtx_err_count")
+
+
+def ingest_text(case: str, seed: int = 1, lines: int = 60_000) -> str:
+    """Seeded edge-list / Matrix Market text for the ingestion parity
+    fixtures (tests/golden/ingest_large.json): comment and blank lines, tabs,
+    CRLF endings, '+' signs, '_' digit grouping, leading zeros, reversed and
+    repeated pairs, self-loops, no trailing newline; the error cases place one
+    malformed line at a seeded position."""
+    rng = np.random.default_rng([seed, INGEST_TEXT_CASES.index(case)])
+    mtx = case.startswith("mtx")
+    if case == "edgelist_sparse":
+        pool = np.unique(rng.integers(0, 10**12, size=lines // 2))
+    elif mtx:
+        pool = np.arange(1, 40_001)
+    else:
+        pool = np.arange(0, lines // 3)
+    u = pool[rng.integers(0, pool.size, size=lines)]
+    v = pool[rng.integers(0, pool.size, size=lines)]
+    dup = rng.random(lines) < 0.1
+    u[dup], v[dup] = np.roll(v, 1)[dup], np.roll(u, 1)[dup]
+    loops = rng.random(lines) < 0.01
+    v[loops] = u[loops]
+
+    def tok(x: int, r: float) -> str:
+        if r < 0.03:
+            return "+" + str(x)
+        if r < 0.05 and x >= 1000:
+            s = str(x)
+            return s[:-3] + "_" + s[-3:]
+        if r < 0.07:
+            return "00" + str(x)
+        return str(x)
+
+    out = []
+    if mtx:
+        field = "real" if case == "mtx_symmetric_real" else "pattern"
+        sym = "symmetric" if case == "mtx_symmetric_real" else "general"
+        out.append(f"%%MatrixMarket matrix coordinate {field} {sym}")
+        out.append("% generated by oracle/gen.py ingest_text")
+        declared = lines + (1 if case == "mtx_err_count" else 0)
+        out.append(f"{pool.size} {pool.size} {declared}")
+    r = rng.random((lines, 4))
+    for i in range(lines):
+        if not mtx and r[i, 3] < 0.02:
+            out.append("# comment " + str(i))
+        if r[i, 3] > 0.99:
+            out.append("")
+        if mtx and r[i, 3] < 0.01:
+            out.append("% note")
+        sep = "\t" if r[i, 2] < 0.1 else (" " * (1 + int(r[i, 2] * 3)))
+        line = tok(int(u[i]), r[i, 0]) + sep + tok(int(v[i]), r[i, 1])
+        if case == "mtx_symmetric_real":
+            line += f" {r[i, 2]:.4f}"
+        if r[i, 2] > 0.95:
+            line = "  " + line + " \r"
+        out.append(line)
+    bad = {"edgelist_err_nonint": "12 x7", "edgelist_err_tokens": "1 2 3",
+           "edgelist_err_negative": "5 -3", "mtx_err_range": f"1 {pool.size + 1}"}
+    if case in bad:
+        pos = int(rng.integers(len(out) // 2, len(out)))
+        out.insert(pos, bad[case])
+    text = "\n".join(out)
+    return text if int(rng.integers(0, 2)) else text + "\n"

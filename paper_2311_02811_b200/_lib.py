@@ -120,6 +120,22 @@ SIGNATURES = {
                                       ctypes.c_int64, _I64P, _I64P, ctypes.POINTER(ctypes.c_int),
                                       ctypes.POINTER(ctypes.c_int), ctypes.c_int, ctypes.c_int64,
                                       _I64P]),
+    "cc_ingest_create": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_void_p)]),
+    "cc_ingest_destroy": (None, [ctypes.c_void_p]),
+    "cc_ingest_parse": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_char_p, ctypes.c_int64,
+                                       ctypes.c_int, ctypes.c_int64, ctypes.c_int, _I64P, _I64P,
+                                       ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int),
+                                       _I64P]),
+    "cc_ingest_parse_device": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
+                                              ctypes.c_int, ctypes.c_int64, ctypes.c_int, _I64P,
+                                              _I64P, ctypes.POINTER(ctypes.c_int),
+                                              ctypes.POINTER(ctypes.c_int), _I64P]),
+    "cc_ingest_finish": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
+                                        ctypes.c_int64, _I64P, _I64P,
+                                        ctypes.POINTER(ctypes.c_int)]),
+    "cc_ingest_result": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_void_p),
+                                        ctypes.POINTER(ctypes.c_void_p)]),
+    "cc_ingest_copy": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
 }
 
 _lib = None

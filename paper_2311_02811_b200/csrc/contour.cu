@@ -80,6 +80,8 @@ struct NvtxRange {
 
 #include "relabel.inc"
 
+#include "ingest.inc"
+
 // ------------------------------------------------------------------ C-ABI
 extern "C" {
 

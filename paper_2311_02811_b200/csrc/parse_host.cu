@@ -1,4 +1,6 @@
-// Multi-threaded text parsers for graph ingestion.
+// Multi-threaded host text parsers for graph ingestion;
+// the line semantics live in parse_line.cuh, shared with the device parser
+// (ingest.inc).
 //
 // Same line semantics as the reference loaders
 // (/root/reference/pkg/src/minmapcc/graph.py:149-197 load_edge_list,
@@ -17,70 +19,10 @@
 #include <vector>
 
 #include "contour.h"
+#include "parse_line.cuh"
 
-namespace {
-
-inline bool is_space(char c) { return c == ' ' || c == '\t' || c == '\r' || c == '\v' || c == '\f'; }
-
-struct LineResult {
-    int status;  // 0 skip, 1 row, <0 error code
-    int64_t u, v;
-    int ntok;
-};
-
-// parse an integer token [p, e); returns false if not an integer
-inline bool parse_int(const char* p, const char* e, int64_t& out) {
-    bool neg = false;
-    if (p < e && (*p == '+' || *p == '-')) { neg = *p == '-'; ++p; }
-    if (p == e) return false;
-    int64_t x = 0;
-    const char* s = p;
-    for (; p < e; ++p) {
-        if (*p == '_' && p > s && p + 1 < e && p[-1] >= '0' && p[-1] <= '9' && p[1] >= '0' &&
-            p[1] <= '9')
-            continue;  // Python int() digit grouping, as the reference's int(token)
-        if (*p < '0' || *p > '9') return false;
-        if (x > (INT64_MAX - 9) / 10) return false;
-        x = x * 10 + (*p - '0');
-    }
-    out = neg ? -x : x;
-    return true;
-}
-
-inline LineResult parse_line(const char* b, const char* e, int mode, int64_t bound) {
-    while (b < e && is_space(*b)) ++b;
-    while (e > b && is_space(e[-1])) --e;
-    LineResult r{0, 0, 0, 0};
-    if (b == e) return r;
-    if (*b == '%' || (mode == 0 && *b == '#')) return r;
-    const char* tok[3][2];
-    int nt = 0;
-    const char* p = b;
-    while (p < e) {
-        while (p < e && is_space(*p)) ++p;
-        if (p >= e) break;
-        const char* s = p;
-        while (p < e && !is_space(*p)) ++p;
-        if (nt < 3) { tok[nt][0] = s; tok[nt][1] = p; }
-        ++nt;
-    }
-    r.ntok = nt;
-    if (mode == 0 && nt != 2) { r.status = CC_PARSE_TOKENS; return r; }
-    if (mode == 1 && nt < 2) { r.status = CC_PARSE_TOKENS; return r; }
-    if (!parse_int(tok[0][0], tok[0][1], r.u) || !parse_int(tok[1][0], tok[1][1], r.v)) {
-        r.status = CC_PARSE_NONINT;
-        return r;
-    }
-    if (mode == 0 && (r.u < 0 || r.v < 0)) { r.status = CC_PARSE_NEGATIVE; return r; }
-    if (mode == 1 && bound != 0 && !(1 <= r.u && r.u <= bound && 1 <= r.v && r.v <= bound)) {
-        r.status = CC_PARSE_RANGE;
-        return r;
-    }
-    r.status = 1;
-    return r;
-}
-
-}  // namespace
+using ccparse::LineResult;
+using ccparse::parse_line;
 
 extern "C" {
 

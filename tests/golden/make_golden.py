@@ -219,6 +219,30 @@ def ingest_cases():
     return out
 
 
+def ingest_large_cases():
+    """The reference loaders on seeded texts (oracle/gen.py ingest_text) of
+    ~60k lines: outputs as SHA-256 of the int64 edges / id_map, or the error."""
+    import io
+    out = []
+    for case in gen.INGEST_TEXT_CASES:
+        text = gen.ingest_text(case)
+        kwargs = ([{}, {"remap": False}, {"dedupe": False}, {"remap": False, "dedupe": False}]
+                  if case.startswith("edgelist") else [{}])
+        for kw in kwargs:
+            try:
+                if case.startswith("edgelist"):
+                    g = ref.load_edge_list(io.StringIO(text), **kw)
+                else:
+                    g = ref.load_matrix_market(io.StringIO(text))
+                res = {"n": int(g.n), "m": int(g.m), "edges": sha(g.edges),
+                       "id_map": None if g.id_map is None else sha(g.id_map),
+                       "head": g.edges[:3].tolist()}
+            except Exception as exc:  # noqa: BLE001 - recording the reference's error
+                res = {"error": type(exc).__name__, "message": str(exc)}
+            out.append({"case": case, "kwargs": kw, "result": res})
+    return out
+
+
 def forest_diag_cases(rng):
     """forest_diagnostics (engine.py:373-405) on pointer graphs: the
     reference's own examples (test_engine.py:281-309), converged run labels,
@@ -248,6 +272,12 @@ def forest_diag_cases(rng):
 
 
 def main():
+    if "--ingest-large" in sys.argv:  # only the large ingestion fixture (ingest_large.json)
+        with open(os.path.join(HERE, "ingest_large.json"), "w") as fh:
+            json.dump({"generator": "tests/golden/make_golden.py --ingest-large",
+                       "reference": "minmapcc " + ref.__version__,
+                       "cases": ingest_large_cases()}, fh, indent=0)
+        return
     if "--forest-diag" in sys.argv:  # only the forest_diagnostics fixture (forest_diag.json)
         with open(os.path.join(HERE, "forest_diag.json"), "w") as fh:
             json.dump({"generator": "tests/golden/make_golden.py --forest-diag",

@@ -116,3 +116,50 @@ def test_gpu_harness_records(tmp_path):
     assert recs[5].error and not recs[5].oracle_match
     harness.write_csv(recs, tmp_path / "out.csv")
     assert (tmp_path / "out.csv").read_text().count("\n") == len(recs) + 1
+
+
+def _sha(a) -> str:
+    import hashlib
+    return hashlib.sha256(np.ascontiguousarray(a, dtype=np.int64).tobytes()).hexdigest()
+
+
+def _ingest_large():
+    import json
+    import os
+    with open(os.path.join(os.path.dirname(__file__), "golden", "ingest_large.json")) as fh:
+        return json.load(fh)["cases"]
+
+
+def check_ingest_large(load, to_numpy):
+    """Run every ~60k-line fixture (oracle/gen.py ingest_text) through
+    ``load(case, text, kwargs)`` and compare with the reference's recorded
+    output (tests/golden/ingest_large.json)."""
+    errors = {"EdgeListParseError": EdgeListParseError,
+              "MatrixMarketFormatError": MatrixMarketFormatError}
+    for c in _ingest_large():
+        text = gen.ingest_text(c["case"])
+        res = c["result"]
+        if res.get("error") == "MemoryError":
+            continue  # the reference's CSR of n = max ID + 1 ~ 1e12 (graph.py:80); see below
+        if "error" in res:
+            with pytest.raises(errors[res["error"]]) as ei:
+                load(c["case"], text, c["kwargs"])
+            assert str(ei.value) == res["message"], (c["case"], c["kwargs"])
+            continue
+        g = load(c["case"], text, c["kwargs"])
+        edges = to_numpy(g.edges)
+        assert (g.n, edges.shape[0]) == (res["n"], res["m"]), (c["case"], c["kwargs"])
+        assert edges[:3].tolist() == res["head"]
+        assert _sha(edges) == res["edges"], (c["case"], c["kwargs"])
+        got_map = None if g.id_map is None else _sha(to_numpy(g.id_map))
+        assert got_map == res["id_map"], (c["case"], c["kwargs"])
+
+
+def _load_host(case, text, kwargs):
+    if case.startswith("edgelist"):
+        return ingest.load_edge_list(io.StringIO(text), **kwargs)
+    return ingest.load_matrix_market(io.StringIO(text))
+
+
+def test_loaders_match_reference_large():
+    check_ingest_large(_load_host, np.asarray)
