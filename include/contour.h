@@ -334,7 +334,8 @@ int cc_ingest_create(int device, cc_ingest** out);
 void cc_ingest_destroy(cc_ingest* h);
 /* Parse host text buf[0, len) (pageable or pinned); errors as cc_parse_edges
  * (first malformed line in file order, 1-based).  canonical != 0 stores every
- * row as (min, max) (graph.py:133-139).  *m_out = rows kept. */
+ * row as (min, max) (graph.py:133-139); mode 1 rows are made 0-based
+ * (graph.py:267).  *m_out = rows kept. */
 int cc_ingest_parse(cc_ingest* h, const char* buf, int64_t len, int mode, int64_t bound,
                     int canonical, int64_t* m_out, int64_t* err_line, int* err_code,
                     int* err_tokens, int64_t* err_vals);

@@ -168,9 +168,26 @@ def _canonicalize(edges: np.ndarray) -> np.ndarray:  # graph.py:133-139
                             np.maximum(edges[:, 0], edges[:, 1])])
 
 
+def _sorted_unique(x: np.ndarray) -> np.ndarray:
+    """np.unique(x) for 1-D integers by sort + neighbour compare (numpy 2's
+    hash-based unique is several times slower on tens of millions of IDs)."""
+    s = np.sort(x, axis=None)
+    if s.size == 0:
+        return s
+    keep = np.empty(s.size, dtype=bool)
+    keep[0] = True
+    np.not_equal(s[1:], s[:-1], out=keep[1:])
+    return s[keep]
+
+
 def _dedupe_sorted(edges: np.ndarray) -> np.ndarray:  # graph.py:142-146
     if edges.shape[0] == 0:
         return edges
+    if int(edges.max()) < (1 << 31):
+        # np.unique(edges, axis=0) sorts rows as byte records; one packed
+        # (u << 32 | v) key per row sorts in the same (lexicographic) order
+        key = _sorted_unique((edges[:, 0].astype(np.int64) << 32) | edges[:, 1])
+        return np.column_stack([key >> 32, key & 0xFFFFFFFF])
     return np.unique(edges, axis=0)
 
 
@@ -210,7 +227,7 @@ def load_edge_list(source, *, dedupe: bool = True, remap: bool = True,
     edges = _canonicalize(rows)
     id_map = None
     if remap:
-        ids = np.unique(edges)
+        ids = _sorted_unique(edges)
         if ids[0] == 0 and ids[-1] == ids.size - 1:
             n = int(ids.size)
         else:  # densify by ascending original ID

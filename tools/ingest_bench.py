@@ -67,7 +67,7 @@ def main():
                  and np.array_equal(dev.id_map.cpu().numpy(), host.id_map))
     ref = {}
     ref_dir = os.path.join(ROOT, "baseline", "_ref")
-    if os.path.isdir(ref_dir):
+    if args.ref_lines > 0 and os.path.isdir(ref_dir):
         sys.path.insert(0, ref_dir)
         try:
             import minmapcc
