@@ -97,8 +97,10 @@ __device__ __forceinline__ bool batch_o1(const lab_t* R, lab_t* T, const lab_t (
 // kHintEdgeFirst: the edge stream is loaded L1::no_allocate with an L2
 // evict-first policy; kHintSrcKeep: src-side gathers evict-last.
 // kHintDstCg: dst gathers bypass L1 (ld.global.cg; they almost never hit it).
+// kHintPipe: software-pipelined edge stream (the next iteration's rows are
+// loaded before this iteration's gathers; k_sweep only).
 constexpr int kStoreMask = 7, kHintSrcStream = 8, kHintDstKeep = 16, kHintEdgeFirst = 32,
-              kHintSrcKeep = 64, kHintDstCg = 128;
+              kHintSrcKeep = 64, kHintDstCg = 128, kHintPipe = 256;
 
 __device__ __forceinline__ lab_t ld_evict_last(const lab_t* p) {
     uint64_t pol;
@@ -471,25 +473,47 @@ __global__ void __launch_bounds__(kThreads, MINB) k_sweep(const lab_t* __restric
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     bool wrote = false;
-    for (int64_t base = tid; base < nvec; base += stride * NV) {
-        lab_t u[4 * NV], v[4 * NV];
-#pragma unroll
-        for (int q = 0; q < NV; ++q) {
-            const int64_t i = base + (int64_t)q * stride;
-            uint4 a = make_uint4(0, 0, 0, 0), b = make_uint4(0, 0, 0, 0);
-            if (i < nvec) {
-                if (SM & kHintEdgeFirst) {
-                    a = ld_edges_evict_first(s4 + i);
-                    b = ld_edges_evict_first(d4 + i);
-                } else {
-                    a = __ldcs(s4 + i);
-                    b = __ldcs(d4 + i);
-                }
+    auto load = [&](int64_t i, uint4& a, uint4& b) {
+        a = make_uint4(0, 0, 0, 0);
+        b = make_uint4(0, 0, 0, 0);
+        if (i < nvec) {
+            if (SM & kHintEdgeFirst) {
+                a = ld_edges_evict_first(s4 + i);
+                b = ld_edges_evict_first(d4 + i);
+            } else {
+                a = __ldcs(s4 + i);
+                b = __ldcs(d4 + i);
             }
-            u[4 * q + 0] = a.x; u[4 * q + 1] = a.y; u[4 * q + 2] = a.z; u[4 * q + 3] = a.w;
-            v[4 * q + 0] = b.x; v[4 * q + 1] = b.y; v[4 * q + 2] = b.z; v[4 * q + 3] = b.w;
         }
-        wrote |= batch<OK, 4 * NV, SM>(R, T, u, v, order);
+    };
+    if constexpr ((SM & kHintPipe) != 0) {
+        uint4 a[NV], b[NV];
+#pragma unroll
+        for (int q = 0; q < NV; ++q) load(tid + (int64_t)q * stride, a[q], b[q]);
+        for (int64_t base = tid; base < nvec; base += stride * NV) {
+            lab_t u[4 * NV], v[4 * NV];
+#pragma unroll
+            for (int q = 0; q < NV; ++q) {
+                u[4 * q + 0] = a[q].x; u[4 * q + 1] = a[q].y; u[4 * q + 2] = a[q].z;
+                u[4 * q + 3] = a[q].w;
+                v[4 * q + 0] = b[q].x; v[4 * q + 1] = b[q].y; v[4 * q + 2] = b[q].z;
+                v[4 * q + 3] = b[q].w;
+                load(base + stride * NV + (int64_t)q * stride, a[q], b[q]);
+            }
+            wrote |= batch<OK, 4 * NV, SM>(R, T, u, v, order);
+        }
+    } else {
+        for (int64_t base = tid; base < nvec; base += stride * NV) {
+            lab_t u[4 * NV], v[4 * NV];
+#pragma unroll
+            for (int q = 0; q < NV; ++q) {
+                uint4 a, b;
+                load(base + (int64_t)q * stride, a, b);
+                u[4 * q + 0] = a.x; u[4 * q + 1] = a.y; u[4 * q + 2] = a.z; u[4 * q + 3] = a.w;
+                v[4 * q + 0] = b.x; v[4 * q + 1] = b.y; v[4 * q + 2] = b.z; v[4 * q + 3] = b.w;
+            }
+            wrote |= batch<OK, 4 * NV, SM>(R, T, u, v, order);
+        }
     }
     for (int64_t e = (nvec << 2) + tid; e < m; e += stride) {
         lab_t u[1] = {src[e]}, v[1] = {dst[e]};
