@@ -136,6 +136,7 @@ void cc_destroy(cc_ctx* c) {
     cudaFree(c->bdst);
     cudaFree(c->bdst16);
     cudaFree(c->bits);
+    cudaFree(c->cgbase);
     cudaFree(c->dr0);
     cudaFree(c->rlab);
     cudaFree(c->rorig);
@@ -884,7 +885,7 @@ int cc_set_option(cc_ctx* c, int option, int64_t value) {
             c->shortcut = (int)value;
             return CC_OK;
         case CC_OPT_SWEEP_VARIANT:
-            if (value < 0 || value > 18) return fail(CC_EINVAL, "sweep variant must be 0..18");
+            if (value < 0 || value > 21) return fail(CC_EINVAL, "sweep variant must be 0..21");
             c->sweep_variant = (int)value;
             c->loop_key.m = -1;
             return CC_OK;
@@ -922,7 +923,8 @@ int cc_set_option(cc_ctx* c, int option, int64_t value) {
             c->loop_key.m = -1;
             return CC_OK;
         case CC_OPT_CHECK_PACK:
-            c->check_pack = value != 0;
+            if (value < 0 || value > 2) return fail(CC_EINVAL, "check pack must be 0..2");
+            c->check_pack = (int)value;
             return CC_OK;
         case CC_OPT_HOST_SUB:
             if (value < 4096 || value > ((int64_t)1 << 26))

@@ -772,12 +772,14 @@ def test_relabel_layout_exact():
     ctx.close()
 
 
-@pytest.mark.parametrize("check_shift,pack", [(16, 1), (17, 1), (17, 0)])
+@pytest.mark.parametrize("check_shift,pack", [(16, 1), (17, 1), (17, 0), (16, 2), (17, 2),
+                                              (18, 2)])
 def test_packed_check_copy_exact(check_shift, pack):
-    """The 6-byte packed check copy (src | high offset bits, uint16 low bits;
-    used when log2(n) + check_shift - 16 <= 32, e.g. RMAT-28) against the
-    oracle: the bitmap check's verdicts and whole runs through the bitmap
-    sweep."""
+    """The packed check copies against the oracle: 6-byte rows (src | high
+    offset bits, uint16 low bits; pack 1) and delta-packed groups of 128 rows
+    (pack 2, the default: 32 - check_shift bits per source gap; the sparse
+    forest's gaps overflow them and the build falls back to 6-byte rows) --
+    the bitmap check's verdicts and whole runs through the bitmap sweep."""
     rng = np.random.default_rng(17)
     ctx = _lib.Context(0)
     ctx.set_option(_lib.CC_OPT_TILE_SHIFT, 18)
