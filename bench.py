@@ -545,14 +545,18 @@ def run_single(args, device):
             "streamed_bytes_per_launch": b2, "frac_streamed": b2 / t2 / 1e9 / peak}
     elif rt2:  # layout 6: later sweeps are the bitmap sweep over the check copy
         t2 = sum(rt2) / len(rt2)
-        # copy rows (6 B packed when log2(n) + check_shift(20) - 16 <= 32, else 8 B)
-        # + the bitmap + the vertex pass's label read
-        packed = max(1, (n - 1).bit_length()) + 4 <= 32
-        b2 = (6 if packed else 8) * m + n // 8 + 4 * n
+        # the check copy as staged (cc_layout_info: delta-packed groups, 4.03 B
+        # per row; or 6 / 8 B rows) + the bitmap + the vertex pass's label read
+        info = ctx.layout_info()
+        b2 = info["check_bytes"] + n // 8 + 4 * n
         roofline["bitmap_sweep_kernel"] = {
-            "kernel": "k_pick_root + k_bits_idem + k_sweep_bits (dst-bucketed check copy, "
+            "kernel": "k_pick_root + k_bits_idem + k_sweep_bits[_dp] (dst-bucketed check copy, "
                       "component bitmap; rows both of whose ends carry the root label are "
                       "decided without label gathers)",
+            "check_copy": {"format": {2: "delta-packed 128-row groups", 1: "6-byte rows",
+                                      0: "8-byte rows"}.get(info["check_format"]),
+                           "bytes": info["check_bytes"],
+                           "bytes_per_row": round(info["check_bytes"] / max(m, 1), 3)},
             "avg_launch_s": t2, "frac_of_B_sweep": b_sweep / t2 / 1e9 / peak,
             "streamed_bytes_per_launch": b2, "frac_streamed": b2 / t2 / 1e9 / peak,
             "launch_ms": [round(t * 1e3, 4) for t in rt2]}

@@ -78,6 +78,11 @@ int cc_create(int device, void* stream, cc_ctx** out);
 void cc_destroy(cc_ctx* ctx);
 const char* cc_last_error(void);
 int cc_version(void);
+/* Staged-layout facts for measurement (bench.py's rooflines): out[0] layout
+ * code, out[1] check-copy format (-1 none, 0 8-byte rows, 1 6-byte rows, 2
+ * delta-packed groups), out[2] bytes one pass over the check copy streams,
+ * out[3] work items, out[4] staged rows; the first `count` entries are written. */
+int cc_layout_info(cc_ctx* ctx, int64_t* out, int count);
 
 /* ---- staging: the Graph input contract (graph.py:57-90, engine.py:268-270) ----
  * edges: (m, 2) row-major pairs, elem_bytes 4 (int32) or 8 (int64), as the

@@ -56,6 +56,7 @@ SIGNATURES = {
     "cc_destroy": (None, [ctypes.c_void_p]),
     "cc_last_error": (ctypes.c_char_p, []),
     "cc_version": (ctypes.c_int, []),
+    "cc_layout_info": (ctypes.c_int, [ctypes.c_void_p, _I64P, ctypes.c_int]),
     "cc_stage_edges": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int,
                                       ctypes.c_int64, ctypes.c_int64]),
     "cc_stage_edges_device": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int,
@@ -190,6 +191,14 @@ class Context:
 
     def set_option(self, option: int, value: int) -> None:
         check(self.lib.cc_set_option(self.handle, option, value), "cc_set_option")
+
+    def layout_info(self) -> dict:
+        """cc_layout_info: layout code, check-copy format and bytes per pass."""
+        import numpy as np
+        out = np.zeros(5, dtype=np.int64)
+        check(self.lib.cc_layout_info(self.handle, out.ctypes.data_as(_I64P), 5), "cc_layout_info")
+        return {"layout": int(out[0]), "check_format": int(out[1]), "check_bytes": int(out[2]),
+                "items": int(out[3]), "m": int(out[4])}
 
     def close(self):
         if getattr(self, "handle", None):

@@ -88,6 +88,15 @@ extern "C" {
 const char* cc_last_error(void) { return g_err; }
 int cc_version(void) { return 1; }
 
+int cc_layout_info(cc_ctx* c, int64_t* out, int count) {
+    if (!c || !out || count < 1) return fail(CC_EINVAL, "cc_layout_info: invalid argument");
+    std::lock_guard<std::mutex> lk(c->mu);
+    const int64_t v[5] = {c->layout, c->layout == 6 ? (c->check_dp ? 2 : c->check_sbits ? 1 : 0) : -1,
+                          c->layout == 6 ? c->check_bytes : 0, c->n_items, c->m};
+    for (int i = 0; i < count && i < 5; ++i) out[i] = v[i];
+    return CC_OK;
+}
+
 int cc_create(int device, void* stream, cc_ctx** out) {
     if (!out) return fail(CC_EINVAL, "null output pointer");
     *out = nullptr;
