@@ -210,9 +210,15 @@ int cc_reorder_edges(cc_ctx* ctx, int mode);
                                       until the copy engine reads it) */
 #define CC_OPT_HOST_NT 20          /* 1: streaming (non-temporal) stores into the pinned
                                       sub-chunks (default 0: cached stores) */
-#define CC_OPT_CHECK_PACK 21       /* layout 6: 1 (default) = 6-byte check-copy rows (uint32
-                                      src + high offset bits, uint16 low offset bits) when
-                                      log2(n) + shift - 16 <= 32; 0 = 8-byte rows */
+#define CC_OPT_CHECK_PACK 21       /* layout 6 check copy: 2 (default) = delta-packed groups of
+                                      128 rows (source offset from the group's first source in
+                                      32 - shift bits | dst offset, 4.03 B/row) when they fit,
+                                      else 1 = 6-byte rows (uint32 src + high offset bits, uint16
+                                      low offset bits) when log2(n) + shift - 16 <= 32, else
+                                      0 = 8-byte rows */
+#define CC_OPT_LINK_PACK 22        /* pageable host edges: 1 (default) = rows cross PCIe as
+                                      ceil(2 log2(n) / 8) in {6, 7} bytes (u | v << log2 n)
+                                      when that is under 8; 0 = uint32 pairs */
 #define CC_OPT_STAGE_LAYOUT 4     /* layout applied while staging: 0 input order (default),
                                       2 chunk-sorted, each chunk sorted as soon as it lands,
                                       overlapped with the next chunk's host->device copy */

@@ -931,6 +931,9 @@ int cc_set_option(cc_ctx* c, int option, int64_t value) {
             c->flat_bits = (int)value;
             c->loop_key.m = -1;
             return CC_OK;
+        case CC_OPT_LINK_PACK:
+            c->link_pack = value != 0;
+            return CC_OK;
         case CC_OPT_CHECK_PACK:
             if (value < 0 || value > 2) return fail(CC_EINVAL, "check pack must be 0..2");
             c->check_pack = (int)value;

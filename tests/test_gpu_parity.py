@@ -1031,6 +1031,43 @@ def test_pageable_narrowing_range_checks_in_the_vector_body():
         run_contour((n, b), make_schedule("c2"))
 
 
+@pytest.mark.parametrize("n", [1, 2, 97, 1 << 16, (1 << 24) - 5, (1 << 24) + 3, (1 << 28) - 1])
+def test_pageable_link_packing(n):
+    """Pageable host edges cross PCIe as ceil(2 log2(n) / 8)-byte packed rows
+    (6 B up to n = 2^24, 7 B up to 2^28, else uint32 pairs): staged rows read
+    back equal to the input, labels equal the oracle's with packing on and
+    off, and IDs outside [0, n) -- in [n, 2^b) (device check) or beyond 2^b /
+    negative (host check) -- raise ValueError, int64 and int32."""
+    rng = np.random.default_rng(n)
+    m = 200_003
+    e = rng.integers(0, n, size=(m, 2), dtype=np.int64)
+    e[:: 7, 1] = e[:: 7, 0]  # self loops
+    exp = oracle.rem_union_find(n, e)
+    ctx = engine._context(0)
+    b = max(1, (n - 1).bit_length())
+    for pack in (1, 0):
+        ctx.set_option(_lib.CC_OPT_LINK_PACK, pack)
+        try:
+            for dt in (np.int64, np.int32):
+                a = np.ascontiguousarray(e, dtype=dt)
+                engine.stage_graph(ctx, n, a, "input")
+                back = np.empty((m, 2), dtype=np.int64)
+                _lib.check(ctx.lib.cc_read_edges(ctx.handle, back.ctypes.data, 8, 0, m))
+                assert np.array_equal(back, e), (pack, dt)
+                labels, _ = run_contour((n, a), make_schedule("c2"))
+                assert np.array_equal(labels, exp), (pack, dt)
+                bad_vals = [n, -1, (1 << b) + 1, -(1 << 30)]
+                if dt == np.int64:
+                    bad_vals.append(1 << 40)
+                for pos, val in zip((5, 100_001, 2 * m - 1, 77_777, 150_000), bad_vals):
+                    x = a.copy()
+                    x.flat[pos] = val
+                    with pytest.raises(ValueError):
+                        run_contour((n, x), make_schedule("c2"))
+        finally:
+            ctx.set_option(_lib.CC_OPT_LINK_PACK, 1)
+
+
 def test_frozen_edges_stay_resident():
     """run_contour on a read-only edge array (the reference's Graph freezes
     its arrays) reuses the graph staged by the previous call on the context,
