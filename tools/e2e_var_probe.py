@@ -21,11 +21,14 @@ def main():
     e = graphgen.read_edges(ctx, 8)
     ctx.close()
     c2 = engine._context(0)
-    st, rd, rc = [], [], []
-    for _ in range(reps):
-        t = time.perf_counter()
-        engine.stage_graph(c2, n, e, "input")
-        st.append(round(time.perf_counter() - t, 3))
+    st, rd, rc, st8 = [], [], [], []
+    for _ in range(reps):  # alternating: 7-byte packed rows / uint32 pairs on the link
+        for pack, out in ((1, st), (0, st8)):
+            c2.set_option(_lib.CC_OPT_LINK_PACK, pack)
+            t = time.perf_counter()
+            engine.stage_graph(c2, n, e, "input")
+            out.append(round(time.perf_counter() - t, 3))
+    c2.set_option(_lib.CC_OPT_LINK_PACK, 1)
     for _ in range(reps):
         t = time.perf_counter()
         lab = np.empty(n, dtype=np.int64)
@@ -37,7 +40,8 @@ def main():
         lab, _ = run_contour((n, e), make_schedule("c2"))
         rc.append(round(time.perf_counter() - t, 3))
         del lab
-    print(json.dumps({"stage_input_s": st, "read_labels_fresh_s": rd, "run_contour_s": rc}))
+    print(json.dumps({"stage_input_uint32_pairs_s": st8, "stage_input_packed_s": st,
+                      "read_labels_fresh_s": rd, "run_contour_s": rc}))
 
 
 if __name__ == "__main__":
