@@ -894,7 +894,7 @@ int cc_set_option(cc_ctx* c, int option, int64_t value) {
             c->shortcut = (int)value;
             return CC_OK;
         case CC_OPT_SWEEP_VARIANT:
-            if (value < 0 || value > 21) return fail(CC_EINVAL, "sweep variant must be 0..21");
+            if (value < 0 || value > 22) return fail(CC_EINVAL, "sweep variant must be 0..22");
             c->sweep_variant = (int)value;
             c->loop_key.m = -1;
             return CC_OK;

@@ -110,6 +110,15 @@ __device__ __forceinline__ lab_t ld_evict_last(const lab_t* p) {
     return r;
 }
 
+// the same, bypassing L1 (ld.global.cg): random gathers that rarely hit L1
+__device__ __forceinline__ lab_t ld_cg_evict_last(const lab_t* p) {
+    uint64_t pol;
+    lab_t r;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    asm volatile("ld.global.cg.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(pol));
+    return r;
+}
+
 __device__ __forceinline__ uint4 ld_edges_evict_first(const uint4* p) {
     uint64_t pol;
     uint4 r;
@@ -131,7 +140,9 @@ __device__ __forceinline__ bool batch_o2(const lab_t* R, lab_t* T, const lab_t (
         if (SMH & kHintSrcStream) lu[k] = live ? __ldcs(R + u[k]) : u[k];
         else if (SMH & kHintSrcKeep) lu[k] = live ? ld_evict_last(R + u[k]) : u[k];
         else lu[k] = live ? R[u[k]] : u[k];
-        if (SMH & kHintDstKeep) lv[k] = live ? ld_evict_last(R + v[k]) : v[k];
+        if ((SMH & kHintDstKeep) && (SMH & kHintDstCg))
+            lv[k] = live ? ld_cg_evict_last(R + v[k]) : v[k];
+        else if (SMH & kHintDstKeep) lv[k] = live ? ld_evict_last(R + v[k]) : v[k];
         else if (SMH & kHintDstCg) lv[k] = live ? __ldcg(R + v[k]) : v[k];
         else lv[k] = live ? R[v[k]] : v[k];
     }
