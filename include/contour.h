@@ -216,6 +216,9 @@ int cc_reorder_edges(cc_ctx* ctx, int mode);
                                       else 1 = 6-byte rows (uint32 src + high offset bits, uint16
                                       low offset bits) when log2(n) + shift - 16 <= 32, else
                                       0 = 8-byte rows */
+#define CC_OPT_SPLIT_SWEEP 23       /* layout 6, order-2 sweep 1: the first k L2 windows on the
+                                      tiles, then the bitmap sweep over the check copy of the
+                                      rest (0 = off: all windows on the tiles) */
 #define CC_OPT_LINK_PACK 22        /* pageable host edges: 1 (default) = rows cross PCIe as
                                       ceil(2 log2(n) / 8) in {6, 7} bytes (u | v << log2 n)
                                       when that is under 8; 0 = uint32 pairs */
