@@ -218,10 +218,12 @@ int cc_reorder_edges(cc_ctx* ctx, int mode);
                                       0 = 8-byte rows */
 #define CC_OPT_SPLIT_SWEEP 23       /* layout 6, order-2 sweep 1: the first k L2 windows on the
                                       tiles, then the bitmap sweep over the check copy of the
-                                      rest (0 = off: all windows on the tiles) */
+                                      rest (0 = off: all windows on the tiles; -1 = auto, the
+                                      default: a quarter of the windows on dense graphs) */
 #define CC_OPT_SPLIT_REBUILD 24     /* split sweep 1: L2 windows per component bitmap (the bitmap
                                       is rebuilt from the current labels before every group of
-                                      that many windows; 0 = one bitmap for all) */
+                                      that many windows; 0 = one bitmap for all; -1 = auto,
+                                      the default: 3/16 of the windows) */
 #define CC_OPT_LINK_PACK 22        /* pageable host edges: 1 (default) = rows cross PCIe as
                                       ceil(2 log2(n) / 8) in {6, 7} bytes (u | v << log2 n)
                                       when that is under 8; 0 = uint32 pairs */

@@ -932,11 +932,11 @@ int cc_set_option(cc_ctx* c, int option, int64_t value) {
             c->loop_key.m = -1;
             return CC_OK;
         case CC_OPT_SPLIT_REBUILD:
-            if (value < 0 || value > kMaxTiles) return fail(CC_EINVAL, "split rebuild out of range");
+            if (value < -1 || value > kMaxTiles) return fail(CC_EINVAL, "split rebuild out of range");
             c->split_rebuild = (int)value;
             return CC_OK;
         case CC_OPT_SPLIT_SWEEP:
-            if (value < 0 || value > kMaxTiles) return fail(CC_EINVAL, "split windows out of range");
+            if (value < -1 || value > kMaxTiles) return fail(CC_EINVAL, "split windows out of range");
             c->split_windows = (int)value;
             return CC_OK;
         case CC_OPT_LINK_PACK:

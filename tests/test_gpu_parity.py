@@ -807,6 +807,36 @@ def test_packed_check_copy_exact(check_shift, pack):
     ctx.close()
 
 
+@pytest.mark.parametrize("split,rebuild", [(1, 0), (3, 1), (5, 2), (-1, -1), (7, 3), (0, 0)])
+def test_split_sweep1_exact(split, rebuild):
+    """Sweep 1 on layout 6 split at an L2 window (CC_OPT_SPLIT_SWEEP): the
+    first windows on the tiles, the rest as bitmap sweeps over the check copy
+    with the bitmap rebuilt every `rebuild` windows -- labels equal the oracle's
+    for async / counted / host-loop / graph-loop runs and C-m, on RMAT (dense,
+    where auto splits) and a grid (sparse), 8-10 windows of 2^16 vertices."""
+    ctx = _lib.Context(0)
+    ctx.set_option(_lib.CC_OPT_TILE_SHIFT, 16)
+    ctx.set_option(_lib.CC_OPT_CHECK_SHIFT, 16)
+    ctx.set_option(_lib.CC_OPT_ITEM_ROWS, 20000)
+    ctx.set_option(_lib.CC_OPT_SPLIT_SWEEP, split)
+    ctx.set_option(_lib.CC_OPT_SPLIT_REBUILD, rebuild)
+    for n, e in (graphgen.rmat(19, 16, 2), graphgen.rmat(19, 16, 7),
+                 graphgen.grid(700, 900, 0.55, 5)):
+        exp = oracle.rem_union_find(n, e)
+        engine.stage_graph(ctx, n, e, "l2_tiled_check")
+        assert ctx.layout_info()["check_format"] == 2
+        for sched in (make_schedule("c2"), make_schedule("cm", 6), make_schedule("c2", sync=True)):
+            for count in (False, True):
+                for host_loop in (False, True):
+                    labels = np.empty(n, dtype=np.int64)
+                    _, st = engine.run_staged(ctx, sched, count_changes=count,
+                                              host_loop=host_loop, labels_out=labels)
+                    assert np.array_equal(labels, exp), (n, sched, count, host_loop)
+                    check_invariants(labels, st)
+        assert engine.verify_staged(ctx) == 0
+    ctx.close()
+
+
 @pytest.mark.parametrize("check_shift", [7, 9, 12])
 def test_bitmap_check_equals_oracle_early_check(check_shift):
     """The layout-6 early check (component bitmap + check copy) decides

@@ -28,8 +28,8 @@ def main():
     ap.add_argument("--ctas", default="0")
     ap.add_argument("--runs", type=int, default=3)
     ap.add_argument("--layout", default="auto")
-    ap.add_argument("--split", default="0", help="comma list of CC_OPT_SPLIT_SWEEP")
-    ap.add_argument("--rebuild", default="0", help="comma list of CC_OPT_SPLIT_REBUILD")
+    ap.add_argument("--split", default="-1", help="comma list of CC_OPT_SPLIT_SWEEP (-1 auto)")
+    ap.add_argument("--rebuild", default="-1", help="comma list of CC_OPT_SPLIT_REBUILD (-1 auto)")
     args = ap.parse_args()
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
