@@ -224,9 +224,6 @@ int cc_reorder_edges(cc_ctx* ctx, int mode);
                                       is rebuilt from the current labels before every group of
                                       that many windows; 0 = one bitmap for all; -1 = auto,
                                       the default: 3/16 of the windows) */
-#define CC_OPT_BITS_QUEUE 25        /* delta-packed bitmap sweep: 1 (default) = rows the bitmap
-                                      does not decide are queued in shared memory and run as
-                                      dense batches; 0 = on the spot */
 #define CC_OPT_LINK_PACK 22        /* pageable host edges: 1 (default) = rows cross PCIe as
                                       ceil(2 log2(n) / 8) in {6, 7} bytes (u | v << log2 n)
                                       when that is under 8; 0 = uint32 pairs */

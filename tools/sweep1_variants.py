@@ -30,7 +30,6 @@ def main():
     ap.add_argument("--layout", default="auto")
     ap.add_argument("--split", default="-1", help="comma list of CC_OPT_SPLIT_SWEEP (-1 auto)")
     ap.add_argument("--rebuild", default="-1", help="comma list of CC_OPT_SPLIT_REBUILD (-1 auto)")
-    ap.add_argument("--queue", default="1", help="comma list of CC_OPT_BITS_QUEUE")
     args = ap.parse_args()
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
@@ -39,14 +38,12 @@ def main():
     layout = engine.resolve_layout(args.layout, m, n)
     engine.apply_layout(ctx, layout)
     sched = make_schedule("c2")
-    combos = [(v, c_, sp, rb, qu) for v in [int(x) for x in args.variants.split(",")]
+    combos = [(v, c_, sp, rb) for v in [int(x) for x in args.variants.split(",")]
               for c_ in [int(x) for x in args.ctas.split(",")]
               for sp in [int(x) for x in args.split.split(",")]
-              for rb in [int(x) for x in args.rebuild.split(",")]
-              for qu in [int(x) for x in args.queue.split(",")]]
-    for var, ctas, split, rebuild, queue in combos:
+              for rb in [int(x) for x in args.rebuild.split(",")]]
+    for var, ctas, split, rebuild in combos:
         if True:
-            ctx.set_option(_lib.CC_OPT_BITS_QUEUE, queue)
             ctx.set_option(_lib.CC_OPT_SPLIT_SWEEP, split)
             ctx.set_option(_lib.CC_OPT_SPLIT_REBUILD, rebuild)
             ctx.set_option(_lib.CC_OPT_SWEEP_VARIANT, var)
@@ -63,7 +60,7 @@ def main():
             b_sweep = 8 * m + 4 * n
             med = statistics.median(s1)
             print(json.dumps({"scale": args.scale, "layout": layout, "variant": var,
-                              "ctas": ctas, "split": split, "rebuild": rebuild, "queue": queue, "sweep1_ms": round(med, 3),
+                              "ctas": ctas, "split": split, "rebuild": rebuild, "sweep1_ms": round(med, 3),
                               "sweep1_all": [round(x, 2) for x in s1],
                               "run_ms": [round(x, 2) for x in run], "sweeps": sweeps,
                               "frac": round(b_sweep / (med * 1e-3) / 6.55e12, 4),
