@@ -224,6 +224,9 @@ int cc_reorder_edges(cc_ctx* ctx, int mode);
                                       is rebuilt from the current labels before every group of
                                       that many windows; 0 = one bitmap for all; -1 = auto,
                                       the default: 3/16 of the windows) */
+#define CC_OPT_SPLIT_MASK 26        /* split sweep 1, explicit schedule: bit w set = a bitmap part
+                                      starts at L2 window w (the lowest set bit ends the tiled
+                                      part); 0 (default) = use the two options above */
 #define CC_OPT_LINK_PACK 22        /* pageable host edges: 1 (default) = rows cross PCIe as
                                       ceil(2 log2(n) / 8) in {6, 7} bytes (u | v << log2 n)
                                       when that is under 8; 0 = uint32 pairs */

@@ -34,6 +34,7 @@ CC_OPT_CHECK_PACK = 21
 CC_OPT_LINK_PACK = 22
 CC_OPT_SPLIT_SWEEP = 23
 CC_OPT_SPLIT_REBUILD = 24
+CC_OPT_SPLIT_MASK = 26
 STORE_PLAIN, STORE_RED, STORE_CHECK_PLAIN, STORE_CHECK_RED = 0, 1, 2, 3
 
 _I64P = ctypes.POINTER(ctypes.c_int64)

@@ -931,6 +931,9 @@ int cc_set_option(cc_ctx* c, int option, int64_t value) {
             c->flat_bits = (int)value;
             c->loop_key.m = -1;
             return CC_OK;
+        case CC_OPT_SPLIT_MASK:
+            c->split_mask = (uint64_t)value;
+            return CC_OK;
         case CC_OPT_SPLIT_REBUILD:
             if (value < -1 || value > kMaxTiles) return fail(CC_EINVAL, "split rebuild out of range");
             c->split_rebuild = (int)value;

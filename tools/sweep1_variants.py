@@ -30,6 +30,8 @@ def main():
     ap.add_argument("--layout", default="auto")
     ap.add_argument("--split", default="-1", help="comma list of CC_OPT_SPLIT_SWEEP (-1 auto)")
     ap.add_argument("--rebuild", default="-1", help="comma list of CC_OPT_SPLIT_REBUILD (-1 auto)")
+    ap.add_argument("--masks", default="", help="';'-separated lists of bitmap-part start windows "
+                    "(CC_OPT_SPLIT_MASK), e.g. 4,6,8,11;3,5,8,12")
     args = ap.parse_args()
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
@@ -42,8 +44,14 @@ def main():
               for c_ in [int(x) for x in args.ctas.split(",")]
               for sp in [int(x) for x in args.split.split(",")]
               for rb in [int(x) for x in args.rebuild.split(",")]]
-    for var, ctas, split, rebuild in combos:
+    masks = [sum(1 << int(w) for w in grp.split(",")) for grp in args.masks.split(";") if grp]
+    if masks:
+        combos = [(combos[0][0], combos[0][1], -1, -1, mk) for mk in masks]
+    else:
+        combos = [cb + (0,) for cb in combos]
+    for var, ctas, split, rebuild, mask in combos:
         if True:
+            ctx.set_option(_lib.CC_OPT_SPLIT_MASK, mask)
             ctx.set_option(_lib.CC_OPT_SPLIT_SWEEP, split)
             ctx.set_option(_lib.CC_OPT_SPLIT_REBUILD, rebuild)
             ctx.set_option(_lib.CC_OPT_SWEEP_VARIANT, var)
@@ -60,7 +68,8 @@ def main():
             b_sweep = 8 * m + 4 * n
             med = statistics.median(s1)
             print(json.dumps({"scale": args.scale, "layout": layout, "variant": var,
-                              "ctas": ctas, "split": split, "rebuild": rebuild, "sweep1_ms": round(med, 3),
+                              "ctas": ctas, "split": split, "rebuild": rebuild,
+                              "mask": [w for w in range(64) if (mask >> w) & 1], "sweep1_ms": round(med, 3),
                               "sweep1_all": [round(x, 2) for x in s1],
                               "run_ms": [round(x, 2) for x in run], "sweeps": sweeps,
                               "frac": round(b_sweep / (med * 1e-3) / 6.55e12, 4),
