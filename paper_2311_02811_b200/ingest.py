@@ -129,6 +129,10 @@ def _parse_device(h: _Ingest, buf, mode: int, bound: int = 0):
     vp = vals.ctypes.data_as(_lib._I64P)
     if hasattr(buf, "data_ptr") and getattr(buf, "is_cuda", False):
         import torch
+        if buf.dtype != torch.uint8 or not buf.is_contiguous():
+            raise ValueError("text on the device must be a contiguous uint8 CUDA tensor")
+        if buf.device.index != h.device:
+            buf = buf.to(torch.device("cuda", h.device))
         torch.cuda.current_stream(buf.device).synchronize()
         rc = h.lib.cc_ingest_parse_device(h.handle, ctypes.c_void_p(buf.data_ptr()), buf.numel(),
                                           mode, bound, 1, ctypes.byref(m), ctypes.byref(line),
