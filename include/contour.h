@@ -81,7 +81,8 @@ int cc_version(void);
 /* Staged-layout facts for measurement (bench.py's rooflines): out[0] layout
  * code, out[1] check-copy format (-1 none, 0 8-byte rows, 1 6-byte rows, 2
  * delta-packed groups), out[2] bytes one pass over the check copy streams,
- * out[3] work items, out[4] staged rows; the first `count` entries are written. */
+ * out[3] work items, out[4] staged rows, out[5] / out[6] rows and bytes of the
+ * canonical check copy (0 if none); the first `count` entries are written. */
 int cc_layout_info(cc_ctx* ctx, int64_t* out, int count);
 
 /* ---- staging: the Graph input contract (graph.py:57-90, engine.py:268-270) ----
@@ -227,6 +228,10 @@ int cc_reorder_edges(cc_ctx* ctx, int mode);
 #define CC_OPT_SPLIT_MASK 26        /* split sweep 1, explicit schedule: bit w set = a bitmap part
                                       starts at L2 window w (the lowest set bit ends the tiled
                                       part); 0 (default) = use the two options above */
+#define CC_OPT_CANON_CHECK 27       /* layout 6: 1 (default) = also build a copy with each
+                                      undirected pair once (canonical, de-duplicated; kept only
+                                      if under 55 % of the rows) for the early check, which then
+                                      runs on its own instead of folded into a bitmap sweep */
 #define CC_OPT_LINK_PACK 22        /* pageable host edges: 1 (default) = rows cross PCIe as
                                       ceil(2 log2(n) / 8) in {6, 7} bytes (u | v << log2 n)
                                       when that is under 8; 0 = uint32 pairs */

@@ -91,9 +91,10 @@ int cc_version(void) { return 1; }
 int cc_layout_info(cc_ctx* c, int64_t* out, int count) {
     if (!c || !out || count < 1) return fail(CC_EINVAL, "cc_layout_info: invalid argument");
     std::lock_guard<std::mutex> lk(c->mu);
-    const int64_t v[5] = {c->layout, c->layout == 6 ? (c->check_dp ? 2 : c->check_sbits ? 1 : 0) : -1,
-                          c->layout == 6 ? c->check_bytes : 0, c->n_items, c->m};
-    for (int i = 0; i < count && i < 5; ++i) out[i] = v[i];
+    const int64_t v[7] = {c->layout, c->layout == 6 ? (c->check_dp ? 2 : c->check_sbits ? 1 : 0) : -1,
+                          c->layout == 6 ? c->check_bytes : 0, c->n_items, c->m,
+                          c->citems ? c->canon_rows : 0, c->citems ? c->canon_bytes : 0};
+    for (int i = 0; i < count && i < 7; ++i) out[i] = v[i];
     return CC_OK;
 }
 
@@ -146,6 +147,9 @@ void cc_destroy(cc_ctx* c) {
     cudaFree(c->bdst16);
     cudaFree(c->bits);
     cudaFree(c->cgbase);
+    cudaFree(c->cwords);
+    cudaFree(c->cgb);
+    cudaFree(c->citems);
     cudaFree(c->dr0);
     cudaFree(c->rlab);
     cudaFree(c->rorig);
@@ -930,6 +934,9 @@ int cc_set_option(cc_ctx* c, int option, int64_t value) {
             if (value < 0 || value > 2) return fail(CC_EINVAL, "flat bits must be 0, 1 or 2");
             c->flat_bits = (int)value;
             c->loop_key.m = -1;
+            return CC_OK;
+        case CC_OPT_CANON_CHECK:
+            c->canon_check = value != 0;
             return CC_OK;
         case CC_OPT_SPLIT_MASK:
             c->split_mask = (uint64_t)value;

@@ -837,6 +837,48 @@ def test_split_sweep1_exact(split, rebuild):
     ctx.close()
 
 
+@pytest.mark.parametrize("canon", [1, 0])
+def test_canonical_check_copy(canon):
+    """The early check over the canonical copy (each undirected pair once,
+    CC_OPT_CANON_CHECK) decides exactly as early_convergence_check
+    (engine.py:331-348) on converged labels and single-cell perturbations,
+    and whole runs (graph loop, where the check is then not folded into a
+    bitmap sweep, and host loop) stay exact.  A symmetrised RMAT graph gets
+    the copy (< 55 % of the rows); a one-orientation grid does not."""
+    rng = np.random.default_rng(11)
+    ctx = _lib.Context(0)
+    ctx.set_option(_lib.CC_OPT_TILE_SHIFT, 16)
+    ctx.set_option(_lib.CC_OPT_CHECK_SHIFT, 16)
+    ctx.set_option(_lib.CC_OPT_CANON_CHECK, canon)
+    for n, e, sym in ((*graphgen.rmat(19, 16, 3), True), (*graphgen.grid(700, 900, 0.55, 5), False)):
+        exp = oracle.rem_union_find(n, e)
+        engine.stage_graph(ctx, n, e, "l2_tiled_check")
+        info = ctx.layout_info()
+        if canon and sym:
+            assert 0 < info["canon_rows"] < 0.55 * e.shape[0]
+            canon_pairs = np.unique(np.stack([e.min(axis=1), e.max(axis=1)], 1)[e[:, 0] != e[:, 1]],
+                                    axis=0)
+            assert info["canon_rows"] == canon_pairs.shape[0]
+        else:
+            assert info["canon_rows"] == 0
+        for host_loop in (False, True):
+            for count in (False, True):
+                labels = np.empty(n, dtype=np.int64)
+                _, st = engine.run_staged(ctx, make_schedule("c2"), count_changes=count,
+                                          host_loop=host_loop, labels_out=labels)
+                assert np.array_equal(labels, exp), (n, host_loop, count)
+                check_invariants(labels, st)
+        for _ in range(6):
+            lab = exp.copy()
+            x = int(rng.integers(1, n))
+            lab[x] = int(rng.integers(0, x))
+            _lib.check(ctx.lib.cc_write_labels(ctx.handle, lab.ctypes.data, 8))
+            assert engine.loop_check(ctx) == oracle.early_convergence_check(n, e, lab)
+        _lib.check(ctx.lib.cc_write_labels(ctx.handle, exp.ctypes.data, 8))
+        assert engine.loop_check(ctx)
+    ctx.close()
+
+
 @pytest.mark.parametrize("check_shift", [7, 9, 12])
 def test_bitmap_check_equals_oracle_early_check(check_shift):
     """The layout-6 early check (component bitmap + check copy) decides
