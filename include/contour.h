@@ -82,7 +82,9 @@ int cc_version(void);
  * code, out[1] check-copy format (-1 none, 0 8-byte rows, 1 6-byte rows, 2
  * delta-packed groups), out[2] bytes one pass over the check copy streams,
  * out[3] work items, out[4] staged rows, out[5] / out[6] rows and bytes of the
- * canonical check copy (0 if none); the first `count` entries are written. */
+ * canonical check copy (0 if none), out[7] its build status (0 built, 1 off or not
+ * applicable, 2 a window beyond 2^31 rows, 3 no memory, 4 not under 55 % of the rows,
+ * 5 a source gap overflow); the first `count` entries are written. */
 int cc_layout_info(cc_ctx* ctx, int64_t* out, int count);
 
 /* ---- staging: the Graph input contract (graph.py:57-90, engine.py:268-270) ----

@@ -200,11 +200,11 @@ class Context:
     def layout_info(self) -> dict:
         """cc_layout_info: layout code, check-copy format and bytes per pass."""
         import numpy as np
-        out = np.zeros(7, dtype=np.int64)
-        check(self.lib.cc_layout_info(self.handle, out.ctypes.data_as(_I64P), 7), "cc_layout_info")
+        out = np.zeros(8, dtype=np.int64)
+        check(self.lib.cc_layout_info(self.handle, out.ctypes.data_as(_I64P), 8), "cc_layout_info")
         return {"layout": int(out[0]), "check_format": int(out[1]), "check_bytes": int(out[2]),
                 "items": int(out[3]), "m": int(out[4]), "canon_rows": int(out[5]),
-                "canon_bytes": int(out[6])}
+                "canon_bytes": int(out[6]), "canon_status": int(out[7])}
 
     def close(self):
         if getattr(self, "handle", None):

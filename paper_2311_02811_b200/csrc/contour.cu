@@ -91,10 +91,11 @@ int cc_version(void) { return 1; }
 int cc_layout_info(cc_ctx* c, int64_t* out, int count) {
     if (!c || !out || count < 1) return fail(CC_EINVAL, "cc_layout_info: invalid argument");
     std::lock_guard<std::mutex> lk(c->mu);
-    const int64_t v[7] = {c->layout, c->layout == 6 ? (c->check_dp ? 2 : c->check_sbits ? 1 : 0) : -1,
+    const int64_t v[8] = {c->layout, c->layout == 6 ? (c->check_dp ? 2 : c->check_sbits ? 1 : 0) : -1,
                           c->layout == 6 ? c->check_bytes : 0, c->n_items, c->m,
-                          c->citems ? c->canon_rows : 0, c->citems ? c->canon_bytes : 0};
-    for (int i = 0; i < count && i < 7; ++i) out[i] = v[i];
+                          c->citems ? c->canon_rows : 0, c->citems ? c->canon_bytes : 0,
+                          c->canon_status};
+    for (int i = 0; i < count && i < 8; ++i) out[i] = v[i];
     return CC_OK;
 }
 

@@ -39,6 +39,7 @@ def main():
     n, m = graphgen.rmat_device(ctx, args.scale, 16, 1)
     layout = engine.resolve_layout(args.layout, m, n)
     engine.apply_layout(ctx, layout)
+    print(json.dumps({"layout_info": ctx.layout_info()}), flush=True)
     sched = make_schedule("c2")
     combos = [(v, c_, sp, rb) for v in [int(x) for x in args.variants.split(",")]
               for c_ in [int(x) for x in args.ctas.split(",")]
