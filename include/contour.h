@@ -84,7 +84,8 @@ int cc_version(void);
  * out[3] work items, out[4] staged rows, out[5] / out[6] rows and bytes of the
  * canonical check copy (0 if none), out[7] its build status (0 built, 1 off or not
  * applicable, 2 a window beyond 2^31 rows, 3 no memory, 4 not under 55 % of the rows,
- * 5 a source gap overflow); the first `count` entries are written. */
+ * 5 side table full), out[8] its groups kept with raw sources (side table); the
+ * first `count` entries are written. */
 int cc_layout_info(cc_ctx* ctx, int64_t* out, int count);
 
 /* ---- staging: the Graph input contract (graph.py:57-90, engine.py:268-270) ----
@@ -234,6 +235,9 @@ int cc_reorder_edges(cc_ctx* ctx, int mode);
                                       undirected pair once (canonical, de-duplicated; kept only
                                       if under 55 % of the rows) for the early check, which then
                                       runs on its own instead of folded into a bitmap sweep */
+#define CC_OPT_CANON_SPAN_BITS 28   /* tests: canonical-copy groups whose source span reaches
+                                      2^bits keep raw sources (side table); 0 (default) = only
+                                      spans beyond the 32 - check_shift offset bits */
 #define CC_OPT_LINK_PACK 22        /* pageable host edges: 1 (default) = rows cross PCIe as
                                       ceil(2 log2(n) / 8) in {6, 7} bytes (u | v << log2 n)
                                       when that is under 8; 0 = uint32 pairs */

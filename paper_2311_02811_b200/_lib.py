@@ -36,6 +36,7 @@ CC_OPT_SPLIT_SWEEP = 23
 CC_OPT_SPLIT_REBUILD = 24
 CC_OPT_SPLIT_MASK = 26
 CC_OPT_CANON_CHECK = 27
+CC_OPT_CANON_SPAN_BITS = 28
 STORE_PLAIN, STORE_RED, STORE_CHECK_PLAIN, STORE_CHECK_RED = 0, 1, 2, 3
 
 _I64P = ctypes.POINTER(ctypes.c_int64)
@@ -200,11 +201,12 @@ class Context:
     def layout_info(self) -> dict:
         """cc_layout_info: layout code, check-copy format and bytes per pass."""
         import numpy as np
-        out = np.zeros(8, dtype=np.int64)
-        check(self.lib.cc_layout_info(self.handle, out.ctypes.data_as(_I64P), 8), "cc_layout_info")
+        out = np.zeros(9, dtype=np.int64)
+        check(self.lib.cc_layout_info(self.handle, out.ctypes.data_as(_I64P), 9), "cc_layout_info")
         return {"layout": int(out[0]), "check_format": int(out[1]), "check_bytes": int(out[2]),
                 "items": int(out[3]), "m": int(out[4]), "canon_rows": int(out[5]),
-                "canon_bytes": int(out[6]), "canon_status": int(out[7])}
+                "canon_bytes": int(out[6]), "canon_status": int(out[7]),
+                "canon_side_groups": int(out[8])}
 
     def close(self):
         if getattr(self, "handle", None):

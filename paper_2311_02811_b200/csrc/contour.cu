@@ -91,11 +91,11 @@ int cc_version(void) { return 1; }
 int cc_layout_info(cc_ctx* c, int64_t* out, int count) {
     if (!c || !out || count < 1) return fail(CC_EINVAL, "cc_layout_info: invalid argument");
     std::lock_guard<std::mutex> lk(c->mu);
-    const int64_t v[8] = {c->layout, c->layout == 6 ? (c->check_dp ? 2 : c->check_sbits ? 1 : 0) : -1,
+    const int64_t v[9] = {c->layout, c->layout == 6 ? (c->check_dp ? 2 : c->check_sbits ? 1 : 0) : -1,
                           c->layout == 6 ? c->check_bytes : 0, c->n_items, c->m,
                           c->citems ? c->canon_rows : 0, c->citems ? c->canon_bytes : 0,
-                          c->canon_status};
-    for (int i = 0; i < count && i < 8; ++i) out[i] = v[i];
+                          c->canon_status, c->citems ? c->canon_side_groups : 0};
+    for (int i = 0; i < count && i < 9; ++i) out[i] = v[i];
     return CC_OK;
 }
 
@@ -150,6 +150,7 @@ void cc_destroy(cc_ctx* c) {
     cudaFree(c->cgbase);
     cudaFree(c->cwords);
     cudaFree(c->cgb);
+    cudaFree(c->cside);
     cudaFree(c->citems);
     cudaFree(c->dr0);
     cudaFree(c->rlab);
@@ -935,6 +936,10 @@ int cc_set_option(cc_ctx* c, int option, int64_t value) {
             if (value < 0 || value > 2) return fail(CC_EINVAL, "flat bits must be 0, 1 or 2");
             c->flat_bits = (int)value;
             c->loop_key.m = -1;
+            return CC_OK;
+        case CC_OPT_CANON_SPAN_BITS:
+            if (value < 0 || value > 31) return fail(CC_EINVAL, "span bits must be 0..31");
+            c->canon_span_bits = (int)value;
             return CC_OK;
         case CC_OPT_CANON_CHECK:
             c->canon_check = value != 0;

@@ -837,8 +837,8 @@ def test_split_sweep1_exact(split, rebuild):
     ctx.close()
 
 
-@pytest.mark.parametrize("canon", [1, 0])
-def test_canonical_check_copy(canon):
+@pytest.mark.parametrize("canon,span_bits", [(1, 0), (1, 7), (0, 0)])
+def test_canonical_check_copy(canon, span_bits):
     """The early check over the canonical copy (each undirected pair once,
     CC_OPT_CANON_CHECK) decides exactly as early_convergence_check
     (engine.py:331-348) on converged labels and single-cell perturbations,
@@ -850,6 +850,7 @@ def test_canonical_check_copy(canon):
     ctx.set_option(_lib.CC_OPT_TILE_SHIFT, 16)
     ctx.set_option(_lib.CC_OPT_CHECK_SHIFT, 16)
     ctx.set_option(_lib.CC_OPT_CANON_CHECK, canon)
+    ctx.set_option(_lib.CC_OPT_CANON_SPAN_BITS, span_bits)  # 7: most groups raw (side table)
     for n, e, sym in ((*graphgen.rmat(19, 16, 3), True), (*graphgen.grid(700, 900, 0.55, 5), False)):
         exp = oracle.rem_union_find(n, e)
         engine.stage_graph(ctx, n, e, "l2_tiled_check")
@@ -859,6 +860,7 @@ def test_canonical_check_copy(canon):
             canon_pairs = np.unique(np.stack([e.min(axis=1), e.max(axis=1)], 1)[e[:, 0] != e[:, 1]],
                                     axis=0)
             assert info["canon_rows"] == canon_pairs.shape[0]
+            assert (info["canon_side_groups"] > 0) == (span_bits > 0)
         else:
             assert info["canon_rows"] == 0
         for host_loop in (False, True):
