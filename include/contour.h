@@ -238,6 +238,8 @@ int cc_reorder_edges(cc_ctx* ctx, int mode);
 #define CC_OPT_CANON_SPAN_BITS 28   /* tests: canonical-copy groups whose source span reaches
                                       2^bits keep raw sources (side table); 0 (default) = only
                                       spans beyond the 32 - check_shift offset bits */
+#define CC_OPT_CANON_GROUP_WINDOWS 29 /* tests: L2 windows per build group of the canonical copy
+                                        (default 0 = up to 64, fewer if over 2^30 rows) */
 #define CC_OPT_LINK_PACK 22        /* pageable host edges: 1 (default) = rows cross PCIe as
                                       ceil(2 log2(n) / 8) in {6, 7} bytes (u | v << log2 n)
                                       when that is under 8; 0 = uint32 pairs */

@@ -937,6 +937,10 @@ int cc_set_option(cc_ctx* c, int option, int64_t value) {
             c->flat_bits = (int)value;
             c->loop_key.m = -1;
             return CC_OK;
+        case CC_OPT_CANON_GROUP_WINDOWS:
+            if (value < 0 || value > 64) return fail(CC_EINVAL, "group windows must be 0..64");
+            c->canon_group_windows = (int)value;
+            return CC_OK;
         case CC_OPT_CANON_SPAN_BITS:
             if (value < 0 || value > 31) return fail(CC_EINVAL, "span bits must be 0..31");
             c->canon_span_bits = (int)value;

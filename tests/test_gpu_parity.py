@@ -837,8 +837,9 @@ def test_split_sweep1_exact(split, rebuild):
     ctx.close()
 
 
-@pytest.mark.parametrize("canon,span_bits", [(1, 0), (1, 7), (0, 0)])
-def test_canonical_check_copy(canon, span_bits):
+@pytest.mark.parametrize("canon,span_bits,group_windows", [(1, 0, 0), (1, 7, 3), (1, 0, 1),
+                                                          (0, 0, 0)])
+def test_canonical_check_copy(canon, span_bits, group_windows):
     """The early check over the canonical copy (each undirected pair once,
     CC_OPT_CANON_CHECK) decides exactly as early_convergence_check
     (engine.py:331-348) on converged labels and single-cell perturbations,
@@ -851,6 +852,7 @@ def test_canonical_check_copy(canon, span_bits):
     ctx.set_option(_lib.CC_OPT_CHECK_SHIFT, 16)
     ctx.set_option(_lib.CC_OPT_CANON_CHECK, canon)
     ctx.set_option(_lib.CC_OPT_CANON_SPAN_BITS, span_bits)  # 7: most groups raw (side table)
+    ctx.set_option(_lib.CC_OPT_CANON_GROUP_WINDOWS, group_windows)  # several build groups
     for n, e, sym in ((*graphgen.rmat(19, 16, 3), True), (*graphgen.grid(700, 900, 0.55, 5), False)):
         exp = oracle.rem_union_find(n, e)
         engine.stage_graph(ctx, n, e, "l2_tiled_check")
