@@ -536,6 +536,17 @@ def run_single(args, device):
             "avg_launch_s": t_chk, "bytes_per_launch": b_sweep,
             "achieved": b_sweep / t_chk / 1e9, "frac": b_sweep / t_chk / 1e9 / peak,
             "traffic": traffic.get("check_dram_bytes_per_launch")}
+        info = ctx.layout_info()
+        if info.get("canon_rows"):
+            # layout 6: the check walks the canonical copy (each undirected pair once)
+            # + the label array (idempotence, bitmap) + the bitmap
+            bc = info["canon_bytes"] + 4 * n + n // 8
+            roofline["check_kernel"].update({
+                "kernel": "k_pick_root + k_bits_idem + k_check_bits_dp over the canonical check "
+                          "copy (each undirected pair once, delta-packed)",
+                "canonical_copy": {"rows": info["canon_rows"], "bytes": info["canon_bytes"],
+                                   "side_groups": info["canon_side_groups"]},
+                "streamed_bytes_per_launch": bc, "frac_streamed": bc / t_chk / 1e9 / peak})
     if rt2 and hybrid:  # hybrid layout: later sweeps run the shared-memory slice kernel
         t2 = sum(rt2) / len(rt2)
         b2 = 6 * m + 4 * n  # compact bucketed copy: 4 B src + 2 B dst offset per row
