@@ -108,11 +108,14 @@ def parse(argv=None):
                    help="use the edge-sharded driver even with one rank (plumbing check)")
     p.add_argument("--cadence", type=int, default=1,
                    help="local sweeps per MIN exchange in the NCCL-only sharded driver")
-    p.add_argument("--exchange", default="hybrid", choices=["hybrid", "peer", "nccl"],
-                   help="multi-GPU label exchange: hybrid (default: one all-reduce-MIN "
-                        "after the local sweep 1, then fused red.min into the peer replicas), "
-                        "peer (fused from the start, CUDA IPC) or nccl (all-reduce-MIN every "
-                        "--cadence local sweeps)")
+    p.add_argument("--exchange", default="checked", choices=["checked", "hybrid", "peer", "nccl"],
+                   help="multi-GPU label exchange: checked (default: each rank lays its shard "
+                        "out as one GPU would -- split sweep 1, bitmap sweeps, canonical "
+                        "check copy -- one all-reduce-MIN of the labels per sweep, the run "
+                        "ends when every shard's early check passes), hybrid (one "
+                        "all-reduce-MIN after the local sweep 1, then fused red.min into the "
+                        "peer replicas), peer (fused from the start, CUDA IPC) or nccl "
+                        "(all-reduce-MIN every --cadence local sweeps)")
     p.add_argument("--clock-interval-ms", type=int, default=100,
                    help="nvidia-smi sampling interval during the timed region")
     p.add_argument("--atomic", type=int, default=1,
@@ -713,6 +716,16 @@ def run_multi(args, rank, world, device):
     exchange = args.exchange
     keep_host = not args.no_e2e
     runner = None
+    if exchange == "checked":
+        runner = distributed.CheckedShardedContour.from_rmat(
+            spec["scale"], spec.get("edgefactor", 16), args.seed, rank, world, device,
+            layout=args.layout, atomic=atomic, keep_host=keep_host)
+        if dist.get_backend() == "gloo":
+            def gloo_min_checked(t):  # plumbing-check runs (ranks sharing a GPU)
+                c = t.cpu()
+                dist.all_reduce(c, op=dist.ReduceOp.MIN)
+                t.copy_(c)
+            runner.allreduce = gloo_min_checked
     if exchange in ("peer", "hybrid"):
         try:  # fused sweep + red.min into the peers' replicas (CUDA IPC over NVLink)
             cls = (distributed.HybridShardedContour if exchange == "hybrid"
@@ -819,7 +832,12 @@ def run_multi(args, rank, world, device):
                        f"sharded run; rank 0: labels -> int64 numpy; host clock, max over ranks"}
     fused = isinstance(runner, (distributed.FusedShardedContour,
                                 distributed.HybridShardedContour))
-    if isinstance(runner, distributed.HybridShardedContour):
+    if isinstance(runner, distributed.CheckedShardedContour):
+        sched = ("per sweep: the local sweep (sweep 1 split, later bitmap sweeps) + shortcut, "
+                 "all-reduce-MIN of the labels, the early check on each shard (canonical check "
+                 "copy) AND-ed by a 1-word MIN all-reduce")
+        launches = sum(2 + r * 20 for r in rounds)  # init + ~20 kernels per round + compress
+    elif isinstance(runner, distributed.HybridShardedContour):
         sched = ("round 1: local sweep + shortcut, all-reduce-MIN of the n+1 labels; later "
                  "rounds: fused sweep + red.min into the peer replicas (CUDA IPC / NVLink), "
                  "1-word MAX all-reduce")

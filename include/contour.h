@@ -138,6 +138,10 @@ int cc_init_labels(cc_ctx* ctx);
  * sync mode and a legal interleaving of it in async mode.  Leaves the
  * "wrote" flag on device; if wrote_out != NULL it is synchronously read back. */
 int cc_sweep(cc_ctx* ctx, int order, int sync, int atomic, int first, int* wrote_out);
+/* Asynchronous sweep number sweep_no (>= 1) of a host-driven run: on layout 6
+ * sweep 1 runs split (CC_OPT_SPLIT_SWEEP) and later order-2 sweeps as bitmap
+ * sweeps over the check copy, as inside cc_run. */
+int cc_sweep_numbered(cc_ctx* ctx, int order, int atomic, int64_t sweep_no, int* wrote_out);
 /* Staging-time edge layout (the analogue of the reference's CSR build at
  * Graph construction, graph.py:80,109-122): mode 0 keeps the input order,
  * mode 1 stably sorts all rows by src (radix sort on device, m < 2^31),

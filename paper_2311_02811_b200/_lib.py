@@ -82,6 +82,8 @@ SIGNATURES = {
     "cc_init_labels": (ctypes.c_int, [ctypes.c_void_p]),
     "cc_sweep": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                 ctypes.c_int, ctypes.POINTER(ctypes.c_int)]),
+    "cc_sweep_numbered": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
+                                         ctypes.c_int64, ctypes.POINTER(ctypes.c_int)]),
     "cc_reorder_edges": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
     "cc_set_option": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int64]),
     "cc_fold_flag": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),

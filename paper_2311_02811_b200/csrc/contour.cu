@@ -270,6 +270,24 @@ int cc_sweep(cc_ctx* c, int order, int sync, int atomic, int first, int* wrote_o
     return CC_OK;
 }
 
+// An asynchronous sweep that knows its place in the run (1-based): on layout
+// 6 sweep 1 is the split sweep and later order-2 sweeps the bitmap sweep over
+// the check copy, as in cc_run -- for drivers that loop on the host (the
+// multi-GPU CheckedShardedContour).
+int cc_sweep_numbered(cc_ctx* c, int order, int atomic, int64_t sweep_no, int* wrote_out) {
+    NvtxRange nvtx_("cc_sweep_numbered");
+    if (!c) return fail(CC_EINVAL, "null context");
+    if (sweep_no < 1) return fail(CC_EINVAL, "sweep number must be >= 1");
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard g(c->device);
+    CC_TRY(enqueue_sweep(c, order, 0, atomic, false, false, sweep_no));
+    if (wrote_out) {
+        CC_TRY(read_flags(c));
+        *wrote_out = c->hflags[kFlagWrote] != 0;
+    }
+    return CC_OK;
+}
+
 // Synchronous sweep split in two for the multi-GPU sync mode (SURVEY 8(e)
 // last bullet): phase 1 lowers a shadow copy of the labels from this
 // context's edge shard (read L, atomic min into the shadow); the caller then

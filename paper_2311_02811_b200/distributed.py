@@ -85,6 +85,19 @@ class CudaShard:
         _lib.check(self.ctx.lib.cc_sync_commit(self.ctx.handle, ctypes.byref(c)))
         return c.value
 
+    def sweep_numbered(self, order: int, sweep_no: int) -> None:
+        """Sweep number sweep_no of the run, laid out as cc_run would run it
+        (cc_sweep_numbered); returns after the sweep finished on the device."""
+        _lib.check(self.ctx.lib.cc_sweep_numbered(self.ctx.handle, order, int(self.atomic),
+                                                  sweep_no, None))
+
+    def loop_check(self) -> bool:
+        """The early check as the device loop runs it on this shard's layout
+        (cc_loop_check: the canonical / bitmap check copy where there is one)."""
+        ok = ctypes.c_int(0)
+        _lib.check(self.ctx.lib.cc_loop_check(self.ctx.handle, ctypes.byref(ok)))
+        return bool(ok.value)
+
     def check(self) -> bool:
         """early_convergence_check on this shard's edges (and every label's
         idempotence) -- all ranks' results AND-ed give the whole graph's."""
@@ -342,6 +355,7 @@ class ShardedContour(_HostIO):
         self.order_for = order_for
         self.cadence = max(1, int(cadence))
         self.allreduce = allreduce or nccl_allreduce_min(group)
+        self.group = group
         self.cap = n + 2 if cap is None else cap
         self.layout = "input"
         self.host_edges = None  # host copy of the shard (from_rmat keep_host)
@@ -390,6 +404,73 @@ class ShardedContour(_HostIO):
             if int(self.shard.labels[self.n].item()) == 1:
                 break
         self.shard.compress()
+        return rounds
+
+
+class CheckedShardedContour(ShardedContour):
+    """One exchange per sweep, ended by the early check instead of a no-write
+    round: each rank lays its shard out as one GPU would (``resolve_layout``
+    with row copies: on a dense graph beyond L2 the L2-window tiles + the
+    delta-packed check copy + the canonical check copy), sweeps it (sweep 1
+    split, later sweeps as bitmap sweeps, ``cc_sweep_numbered``), shortcuts,
+    all-reduces the replicas with MIN, then runs the early check on its own
+    rows (``cc_loop_check``: every edge of the shard agrees, every label is
+    idempotent) and the verdicts are AND-ed (a MIN all-reduce of 0/1).  The
+    replicas are identical after the MIN, so "every shard agrees" is the
+    whole graph's early check (engine.py:318-320): converged.  Rounds = sweeps."""
+
+    @classmethod
+    def from_rmat(cls, scale: int, edgefactor: int, seed: int, rank: int, world: int,
+                  device: int, layout: str = "auto", atomic: bool = True,
+                  keep_host: bool = False, **kw):
+        import torch
+
+        from .engine import LAYOUTS, resolve_layout
+        ctx = _lib.Context(device, torch.cuda.current_stream(device).cuda_stream)
+        n = 1 << scale
+        total = 2 * edgefactor * n
+        lo, hi = shard_rows(total, rank, world)
+        graphgen.rmat_device(ctx, scale, edgefactor, seed, row_lo=lo, row_hi=hi)
+        host = graphgen.read_edges(ctx, 8) if keep_host else None
+        layout = resolve_layout(layout, hi - lo, n)  # as one GPU would (row copies allowed)
+        if layout == "hybrid":
+            _lib.check(ctx.lib.cc_reorder_edges(ctx.handle, LAYOUTS["chunk_sorted"]))
+        if LAYOUTS[layout]:
+            _lib.check(ctx.lib.cc_reorder_edges(ctx.handle, LAYOUTS[layout]))
+        runner = cls(CudaShard(ctx, n, atomic), n, total, **kw)
+        runner.layout = layout
+        runner.host_edges = host
+        return runner
+
+    def stage_host(self, edges, layout: str = "auto") -> None:
+        """Stage this rank's host edge shard in the resident layout (with the
+        check copies, as from_rmat); the attached label buffer is kept."""
+        from .engine import stage_graph
+        stage_graph(self.shard.ctx, self.n, edges, layout)
+
+    def _and(self, ok: bool) -> bool:
+        import torch
+        import torch.distributed as dist
+        dev = "cpu" if dist.get_backend(self.group) == "gloo" else f"cuda:{self.shard.ctx.device}"
+        t = torch.tensor([1 if ok else 0], dtype=torch.int32, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN, group=self.group)
+        return bool(int(t.item()))
+
+    def run(self) -> int:
+        shard = self.shard
+        shard.init()
+        rounds = 0
+        while True:
+            rounds += 1
+            if rounds > self.cap:
+                from .errors import IterationCapExceeded
+                raise IterationCapExceeded(f"no convergence after {self.cap} sweeps")
+            shard.sweep_numbered(self.order_for(rounds), rounds)
+            shard.shortcut()
+            self.allreduce(shard.labels)
+            if self._and(shard.loop_check()):
+                break
+        shard.compress()
         return rounds
 
 

@@ -14,7 +14,8 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 from oracle import gen, oracle
-from paper_2311_02811_b200.distributed import ShardedContour, SyncShardedContour, shard_rows
+from paper_2311_02811_b200.distributed import (CheckedShardedContour, ShardedContour,
+                                               SyncShardedContour, shard_rows)
 
 
 class OracleShard:
@@ -65,6 +66,17 @@ class OracleShard:
         return oracle.early_convergence_check(self.n, self.edges,
                                               self.labels[: self.n].numpy().astype(np.int64))
 
+    # CheckedShardedContour: a numbered sweep, a shortcut pass, the loop check
+    def sweep_numbered(self, order, sweep_no):
+        self.sweep(order)
+
+    def shortcut(self):
+        lab = self.labels[: self.n].numpy()
+        lab[:] = lab[lab]
+
+    def loop_check(self):
+        return self.check()
+
     def compress(self):
         lab = self.labels[: self.n].numpy()
         rounds = 0
@@ -83,21 +95,28 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, cfg, cadence, q):
+def _worker(rank, world, port, cfg, cadence, q, checked=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         n, e = cfg
         lo, hi = shard_rows(e.shape[0], rank, world)
-        runner = ShardedContour(OracleShard(n, e[lo:hi]), n, e.shape[0], cadence=cadence)
+        cls = CheckedShardedContour if checked else ShardedContour
+        runner = cls(OracleShard(n, e[lo:hi]), n, e.shape[0], cadence=cadence)
         rounds = runner.run()
         q.put((rank, runner.shard.labels[:n].numpy().astype(np.int64), rounds))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("graph,cadence", [("rmat", 1), ("grid", 1), ("grid", 3), ("forest", 2)])
-def test_two_rank_gloo_matches_union_find(graph, cadence):
+@pytest.mark.parametrize("graph,cadence,checked", [("rmat", 1, False), ("grid", 1, False),
+                                                   ("grid", 3, False), ("forest", 2, False),
+                                                   ("rmat", 1, True), ("grid", 1, True),
+                                                   ("forest", 1, True)])
+def test_two_rank_gloo_matches_union_find(graph, cadence, checked):
+    """ShardedContour (no-write round ends the run) and CheckedShardedContour
+    (one MIN exchange per sweep, the AND of the shards' early checks ends
+    it) on two gloo ranks: exact labels, every rank stops at the same round."""
     if graph == "rmat":
         cfg = gen.rmat(10, 8, 3)
     elif graph == "grid":
@@ -110,7 +129,7 @@ def test_two_rank_gloo_matches_union_find(graph, cadence):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, cfg, cadence, q))
+    procs = [ctx.Process(target=_worker, args=(r, world, port, cfg, cadence, q, checked))
              for r in range(world)]
     for p in procs:
         p.start()
