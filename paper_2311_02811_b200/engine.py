@@ -457,8 +457,12 @@ def run_contour(g, schedule: Schedule, threads: int = 1, seed: Optional[int] = N
             want = resolve_layout(layout, m, n, resident=True)
             upgrade = None
             if want != staged:
-                # only layouts reachable from the staged order in place
-                upgrade = want if (staged, want) in (("chunk_sorted", "hybrid"),) else None
+                # only layouts reachable from the staged order in place (the
+                # L2-window tiles are built from rows in any order; the hybrid's
+                # bucketed copy needs the chunk-sorted rows)
+                upgrade = want if (staged, want) in (("chunk_sorted", "hybrid"),
+                                                     ("chunk_sorted", "l2_tiled_check"),
+                                                     ("chunk_sorted", "l2_tiled")) else None
             # a weak reference: the cache must not keep the caller's array alive
             ctx.staged = (weakref.ref(edges), n, layout, upgrade, _array_key(edges))
     return labels, stats

@@ -1144,6 +1144,33 @@ def test_pageable_link_packing(n):
             ctx.set_option(_lib.CC_OPT_LINK_PACK, 1)
 
 
+def test_frozen_edges_upgrade_to_the_tiles(monkeypatch):
+    """A read-only edge array whose labels exceed the L2 budget (forced small
+    here) is staged chunk-sorted by the first run_contour call (sweep 1
+    streamed behind the copy) and upgraded in place to the resident layout 6
+    (tiles, check copies, split sweep 1) by the second; every call exact."""
+    monkeypatch.setattr(engine, "AUTO_L2_LABEL_BYTES", 1 << 20)
+    n, e = graphgen.rmat(19, 16, 8)
+    e = np.ascontiguousarray(e)
+    exp = oracle.rem_union_find(n, e)
+    e.flags.writeable = False
+    ctx = engine._context(0)
+    ctx.set_option(_lib.CC_OPT_TILE_SHIFT, 16)
+    ctx.set_option(_lib.CC_OPT_CHECK_SHIFT, 16)
+    try:
+        layouts = []
+        for i in range(3):
+            labels, st = run_contour((n, e), make_schedule("c2"))
+            assert np.array_equal(labels, exp), i
+            check_invariants(labels, st)
+            layouts.append(ctx.layout_info()["layout"])
+        assert layouts[0] == 2 and layouts[1:] == [6, 6], layouts
+    finally:
+        ctx.set_option(_lib.CC_OPT_TILE_SHIFT, 24)
+        ctx.set_option(_lib.CC_OPT_CHECK_SHIFT, 20)
+        ctx.staged = None
+
+
 def test_frozen_edges_stay_resident():
     """run_contour on a read-only edge array (the reference's Graph freezes
     its arrays) reuses the graph staged by the previous call on the context,
