@@ -1164,7 +1164,7 @@ def test_frozen_edges_upgrade_to_the_tiles(monkeypatch):
             assert np.array_equal(labels, exp), i
             check_invariants(labels, st)
             layouts.append(ctx.layout_info()["layout"])
-        assert layouts[0] == 2 and layouts[1:] == [6, 6], layouts
+        assert layouts[0] in (0, 2) and layouts[1:] == [6, 6], layouts  # (0: input order + chunk sorts)
     finally:
         ctx.set_option(_lib.CC_OPT_TILE_SHIFT, 24)
         ctx.set_option(_lib.CC_OPT_CHECK_SHIFT, 20)
