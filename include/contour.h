@@ -244,6 +244,9 @@ int cc_reorder_edges(cc_ctx* ctx, int mode);
                                       spans beyond the 32 - check_shift offset bits */
 #define CC_OPT_CANON_GROUP_WINDOWS 29 /* tests: L2 windows per build group of the canonical copy
                                         (default 0 = up to 64, fewer if over 2^30 rows) */
+#define CC_OPT_RELABEL_INTERLEAVE 30 /* layout 7: rows of each 2^block-row block of the relabeled
+                                       copy interleaved with this stride (0 = off) */
+#define CC_OPT_RELABEL_BLOCK 31      /* layout 7: log2 rows per interleave block (default 24) */
 #define CC_OPT_LINK_PACK 22        /* pageable host edges: 1 (default) = rows cross PCIe as
                                       ceil(2 log2(n) / 8) in {6, 7} bytes (u | v << log2 n)
                                       when that is under 8; 0 = uint32 pairs */

@@ -955,6 +955,14 @@ int cc_set_option(cc_ctx* c, int option, int64_t value) {
             c->flat_bits = (int)value;
             c->loop_key.m = -1;
             return CC_OK;
+        case CC_OPT_RELABEL_INTERLEAVE:
+            if (value < 0 || value > 4096) return fail(CC_EINVAL, "interleave must be 0..4096");
+            c->relabel_interleave = (int)value;
+            return CC_OK;
+        case CC_OPT_RELABEL_BLOCK:
+            if (value < 10 || value > 30) return fail(CC_EINVAL, "relabel block must be 10..30");
+            c->relabel_block = (int)value;
+            return CC_OK;
         case CC_OPT_CANON_GROUP_WINDOWS:
             if (value < 0 || value > 64) return fail(CC_EINVAL, "group windows must be 0..64");
             c->canon_group_windows = (int)value;
