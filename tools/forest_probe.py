@@ -30,7 +30,7 @@ def main():
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
     ctx = _lib.Context(0, stream.cuda_stream)
-    n, host = graphgen.make(spec, 1, elem_bytes=4)
+    n, host = graphgen.make(spec, 1, elem_bytes=8)
     engine.stage_graph(ctx, n, host, "input")
     del host
     sched = make_schedule("c2")
