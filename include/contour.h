@@ -247,6 +247,8 @@ int cc_reorder_edges(cc_ctx* ctx, int mode);
 #define CC_OPT_RELABEL_INTERLEAVE 30 /* layout 7: rows of each 2^block-row block of the relabeled
                                        copy interleaved with this stride (0 = off) */
 #define CC_OPT_RELABEL_BLOCK 31      /* layout 7: log2 rows per interleave block (default 24) */
+#define CC_OPT_SPLIT_SHORTCUT 32    /* split sweep 1: pointer-jumping passes before each bitmap
+                                      part (more rows decided by the bitmap) */
 #define CC_OPT_LINK_PACK 22        /* pageable host edges: 1 (default) = rows cross PCIe as
                                       ceil(2 log2(n) / 8) in {6, 7} bytes (u | v << log2 n)
                                       when that is under 8; 0 = uint32 pairs */

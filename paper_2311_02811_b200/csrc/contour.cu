@@ -974,6 +974,10 @@ int cc_set_option(cc_ctx* c, int option, int64_t value) {
         case CC_OPT_CANON_CHECK:
             c->canon_check = value != 0;
             return CC_OK;
+        case CC_OPT_SPLIT_SHORTCUT:
+            if (value < 0 || value > 4) return fail(CC_EINVAL, "split shortcut must be 0..4");
+            c->split_shortcut = (int)value;
+            return CC_OK;
         case CC_OPT_SPLIT_MASK:
             c->split_mask = (uint64_t)value;
             return CC_OK;

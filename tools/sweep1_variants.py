@@ -30,6 +30,7 @@ def main():
     ap.add_argument("--layout", default="auto")
     ap.add_argument("--split", default="-1", help="comma list of CC_OPT_SPLIT_SWEEP (-1 auto)")
     ap.add_argument("--rebuild", default="-1", help="comma list of CC_OPT_SPLIT_REBUILD (-1 auto)")
+    ap.add_argument("--shortcut", type=int, default=-1, help="CC_OPT_SPLIT_SHORTCUT (-1: default)")
     ap.add_argument("--masks", default="", help="';'-separated lists of bitmap-part start windows "
                     "(CC_OPT_SPLIT_MASK), e.g. 4,6,8,11;3,5,8,12")
     args = ap.parse_args()
@@ -40,6 +41,8 @@ def main():
     layout = engine.resolve_layout(args.layout, m, n)
     engine.apply_layout(ctx, layout)
     print(json.dumps({"layout_info": ctx.layout_info()}), flush=True)
+    if args.shortcut >= 0:
+        ctx.set_option(_lib.CC_OPT_SPLIT_SHORTCUT, args.shortcut)
     sched = make_schedule("c2")
     combos = [(v, c_, sp, rb) for v in [int(x) for x in args.variants.split(",")]
               for c_ in [int(x) for x in args.ctas.split(",")]
