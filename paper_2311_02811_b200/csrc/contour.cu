@@ -880,6 +880,7 @@ int cc_fastsv(cc_ctx* c, int64_t cap, void* labels_out, int out_eb, cc_stats* st
 int cc_set_option(cc_ctx* c, int option, int64_t value) {
     if (!c) return fail(CC_EINVAL, "null context");
     std::lock_guard<std::mutex> lk(c->mu);
+    ++c->opt_epoch;  // any option may change what the captured graph loop launches
     switch (option) {
         case CC_OPT_STORE_MODE_PLAIN:
         case CC_OPT_STORE_MODE_ATOMIC:
