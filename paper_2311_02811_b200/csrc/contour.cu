@@ -880,7 +880,8 @@ int cc_fastsv(cc_ctx* c, int64_t cap, void* labels_out, int out_eb, cc_stats* st
 int cc_set_option(cc_ctx* c, int option, int64_t value) {
     if (!c) return fail(CC_EINVAL, "null context");
     std::lock_guard<std::mutex> lk(c->mu);
-    ++c->opt_epoch;  // any option may change what the captured graph loop launches
+    // any option but the staging layout may change what the captured graph loop launches
+    if (option != CC_OPT_STAGE_LAYOUT) ++c->opt_epoch;
     switch (option) {
         case CC_OPT_STORE_MODE_PLAIN:
         case CC_OPT_STORE_MODE_ATOMIC:
