@@ -249,6 +249,11 @@ int cc_reorder_edges(cc_ctx* ctx, int mode);
 #define CC_OPT_RELABEL_BLOCK 31      /* layout 7: log2 rows per interleave block (default 24) */
 #define CC_OPT_SPLIT_SHORTCUT 32    /* split sweep 1: pointer-jumping passes before each bitmap
                                       part (more rows decided by the bitmap) */
+#define CC_OPT_CANON_SWEEP 33      /* layout 6, when the canonical copy was built: 1 (default) =
+                                      the whole-graph bitmap sweeps (sweep 2 on) walk it, each
+                                      undirected pair once; 2 = the split sweep 1's bitmap parts
+                                      too; 0 = every bitmap sweep walks the dst-bucketed check
+                                      copy (every row) */
 #define CC_OPT_LINK_PACK 22        /* pageable host edges: 1 (default) = rows cross PCIe as
                                       ceil(2 log2(n) / 8) in {6, 7} bytes (u | v << log2 n)
                                       when that is under 8; 0 = uint32 pairs */

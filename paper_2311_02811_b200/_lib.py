@@ -41,6 +41,7 @@ CC_OPT_CANON_GROUP_WINDOWS = 29
 CC_OPT_RELABEL_INTERLEAVE = 30
 CC_OPT_RELABEL_BLOCK = 31
 CC_OPT_SPLIT_SHORTCUT = 32
+CC_OPT_CANON_SWEEP = 33
 STORE_PLAIN, STORE_RED, STORE_CHECK_PLAIN, STORE_CHECK_RED = 0, 1, 2, 3
 
 _I64P = ctypes.POINTER(ctypes.c_int64)

@@ -1011,6 +1011,10 @@ int cc_set_option(cc_ctx* c, int option, int64_t value) {
                 return fail(CC_EINVAL, "check shift must be in [7, 20] (<= 128 KB of bits)");
             c->check_shift = (int)value;
             return CC_OK;
+        case CC_OPT_CANON_SWEEP:
+            if (value < 0 || value > 2) return fail(CC_EINVAL, "canon sweep must be 0, 1 or 2");
+            c->canon_sweep = (int)value;
+            return CC_OK;
         case CC_OPT_WARP_TRANSPOSE:
             c->warp_transpose = value != 0;
             return CC_OK;

@@ -807,14 +807,21 @@ def test_packed_check_copy_exact(check_shift, pack):
     ctx.close()
 
 
-@pytest.mark.parametrize("split,rebuild", [(1, 0), (3, 1), (5, 2), (-1, -1), (7, 3), (0, 0)])
-def test_split_sweep1_exact(split, rebuild):
+@pytest.mark.parametrize("split,rebuild,canon", [(1, 0, 1), (3, 1, 1), (5, 2, 1), (-1, -1, 1),
+                                                (7, 3, 1), (0, 0, 1), (-1, -1, 0), (3, 1, 0),
+                                                (-1, -1, 2), (5, 2, 2)])
+def test_split_sweep1_exact(split, rebuild, canon):
     """Sweep 1 on layout 6 split at an L2 window (CC_OPT_SPLIT_SWEEP): the
     first windows on the tiles, the rest as bitmap sweeps over the check copy
     with the bitmap rebuilt every `rebuild` windows -- labels equal the oracle's
     for async / counted / host-loop / graph-loop runs and C-m, on RMAT (dense,
-    where auto splits) and a grid (sparse), 8-10 windows of 2^16 vertices."""
+    where auto splits) and a grid (sparse), 8-10 windows of 2^16 vertices.
+    canon (CC_OPT_CANON_SWEEP): the whole-graph bitmap sweeps (1, the
+    default) or also the split parts (2) walk the canonical copy (each
+    undirected pair once; built for the symmetrised RMAT graphs), or every
+    bitmap sweep walks the dst-bucketed check copy (0)."""
     ctx = _lib.Context(0)
+    ctx.set_option(_lib.CC_OPT_CANON_SWEEP, canon)
     ctx.set_option(_lib.CC_OPT_TILE_SHIFT, 16)
     ctx.set_option(_lib.CC_OPT_CHECK_SHIFT, 16)
     ctx.set_option(_lib.CC_OPT_ITEM_ROWS, 20000)
