@@ -557,20 +557,27 @@ def run_single(args, device):
             "kernel": "cck::k_sweep_slice (dst-bucketed copy, dst labels in shared memory)",
             "avg_launch_s": t2, "frac_of_B_sweep": b_sweep / t2 / 1e9 / peak,
             "streamed_bytes_per_launch": b2, "frac_streamed": b2 / t2 / 1e9 / peak}
-    elif rt2:  # layout 6: later sweeps are the bitmap sweep over the check copy
+    elif rt2:  # layout 6: later sweeps are the bitmap sweep over a row copy
         t2 = sum(rt2) / len(rt2)
-        # the check copy as staged (cc_layout_info: delta-packed groups, 4.03 B
-        # per row; or 6 / 8 B rows) + the bitmap + the vertex pass's label read
+        # the copy it walks as staged (cc_layout_info): the canonical copy (each
+        # undirected pair once, CC_OPT_CANON_SWEEP default) when it was built,
+        # else the dst-bucketed check copy (delta-packed groups, 4.03 B per
+        # row; or 6 / 8 B rows) + the bitmap + the vertex pass's label read
         info = ctx.layout_info()
-        b2 = info["check_bytes"] + n // 8 + 4 * n
+        canon = bool(info.get("canon_rows"))
+        cb = info["canon_bytes"] if canon else info["check_bytes"]
+        b2 = cb + n // 8 + 4 * n
         roofline["bitmap_sweep_kernel"] = {
-            "kernel": "k_pick_root + k_bits_idem + k_sweep_bits[_dp] (dst-bucketed check copy, "
-                      "component bitmap; rows both of whose ends carry the root label are "
-                      "decided without label gathers)",
+            "kernel": "k_pick_root + k_bits_idem + k_sweep_bits_dp over the "
+                      + ("canonical copy (each undirected pair once; the operator is symmetric "
+                         "in u, v)" if canon else "dst-bucketed check copy")
+                      + ", component bitmap; rows both of whose ends carry the root label are "
+                        "decided without label gathers",
             "check_copy": {"format": {2: "delta-packed 128-row groups", 1: "6-byte rows",
                                       0: "8-byte rows"}.get(info["check_format"]),
                            "bytes": info["check_bytes"],
                            "bytes_per_row": round(info["check_bytes"] / max(m, 1), 3)},
+            "walks": "canonical copy" if canon else "check copy",
             "avg_launch_s": t2, "frac_of_B_sweep": b_sweep / t2 / 1e9 / peak,
             "streamed_bytes_per_launch": b2, "frac_streamed": b2 / t2 / 1e9 / peak,
             "launch_ms": [round(t * 1e3, 4) for t in rt2]}
