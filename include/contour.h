@@ -254,6 +254,17 @@ int cc_reorder_edges(cc_ctx* ctx, int mode);
                                       undirected pair once; 2 = the split sweep 1's bitmap parts
                                       too; 0 = every bitmap sweep walks the dst-bucketed check
                                       copy (every row) */
+#define CC_OPT_CHECK_UNITE 35      /* layout 6 with a delta-packed copy, asynchronous C-2 runs
+                                      without exact counts: the early check after a changing
+                                      sweep unites the trees of every row whose labels differ
+                                      (root hooking) instead of failing, and pointer jumping
+                                      finishes the labels -- the check pass is the last pass
+                                      over the rows (DESIGN 5.32); 0 = the plain check */
+#define CC_OPT_BITS_PUBLISH 34     /* layout 6, delta-packed copies: the bitmap sweeps set a
+                                      vertex's bit as soon as a row leaves it at the root label
+                                      (later rows of that vertex are decided by the bitmap
+                                      again): 1 = in the split sweep 1's parts, 2 = in every
+                                      bitmap sweep, 0 = the bitmap stays as built */
 #define CC_OPT_LINK_PACK 22        /* pageable host edges: 1 (default) = rows cross PCIe as
                                       ceil(2 log2(n) / 8) in {6, 7} bytes (u | v << log2 n)
                                       when that is under 8; 0 = uint32 pairs */

@@ -42,6 +42,8 @@ CC_OPT_RELABEL_INTERLEAVE = 30
 CC_OPT_RELABEL_BLOCK = 31
 CC_OPT_SPLIT_SHORTCUT = 32
 CC_OPT_CANON_SWEEP = 33
+CC_OPT_BITS_PUBLISH = 34
+CC_OPT_CHECK_UNITE = 35
 STORE_PLAIN, STORE_RED, STORE_CHECK_PLAIN, STORE_CHECK_RED = 0, 1, 2, 3
 
 _I64P = ctypes.POINTER(ctypes.c_int64)

@@ -633,7 +633,12 @@ int run_impl(cc_ctx* c, const cc_schedule* s, int flags, int64_t cap, void* labe
             // the check kernels skip when the wrote word is 0; this sweep changed
             // labels (sync / count modes tell it by the diff count)
             CUDA_TRY(cudaMemsetAsync(c->dflags + kFlagWrote, 1, 1, c->stream));
-            CC_TRY(enqueue_loop_check(c, c->stream));
+            // (asynchronous runs without exact counts may unite disagreeing rows
+            // instead of failing, as the graph loop does: the check then always
+            // ends the loop and compress() below finishes the labels)
+            const bool unite = !sync && !count && unite_schedule(c, s);
+            CUDA_TRY(cudaMemsetAsync(c->dflags + kFlagUnite, 0, sizeof(int), c->stream));
+            CC_TRY(enqueue_loop_check(c, c->stream, unite));
             CC_TRY(read_flags(c));
             if (!c->hflags[kFlagCheck]) { converged_by = 1; break; }
         }
@@ -1014,6 +1019,13 @@ int cc_set_option(cc_ctx* c, int option, int64_t value) {
         case CC_OPT_CANON_SWEEP:
             if (value < 0 || value > 2) return fail(CC_EINVAL, "canon sweep must be 0, 1 or 2");
             c->canon_sweep = (int)value;
+            return CC_OK;
+        case CC_OPT_CHECK_UNITE:
+            c->check_unite = value != 0;
+            return CC_OK;
+        case CC_OPT_BITS_PUBLISH:
+            if (value < 0 || value > 2) return fail(CC_EINVAL, "bits publish must be 0, 1 or 2");
+            c->bits_publish = (int)value;
             return CC_OK;
         case CC_OPT_WARP_TRANSPOSE:
             c->warp_transpose = value != 0;

@@ -807,10 +807,11 @@ def test_packed_check_copy_exact(check_shift, pack):
     ctx.close()
 
 
-@pytest.mark.parametrize("split,rebuild,canon", [(1, 0, 1), (3, 1, 1), (5, 2, 1), (-1, -1, 1),
-                                                (7, 3, 1), (0, 0, 1), (-1, -1, 0), (3, 1, 0),
-                                                (-1, -1, 2), (5, 2, 2)])
-def test_split_sweep1_exact(split, rebuild, canon):
+@pytest.mark.parametrize("split,rebuild,canon,publish",
+                         [(1, 0, 1, 0), (3, 1, 1, 0), (5, 2, 1, 0), (-1, -1, 1, 0), (7, 3, 1, 0),
+                          (0, 0, 1, 0), (-1, -1, 0, 0), (3, 1, 0, 0), (-1, -1, 2, 0), (5, 2, 2, 0),
+                          (-1, -1, 1, 1), (3, 1, 1, 2), (1, 0, 2, 2), (5, 2, 0, 1), (-1, -1, 1, 2)])
+def test_split_sweep1_exact(split, rebuild, canon, publish):
     """Sweep 1 on layout 6 split at an L2 window (CC_OPT_SPLIT_SWEEP): the
     first windows on the tiles, the rest as bitmap sweeps over the check copy
     with the bitmap rebuilt every `rebuild` windows -- labels equal the oracle's
@@ -819,9 +820,12 @@ def test_split_sweep1_exact(split, rebuild, canon):
     canon (CC_OPT_CANON_SWEEP): the whole-graph bitmap sweeps (1, the
     default) or also the split parts (2) walk the canonical copy (each
     undirected pair once; built for the symmetrised RMAT graphs), or every
-    bitmap sweep walks the dst-bucketed check copy (0)."""
+    bitmap sweep walks the dst-bucketed check copy (0).
+    publish (CC_OPT_BITS_PUBLISH): the bitmap sweeps of the split parts (1) or
+    all of them (2) set a vertex's bit when a row leaves it at the root label."""
     ctx = _lib.Context(0)
     ctx.set_option(_lib.CC_OPT_CANON_SWEEP, canon)
+    ctx.set_option(_lib.CC_OPT_BITS_PUBLISH, publish)
     ctx.set_option(_lib.CC_OPT_TILE_SHIFT, 16)
     ctx.set_option(_lib.CC_OPT_CHECK_SHIFT, 16)
     ctx.set_option(_lib.CC_OPT_ITEM_ROWS, 20000)
@@ -841,6 +845,65 @@ def test_split_sweep1_exact(split, rebuild, canon):
                     assert np.array_equal(labels, exp), (n, sched, count, host_loop)
                     check_invariants(labels, st)
         assert engine.verify_staged(ctx) == 0
+    ctx.close()
+
+
+@pytest.mark.parametrize("split,canon,publish", [(-1, 1, 1), (1, 2, 1), (0, 0, 0), (3, 1, 2),
+                                                 (1, 1, 0)])
+def test_uniting_check_exact(split, canon, publish):
+    """CC_OPT_CHECK_UNITE: the early check after sweep 1 unites the trees of
+    every row whose labels differ (root hooking) and pointer jumping finishes
+    the labels, so an asynchronous C-2 run without exact counts always ends
+    after one sweep -- with labels equal to the oracle's (rem_union_find:
+    the minimum vertex of every component) on dense graphs (RMAT, where little
+    is left to unite), and on graphs one order-2 sweep leaves far from
+    converged: a grid, a forest of long paths, one permuted path of 300k
+    vertices (deep chains: many hooks, several compress passes), symmetrised
+    (canonical copy) or not.  Graph loop and host loop; synchronous and
+    counted runs keep the plain check and stay exact too."""
+    rng = np.random.default_rng(5)
+    ctx = _lib.Context(0)
+    ctx.set_option(_lib.CC_OPT_CHECK_UNITE, 1)
+    ctx.set_option(_lib.CC_OPT_CANON_SWEEP, canon)
+    ctx.set_option(_lib.CC_OPT_BITS_PUBLISH, publish)
+    ctx.set_option(_lib.CC_OPT_TILE_SHIFT, 16)
+    ctx.set_option(_lib.CC_OPT_CHECK_SHIFT, 16)
+    ctx.set_option(_lib.CC_OPT_ITEM_ROWS, 20000)
+    ctx.set_option(_lib.CC_OPT_SPLIT_SWEEP, split)
+    npath = 300_000
+    perm = rng.permutation(npath)
+    path = np.stack([perm[:-1], perm[1:]], 1).astype(np.int64)
+    sym = lambda e: np.concatenate([e, e[:, ::-1]])
+    # a forest of 400 paths over 60k permuted IDs (+ isolated vertices), small
+    # enough that every 128-row group's source span fits the delta packing
+    fn = 65_000
+    fperm = rng.permutation(fn)[:60_000]
+    cuts = np.sort(rng.choice(np.arange(1, 60_000), 399, replace=False))
+    keep = np.ones(59_999, dtype=bool)
+    keep[cuts - 1] = False
+    fe = np.stack([fperm[:-1], fperm[1:]], 1)[keep].astype(np.int64)
+    graphs = [graphgen.rmat(19, 16, 2), graphgen.rmat(18, 4, 9),
+              graphgen.grid(700, 900, 0.55, 5), (npath, path), (npath, sym(path)),
+              (fn, fe), (fn, sym(fe))]
+    for n, e in graphs:
+        exp = oracle.rem_union_find(n, e)
+        engine.stage_graph(ctx, n, e, "l2_tiled_check")
+        assert ctx.layout_info()["check_format"] == 2, (n, ctx.layout_info())
+        for host_loop in (False, True):
+            for _ in range(2):
+                labels = np.empty(n, dtype=np.int64)
+                _, st = engine.run_staged(ctx, make_schedule("c2"), count_changes=False,
+                                          early_check=True, host_loop=host_loop,
+                                          labels_out=labels)
+                assert np.array_equal(labels, exp), (n, host_loop)
+                assert st.sweeps_executed == 1 and st.converged_by == "early-check"
+                assert engine.verify_staged(ctx) == 0
+        for sched, count in ((make_schedule("c2", sync=True), True), (make_schedule("c2"), True),
+                             (make_schedule("cm", 6), False)):
+            labels = np.empty(n, dtype=np.int64)
+            _, st = engine.run_staged(ctx, sched, count_changes=count, labels_out=labels)
+            assert np.array_equal(labels, exp), (n, sched, count)
+            check_invariants(labels, st)
     ctx.close()
 
 
