@@ -481,17 +481,41 @@ def run_single(args, device):
     if args.host_loop:  # iota + (sweep + shortcut + check) per sweep + compress
         launches = sum(2 + s.sweeps_executed * (1 + shortcut + check) for s in stats)
     elif layout == "l2_tiled_check":
-        # per loop iteration: tiled sweep (guarded) + root pick + bitmap pass + bitmap
-        # sweep (guarded) + shortcut + control; the bitmap sweep that passes as the
-        # early check is one iteration more than the sweeps it books
-        per = 1 + 3 + shortcut + 1
-        launches = sum(3 + (s.sweeps_executed + (s.converged_by == "early-check")) * per
-                       for s in stats)
+        # per loop iteration: sweep 1's tiled part + 3 kernels (root pick, bitmap
+        # pass, bitmap sweep) per bitmap part + the later sweeps' 3 (all order-
+        # guarded) + shortcut + the check's 3 + control; around the loop: init,
+        # compress (+ 3 x (gate, compress) after the uniting check), publish
+        li = ctx.layout_info()
+        per = (1 + 3 * li["split_parts"] if li["split_windows"] else 1) + 3 + shortcut + 3 + 1
+        around = 3 + (6 if li["uniting_check"] else 0)
+        launches = sum(around + s.sweeps_executed * per for s in stats)
     else:  # loop_init + (guarded sweeps + shortcut + check + control) per sweep + compress + publish
         per = (2 if hybrid else 1) + shortcut + check + 1
         launches = sum(3 + s.sweeps_executed * per for s in stats)
     sweep_ms_graph = engine.run_staged(ctx, sched, sweep_times=True, **kw)[1].sweep_seconds
     verify = engine.verify_staged(ctx)
+    run_info = ctx.layout_info()  # (sweep 1's split and the check of the timed runs)
+    # ---- the same runs with the plain early check (sweeps until it passes):
+    # what the uniting check (DESIGN 5.32) buys, on the same staged graph
+    plain = None
+    if run_info["uniting_check"]:
+        ctx.set_option(_lib.CC_OPT_CHECK_UNITE, 0)
+        engine.run_staged(ctx, sched, sweep_times=False, **kw)
+        p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        p0.record(stream)
+        pst = [engine.run_staged(ctx, sched, sweep_times=False, **kw)[1]
+               for _ in range(args.steps)]
+        p1.record(stream)
+        torch.cuda.synchronize()
+        pms = p0.elapsed_time(p1) / args.steps
+        plain = {"value": m / (pms / 1e3), "unit": UNIT, "ms_per_step": pms,
+                 "sweeps_per_run": [x.sweeps_executed for x in pst],
+                 "verified": engine.verify_staged(ctx) == 0,
+                 "what": "CC_OPT_CHECK_UNITE=0: the plain early check (a failing check costs "
+                         "another sweep and another check); sweep 1 split after a quarter of "
+                         "the windows, bitmap rebuilt every 3/16"}
+        ctx.set_option(_lib.CC_OPT_CHECK_UNITE, 1)
+        engine.run_staged(ctx, sched, sweep_times=False, **kw)
     dev_labels = None
     if not args.no_e2e:
         dev_labels = np.empty(n, dtype=np.int64)
@@ -502,9 +526,12 @@ def run_single(args, device):
     # host-driven runs without the check (the graph loop's per-sweep records
     # include control and check kernels); the check kernel separately
     rt1, rt2, rtc = [], [], []
+    # (layout 6: with the check on, as the timed runs -- sweep 1's split follows
+    # the check that ends the run)
     for _ in range(max(1, min(args.steps, 3))):
         _, st = engine.run_staged(ctx, sched, sweep_times=True, count_changes=False,
-                                  early_check=False, host_loop=True)
+                                  early_check=early and layout == "l2_tiled_check",
+                                  host_loop=True)
         if two_kernel:
             rt1.append(st.sweep_seconds[0])
             rt2.extend(st.sweep_seconds[1:])
@@ -522,11 +549,19 @@ def run_single(args, device):
     b_sweep = 8 * m + 4 * n  # edge stream + one label-array read
     peak, peak_src = peak_hbm()
     traffic = load_traffic().get(args.config) or {}
+    kernel_text = traffic.get("kernel", "cck::k_sweep<2, ...> (order-2 async sweep)")
+    if layout == "l2_tiled_check" and run_info["split_windows"]:
+        k, P, parts = run_info["split_windows"], run_info["windows"], run_info["split_parts"]
+        kernel_text = (f"sweep 1 = cck::k_sweep<2, 59, 1, 1> over L2 windows 0-{k - 1} of {P} "
+                       f"(tiles, 3 CTAs/SM, L2 cache hints) + {parts} x (k_pick_root, "
+                       f"k_bits_idem, k_sweep_bits_dp) over windows {k}-{P - 1} of the "
+                       + ("canonical copy (each undirected pair once)"
+                          if run_info["split_parts_canonical"] else "check copy")
+                       + ", bits published as vertices reach the root label")
     roofline = {"bound": "hbm", "achieved": b_sweep / t_sweep / 1e9, "peak": peak, "unit": "GB/s",
                 "frac": b_sweep / t_sweep / 1e9 / peak,
                 "traffic": traffic.get("dram_bytes_per_launch"),
-                "kernel": traffic.get("kernel", "cck::k_sweep<2, ...> (order-2 async sweep)")
-                + " + one shortcut pass",
+                "kernel": kernel_text + " + one shortcut pass",
                 "launch_ms": [round(t * 1e3, 4) for t in rt1],
                 "bytes_per_launch": b_sweep, "avg_launch_s": t_sweep,
                 "bytes_definition": "B_sweep = 8 m (src+dst uint32 stream) + 4 n (one label "
@@ -546,7 +581,11 @@ def run_single(args, device):
             bc = info["canon_bytes"] + 4 * n + n // 8
             roofline["check_kernel"].update({
                 "kernel": "k_pick_root + k_bits_idem + k_check_bits_dp over the canonical check "
-                          "copy (each undirected pair once, delta-packed)",
+                          "copy (each undirected pair once, delta-packed)"
+                          + ("; the timed runs end on its uniting form k_unite_bits_dp (same "
+                             "stream; rows whose labels differ are united, then pointer "
+                             "jumping) -- run minus sweep 1: "
+                             f"{ms - t_sweep * 1e3:.2f} ms" if run_info["uniting_check"] else ""),
                 "canonical_copy": {"rows": info["canon_rows"], "bytes": info["canon_bytes"],
                                    "side_groups": info["canon_side_groups"]},
                 "streamed_bytes_per_launch": bc, "frac_streamed": bc / t_chk / 1e9 / peak})
@@ -644,8 +683,15 @@ def run_single(args, device):
         "vs_baseline": None, "dtype": "u32", "data": "synthetic",
         "config": shared_config(args.config, n, m, atomic),
         "impl_detail": {"layout": layout, "store_mode": store_mode_name(atomic, args.store_mode),
-                        "early_check": early, "termination": "ballot/OR no-write flag or the "
-                        "early check (engine.py:318-320)",
+                        "early_check": early,
+                        "termination": ("a no-write sweep, or the early check after a changing "
+                                        "sweep (engine.py:318-320) in its uniting form: rows "
+                                        "whose labels differ are united (larger root lowered "
+                                        "to the smaller), pointer jumping finishes the labels "
+                                        "-- DESIGN 5.32; `plain_check` = the same runs with "
+                                        "the plain check") if run_info["uniting_check"] else
+                                       "ballot/OR no-write flag or the early check "
+                                       "(engine.py:318-320)",
                         "layout_build_s": round(layout_s, 3), "prep_s": round(prep_s, 2),
                         "value_excludes": "input generation and the staging-time layout "
                                           "(layout_build_s); e2e includes staging + layout",
@@ -653,6 +699,7 @@ def run_single(args, device):
         "sweeps_per_run": [s.sweeps_executed for s in stats],
         "sweep_ms": [round(t * 1e3, 4) for t in sweep_ms_graph],
         "verified": verify == 0,
+        "plain_check": plain,
         "reference_sweeps": ref_sweeps,
         "roofline": roofline,
         "cpu_baseline": cpu,

@@ -84,8 +84,12 @@ int cc_version(void);
  * out[3] work items, out[4] staged rows, out[5] / out[6] rows and bytes of the
  * canonical check copy (0 if none), out[7] its build status (0 built, 1 off or not
  * applicable, 2 a window beyond 2^31 rows, 3 no memory, 4 not under 55 % of the rows,
- * 5 side table full), out[8] its groups kept with raw sources (side table); the
- * first `count` entries are written. */
+ * 5 side table full), out[8] its groups kept with raw sources (side table);
+ * out[9] L2 windows of layout 4/6, out[10] windows sweep 1 runs on the tiles when it
+ * is split (0 = not split), out[11] the bitmap parts that follow them, out[12] 1 if the
+ * last cc_run ended on the uniting check (CC_OPT_CHECK_UNITE), out[13] 1 if the split
+ * parts walk the canonical copy -- out[10..13] describe the last run (or, before any
+ * run, a caller-driven cc_sweep); the first `count` entries are written. */
 int cc_layout_info(cc_ctx* ctx, int64_t* out, int count);
 
 /* ---- staging: the Graph input contract (graph.py:57-90, engine.py:268-270) ----
@@ -249,22 +253,27 @@ int cc_reorder_edges(cc_ctx* ctx, int mode);
 #define CC_OPT_RELABEL_BLOCK 31      /* layout 7: log2 rows per interleave block (default 24) */
 #define CC_OPT_SPLIT_SHORTCUT 32    /* split sweep 1: pointer-jumping passes before each bitmap
                                       part (more rows decided by the bitmap) */
-#define CC_OPT_CANON_SWEEP 33      /* layout 6, when the canonical copy was built: 1 (default) =
-                                      the whole-graph bitmap sweeps (sweep 2 on) walk it, each
+#define CC_OPT_CANON_SWEEP 33      /* layout 6, when the canonical copy was built: 1 = the
+                                      whole-graph bitmap sweeps (sweep 2 on) walk it, each
                                       undirected pair once; 2 = the split sweep 1's bitmap parts
                                       too; 0 = every bitmap sweep walks the dst-bucketed check
-                                      copy (every row) */
+                                      copy (every row); -1 (default) = 2 in runs that end on
+                                      the uniting check, else 1 */
 #define CC_OPT_CHECK_UNITE 35      /* layout 6 with a delta-packed copy, asynchronous C-2 runs
-                                      without exact counts: the early check after a changing
-                                      sweep unites the trees of every row whose labels differ
-                                      (root hooking) instead of failing, and pointer jumping
-                                      finishes the labels -- the check pass is the last pass
-                                      over the rows (DESIGN 5.32); 0 = the plain check */
+                                      (cc_run with CC_RUN_EARLY_CHECK, without exact counts):
+                                      1 (default) = the early check after a changing sweep
+                                      unites the trees of every row whose labels differ (the
+                                      larger root lowered to the smaller, a conditional min
+                                      assignment on the root cell) instead of failing, and
+                                      pointer jumping finishes the labels -- the check pass is
+                                      the last pass over the rows (DESIGN 5.32); sweep 1 then
+                                      splits after an eighth of the windows with one bitmap;
+                                      0 = the plain check (sweeps until it passes) */
 #define CC_OPT_BITS_PUBLISH 34     /* layout 6, delta-packed copies: the bitmap sweeps set a
                                       vertex's bit as soon as a row leaves it at the root label
                                       (later rows of that vertex are decided by the bitmap
-                                      again): 1 = in the split sweep 1's parts, 2 = in every
-                                      bitmap sweep, 0 = the bitmap stays as built */
+                                      again): 1 (default) = in the split sweep 1's parts, 2 = in
+                                      every bitmap sweep, 0 = the bitmap stays as built */
 #define CC_OPT_LINK_PACK 22        /* pageable host edges: 1 (default) = rows cross PCIe as
                                       ceil(2 log2(n) / 8) in {6, 7} bytes (u | v << log2 n)
                                       when that is under 8; 0 = uint32 pairs */

@@ -210,12 +210,14 @@ class Context:
     def layout_info(self) -> dict:
         """cc_layout_info: layout code, check-copy format and bytes per pass."""
         import numpy as np
-        out = np.zeros(9, dtype=np.int64)
-        check(self.lib.cc_layout_info(self.handle, out.ctypes.data_as(_I64P), 9), "cc_layout_info")
+        out = np.zeros(14, dtype=np.int64)
+        check(self.lib.cc_layout_info(self.handle, out.ctypes.data_as(_I64P), 14), "cc_layout_info")
         return {"layout": int(out[0]), "check_format": int(out[1]), "check_bytes": int(out[2]),
                 "items": int(out[3]), "m": int(out[4]), "canon_rows": int(out[5]),
                 "canon_bytes": int(out[6]), "canon_status": int(out[7]),
-                "canon_side_groups": int(out[8])}
+                "canon_side_groups": int(out[8]), "windows": int(out[9]),
+                "split_windows": int(out[10]), "split_parts": int(out[11]),
+                "uniting_check": bool(out[12]), "split_parts_canonical": bool(out[13])}
 
     def close(self):
         if getattr(self, "handle", None):

@@ -91,11 +91,25 @@ int cc_version(void) { return 1; }
 int cc_layout_info(cc_ctx* c, int64_t* out, int count) {
     if (!c || !out || count < 1) return fail(CC_EINVAL, "cc_layout_info: invalid argument");
     std::lock_guard<std::mutex> lk(c->mu);
-    const int64_t v[9] = {c->layout, c->layout == 6 ? (c->check_dp ? 2 : c->check_sbits ? 1 : 0) : -1,
-                          c->layout == 6 ? c->check_bytes : 0, c->n_items, c->m,
-                          c->citems ? c->canon_rows : 0, c->citems ? c->canon_bytes : 0,
-                          c->canon_status, c->citems ? c->canon_side_groups : 0};
-    for (int i = 0; i < count && i < 9; ++i) out[i] = v[i];
+    // sweep 1's split as the last run (or the next caller-driven sweep) takes it
+    const int P = std::max(0, (int)c->win_start.size() - 1);
+    int k = 0, parts = 0;
+    if (split_sweep1(c)) {
+        k = split_k(c);
+        if (c->split_mask) {
+            parts = __builtin_popcountll(c->split_mask >> k);
+        } else {
+            const int r = split_r(c) > 0 ? split_r(c) : P;
+            parts = (P - k + r - 1) / r;
+        }
+    }
+    const int64_t v[14] = {c->layout, c->layout == 6 ? (c->check_dp ? 2 : c->check_sbits ? 1 : 0) : -1,
+                           c->layout == 6 ? c->check_bytes : 0, c->n_items, c->m,
+                           c->citems ? c->canon_rows : 0, c->citems ? c->canon_bytes : 0,
+                           c->canon_status, c->citems ? c->canon_side_groups : 0,
+                           P, k, parts, c->unite_run ? 1 : 0,
+                           (k > 0 && canon_sweep(c, true)) ? 1 : 0};
+    for (int i = 0; i < count && i < 14; ++i) out[i] = v[i];
     return CC_OK;
 }
 
@@ -257,6 +271,7 @@ int cc_sweep(cc_ctx* c, int order, int sync, int atomic, int first, int* wrote_o
     if (!c) return fail(CC_EINVAL, "null context");
     std::lock_guard<std::mutex> lk(c->mu);
     DeviceGuard g(c->device);
+    c->unite_run = false;  // (caller-driven sweeps: the caller's check decides)
     if (sync) {
         CC_TRY(ensure_aux(c, true, false));
         CUDA_TRY(cudaMemcpyAsync(c->shadow, c->labels, sizeof(lab_t) * c->n,
@@ -280,6 +295,7 @@ int cc_sweep_numbered(cc_ctx* c, int order, int atomic, int64_t sweep_no, int* w
     if (sweep_no < 1) return fail(CC_EINVAL, "sweep number must be >= 1");
     std::lock_guard<std::mutex> lk(c->mu);
     DeviceGuard g(c->device);
+    c->unite_run = false;
     CC_TRY(enqueue_sweep(c, order, 0, atomic, false, false, sweep_no));
     if (wrote_out) {
         CC_TRY(read_flags(c));
@@ -589,6 +605,10 @@ int run_impl(cc_ctx* c, const cc_schedule* s, int flags, int64_t cap, void* labe
     const bool check = (flags & CC_RUN_EARLY_CHECK) != 0;
     const bool times = (flags & CC_RUN_SWEEP_TIMES) != 0;
     const bool first_scatter = (flags & CC_RUN_FIRST_SCATTER) != 0;
+    // asynchronous C-2 runs without exact counts end on the uniting check
+    // (sweep 1's split then follows it, launch.inc: split_k)
+    c->unite_run = check && !sync && !count && !first_scatter && c->peers.n == 0 &&
+                   unite_schedule(c, s);
     // layout 7: asynchronous runs without exact counts on the relabeled rows
     // (the dynamics differ from the original IDs', so parity modes use the
     // original rows in input order)
@@ -636,7 +656,7 @@ int run_impl(cc_ctx* c, const cc_schedule* s, int flags, int64_t cap, void* labe
             // (asynchronous runs without exact counts may unite disagreeing rows
             // instead of failing, as the graph loop does: the check then always
             // ends the loop and compress() below finishes the labels)
-            const bool unite = !sync && !count && unite_schedule(c, s);
+            const bool unite = c->unite_run;
             CUDA_TRY(cudaMemsetAsync(c->dflags + kFlagUnite, 0, sizeof(int), c->stream));
             CC_TRY(enqueue_loop_check(c, c->stream, unite));
             CC_TRY(read_flags(c));
@@ -1017,7 +1037,8 @@ int cc_set_option(cc_ctx* c, int option, int64_t value) {
             c->check_shift = (int)value;
             return CC_OK;
         case CC_OPT_CANON_SWEEP:
-            if (value < 0 || value > 2) return fail(CC_EINVAL, "canon sweep must be 0, 1 or 2");
+            if (value < -1 || value > 2)
+                return fail(CC_EINVAL, "canon sweep must be -1 (auto), 0, 1 or 2");
             c->canon_sweep = (int)value;
             return CC_OK;
         case CC_OPT_CHECK_UNITE:
