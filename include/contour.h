@@ -259,6 +259,12 @@ int cc_reorder_edges(cc_ctx* ctx, int mode);
                                       too; 0 = every bitmap sweep walks the dst-bucketed check
                                       copy (every row); -1 (default) = 2 in runs that end on
                                       the uniting check, else 1 */
+#define CC_OPT_BITS_DEFER 36       /* publishing bitmap sweeps: every lane parks up to this many
+                                      (0..4; 0 = off) undecided rows and the warp runs them as
+                                      one batch when a list would overflow or the item ends;
+                                      -1 (default) = 4 in runs that end on the uniting check,
+                                      else 0 (late rows cost the plain check its one-sweep
+                                      convergence) */
 #define CC_OPT_CHECK_UNITE 35      /* layout 6 with a delta-packed copy, asynchronous C-2 runs
                                       (cc_run with CC_RUN_EARLY_CHECK, without exact counts):
                                       1 (default) = the early check after a changing sweep
@@ -267,7 +273,7 @@ int cc_reorder_edges(cc_ctx* ctx, int mode);
                                       assignment on the root cell) instead of failing, and
                                       pointer jumping finishes the labels -- the check pass is
                                       the last pass over the rows (DESIGN 5.32); sweep 1 then
-                                      splits after an eighth of the windows with one bitmap;
+                                      splits after a sixteenth of the windows with one bitmap;
                                       0 = the plain check (sweeps until it passes) */
 #define CC_OPT_BITS_PUBLISH 34     /* layout 6, delta-packed copies: the bitmap sweeps set a
                                       vertex's bit as soon as a row leaves it at the root label

@@ -12,7 +12,8 @@ import os
 from .errors import IterationCapExceeded
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "lib", "libcontour.so")
+# CONTOUR_LIB: another build of the library (A/B runs of two builds on one box)
+LIB_PATH = os.environ.get("CONTOUR_LIB") or os.path.join(_PKG, "lib", "libcontour.so")
 
 CC_OK, CC_EINVAL, CC_ECAP, CC_ECUDA = 0, 1, 2, 3
 CC_RUN_EARLY_CHECK, CC_RUN_COUNT_CHANGES, CC_RUN_SWEEP_TIMES = 1, 2, 4
@@ -44,6 +45,7 @@ CC_OPT_SPLIT_SHORTCUT = 32
 CC_OPT_CANON_SWEEP = 33
 CC_OPT_BITS_PUBLISH = 34
 CC_OPT_CHECK_UNITE = 35
+CC_OPT_BITS_DEFER = 36
 STORE_PLAIN, STORE_RED, STORE_CHECK_PLAIN, STORE_CHECK_RED = 0, 1, 2, 3
 
 _I64P = ctypes.POINTER(ctypes.c_int64)

@@ -1041,6 +1041,10 @@ int cc_set_option(cc_ctx* c, int option, int64_t value) {
                 return fail(CC_EINVAL, "canon sweep must be -1 (auto), 0, 1 or 2");
             c->canon_sweep = (int)value;
             return CC_OK;
+        case CC_OPT_BITS_DEFER:
+            if (value < -1 || value > 4) return fail(CC_EINVAL, "bits defer must be in -1..4");
+            c->bits_defer = (int)value;
+            return CC_OK;
         case CC_OPT_CHECK_UNITE:
             c->check_unite = value != 0;
             return CC_OK;

@@ -848,9 +848,10 @@ def test_split_sweep1_exact(split, rebuild, canon, publish):
     ctx.close()
 
 
-@pytest.mark.parametrize("split,canon,publish", [(-1, 1, 1), (1, 2, 1), (0, 0, 0), (3, 1, 2),
-                                                 (1, 1, 0)])
-def test_uniting_check_exact(split, canon, publish):
+@pytest.mark.parametrize("split,canon,publish,defer", [(-1, -1, 1, 0), (1, 2, 1, 0), (0, 0, 0, 0),
+                                                       (3, 1, 2, 0), (1, 1, 0, 0), (-1, -1, 1, 1),
+                                                       (2, 0, 2, 1), (5, 2, 1, 1)])
+def test_uniting_check_exact(split, canon, publish, defer):
     """CC_OPT_CHECK_UNITE: the early check after sweep 1 unites the trees of
     every row whose labels differ (root hooking) and pointer jumping finishes
     the labels, so an asynchronous C-2 run without exact counts always ends
@@ -866,6 +867,7 @@ def test_uniting_check_exact(split, canon, publish):
     ctx.set_option(_lib.CC_OPT_CHECK_UNITE, 1)
     ctx.set_option(_lib.CC_OPT_CANON_SWEEP, canon)
     ctx.set_option(_lib.CC_OPT_BITS_PUBLISH, publish)
+    ctx.set_option(_lib.CC_OPT_BITS_DEFER, defer)  # undecided rows parked per lane, run in batches
     ctx.set_option(_lib.CC_OPT_TILE_SHIFT, 16)
     ctx.set_option(_lib.CC_OPT_CHECK_SHIFT, 16)
     ctx.set_option(_lib.CC_OPT_ITEM_ROWS, 20000)

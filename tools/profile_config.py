@@ -27,6 +27,8 @@ def main():
         lay = engine.resolve_layout(layout, e.shape[0], n)
         engine.stage_graph(ctx, n, e, lay)
         del e
+    for name, val in [kv.split("=") for kv in os.environ.get("CC_OPTS", "").split(",") if kv]:
+        ctx.set_option(getattr(_lib, "CC_OPT_" + name), int(val))  # e.g. CC_OPTS=BITS_DEFER=4
     check = os.environ.get("CC_CHECK", "0") == "1"
     _, st = engine.run_staged(ctx, make_schedule("c2"), count_changes=False, early_check=check,
                               host_loop=True)

@@ -32,6 +32,9 @@ def main():
     ap.add_argument("--canon", default="1")
     ap.add_argument("--shortcut", default="1", help="pointer-jumping passes after each sweep")
     ap.add_argument("--unite", default="0", help="CC_OPT_CHECK_UNITE values")
+    ap.add_argument("--defer", default="0", help="CC_OPT_BITS_DEFER values")
+    ap.add_argument("--split-shortcut", default="0",
+                    help="pointer-jumping passes before each bitmap part")
     args = ap.parse_args()
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
@@ -47,8 +50,13 @@ def main():
                 ctx.set_option(_lib.CC_OPT_SPLIT_SWEEP, split)
                 for rebuild in ints(args.rebuilds):
                     ctx.set_option(_lib.CC_OPT_SPLIT_REBUILD, rebuild)
-                    for pub, sc, un in [(p, k, q) for p in ints(args.publish)
-                                        for k in ints(args.shortcut) for q in ints(args.unite)]:
+                    for pub, sc, un, ss, df in [(p, k, q, z, d) for p in ints(args.publish)
+                                                for k in ints(args.shortcut)
+                                                for q in ints(args.unite)
+                                                for z in ints(args.split_shortcut)
+                                                for d in ints(args.defer)]:
+                        ctx.set_option(_lib.CC_OPT_BITS_DEFER, df)
+                        ctx.set_option(_lib.CC_OPT_SPLIT_SHORTCUT, ss)
                         ctx.set_option(_lib.CC_OPT_BITS_PUBLISH, pub)
                         ctx.set_option(_lib.CC_OPT_CHECK_UNITE, un)
                         ctx.set_option(_lib.CC_OPT_SHORTCUT, sc)
@@ -68,7 +76,7 @@ def main():
                             host.append([round(x * 1e3, 2) for x in st.sweep_seconds] +
                                         [round(st.device_seconds * 1e3, 2)])
                         print(json.dumps({"scale": args.scale, "seed": seed, "canon": canon,
-                                          "split": split, "rebuild": rebuild, "publish": pub, "shortcut": sc, "unite": un,
+                                          "split": split, "rebuild": rebuild, "publish": pub, "shortcut": sc, "unite": un, "split_shortcut": ss, "defer": df,
                                           "run_ms": dev, "sweeps": sweeps,
                                           "hostloop_sweep_ms": host,
                                           "verify": engine.verify_staged(ctx)}), flush=True)
