@@ -32,7 +32,8 @@ def main():
     ap.add_argument("--canon", default="1")
     ap.add_argument("--shortcut", default="1", help="pointer-jumping passes after each sweep")
     ap.add_argument("--unite", default="0", help="CC_OPT_CHECK_UNITE values")
-    ap.add_argument("--defer", default="0", help="CC_OPT_BITS_DEFER values")
+    ap.add_argument("--defer", default="-1", help="CC_OPT_BITS_DEFER values")
+    ap.add_argument("--item-rows", type=int, default=0, help="CC_OPT_ITEM_ROWS before the layout")
     ap.add_argument("--split-shortcut", default="0",
                     help="pointer-jumping passes before each bitmap part")
     args = ap.parse_args()
@@ -43,6 +44,8 @@ def main():
     ints = lambda s: [int(x) for x in s.split(",")]
     for seed in ints(args.seeds):
         graphgen.rmat_device(ctx, args.scale, 16, seed)
+        if args.item_rows:
+            ctx.set_option(_lib.CC_OPT_ITEM_ROWS, args.item_rows)
         engine.apply_layout(ctx, "l2_tiled_check")
         for canon in ints(args.canon):
             ctx.set_option(_lib.CC_OPT_CANON_SWEEP, canon)
