@@ -390,6 +390,13 @@ def run_contour(g, schedule: Schedule, threads: int = 1, seed: Optional[int] = N
     (every entry the minimum vertex ID of its component) and IterationStats.
     Raises IterationCapExceeded after n+2 sweeps, ValueError on bad input.
 
+    ``count_changes=False`` (no exact per-sweep counts; ``changed_per_sweep``
+    then holds -1 for a changing sweep) is the fast path: the whole loop is one
+    CUDA-graph launch, and on layout 6 an asynchronous C-2 run ends on the
+    uniting early check (CC_OPT_CHECK_UNITE, DESIGN 5.32): rows whose labels
+    still differ after a sweep are united and pointer jumping finishes the
+    labels -- same labels, ``converged_by == "early-check"``.
+
     ``devices`` (a list of CUDA device ordinals, more than one) shards the
     edge rows over those GPUs inside this process -- label replicas merged by
     an element-wise MIN every ``cadence`` local sweeps (distributed.py; one
