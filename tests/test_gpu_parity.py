@@ -5,6 +5,8 @@ runs must also reproduce the reference's per-sweep accounting exactly
 
 import hashlib
 
+import os
+
 import numpy as np
 import pytest
 
@@ -906,6 +908,51 @@ def test_uniting_check_exact(split, canon, publish, defer):
             _, st = engine.run_staged(ctx, sched, count_changes=count, labels_out=labels)
             assert np.array_equal(labels, exp), (n, sched, count)
             check_invariants(labels, st)
+    ctx.close()
+
+
+def test_uniting_check_fuzz():
+    """The bench's default path (layout 6, asynchronous C-2 without exact
+    counts, uniting early check, publishing bitmap parts with per-lane
+    batches) on 150 random multigraphs -- self loops, repeated rows, one
+    orientation or symmetrised, 0 to 8 rows per vertex: 120 small ones (1 to
+    40k vertices: one L2 window, sweep 1 on the tiles, then the uniting check)
+    and 30 of 2^18 to 600k vertices (4-10 windows of 2^16 vertices: split sweep
+    1, several items per bucket): labels equal rem_union_find's, cc_verify
+    certifies them, and a run that ended on the uniting check took one sweep."""
+    rng = np.random.default_rng(int(os.environ.get("CC_FUZZ_SEED", "77")))
+    ctx = _lib.Context(0)
+    ctx.set_option(_lib.CC_OPT_TILE_SHIFT, 16)
+    ctx.set_option(_lib.CC_OPT_CHECK_SHIFT, 16)
+    ctx.set_option(_lib.CC_OPT_ITEM_ROWS, 4096)
+    united = 0
+    for it in range(150):
+        if it < 120:
+            n = int(rng.choice([1, 2, 3, 31, 32, 33, 127, 128, 129, 1000, 4097, 40_000]))
+            if it % 3 == 0:
+                n = int(rng.integers(1, 40_000))
+        else:
+            n = int(rng.integers(1 << 18, 600_000))
+        m = int(rng.integers(0, 8 * n + 1)) if it % 7 else 0
+        if it >= 120:
+            m = int(rng.integers(n // 2, 4 * n))
+        e = rng.integers(0, n, size=(m, 2)).astype(np.int64)
+        if it % 2 and m:
+            e = np.concatenate([e, e[:, ::-1]])
+        if it % 5 == 0 and m:
+            e = np.concatenate([e, e[: m // 3]])  # repeated rows
+        exp = oracle.rem_union_find(n, e)
+        engine.stage_graph(ctx, n, e, "l2_tiled_check")
+        for host_loop in (False, True):
+            labels = np.empty(n, dtype=np.int64)
+            _, st = engine.run_staged(ctx, make_schedule("c2"), count_changes=False,
+                                      early_check=True, host_loop=host_loop, labels_out=labels)
+            assert np.array_equal(labels, exp), (it, n, m, host_loop)
+            assert engine.verify_staged(ctx) == 0, (it, n, m)
+            if ctx.layout_info()["uniting_check"]:
+                united += 1
+                assert st.sweeps_executed <= 1, (it, n, m, st)
+    assert united > 150  # (most graphs get the delta-packed copy the uniting check needs)
     ctx.close()
 
 
