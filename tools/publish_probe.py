@@ -33,6 +33,7 @@ def main():
     ap.add_argument("--shortcut", default="1", help="pointer-jumping passes after each sweep")
     ap.add_argument("--unite", default="0", help="CC_OPT_CHECK_UNITE values")
     ap.add_argument("--defer", default="-1", help="CC_OPT_BITS_DEFER values")
+    ap.add_argument("--opts", default="", help="extra options, NAME=V[,NAME=V...] (CC_OPT_ names)")
     ap.add_argument("--item-rows", type=int, default=0, help="CC_OPT_ITEM_ROWS before the layout")
     ap.add_argument("--split-shortcut", default="0",
                     help="pointer-jumping passes before each bitmap part")
@@ -44,6 +45,8 @@ def main():
     ints = lambda s: [int(x) for x in s.split(",")]
     for seed in ints(args.seeds):
         graphgen.rmat_device(ctx, args.scale, 16, seed)
+        for name, val in [kv.split("=") for kv in args.opts.split(",") if kv]:
+            ctx.set_option(getattr(_lib, "CC_OPT_" + name), int(val))
         if args.item_rows:
             ctx.set_option(_lib.CC_OPT_ITEM_ROWS, args.item_rows)
         engine.apply_layout(ctx, "l2_tiled_check")
