@@ -10,6 +10,11 @@ seeded synthetic.  One step = one whole run of the hot
 path: labels = arange(n) -> order-2 asynchronous sweeps (+ the reference's
 early convergence check) until converged -> pointer-jumping compress, with
 the edges resident in HBM (69 GB of edges >> the 126 MB L2, so no flush).
+On the layout "auto" picks for RMAT-28 (layout 6) the early check runs in its
+uniting form (DESIGN 5.32): rows whose labels still differ after sweep 1 are
+united on the spot and pointer jumping finishes the labels; `plain_check` in
+the line is the same K runs with the plain check (CC_OPT_CHECK_UNITE 0), and
+`verified` is cc_verify's certificate of the final labels.
 
 --gpus N without torchrun re-launches itself under torch.distributed.run with
 N local ranks (one per GPU).  N > 1: the edge rows are split into N
