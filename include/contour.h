@@ -184,7 +184,11 @@ int cc_reorder_edges(cc_ctx* ctx, int mode);
 #define CC_OPT_BUCKET_SHIFT 5      /* layout 3: 2^shift labels per dst bucket (8..15, default 15) */
 #define CC_OPT_ITEM_ROWS 6         /* layout 3: rows per work item (default 2^18) */
 #define CC_OPT_BUCKET_THREADS 7    /* layout 3: threads per CTA (256/512/1024, default 1024) */
-#define CC_OPT_TILE_SHIFT 8        /* layout 4: 2^shift labels per L2 window (default 24 = 64 MB) */
+#define CC_OPT_TILE_SHIFT 8        /* layouts 4/6: 2^shift labels per L2 window.  Unset: 24 (64 MB),
+                                      except layout 6 on a dense graph (m >= 4n) below 2^28
+                                      vertices: n/16-vertex windows (>= 2^16), so that sweep 1
+                                      splits there too; the buckets of CC_OPT_CHECK_SHIFT then
+                                      default to min(20, this) */
 #define CC_OPT_SHORTCUT 9          /* pointer-jumping passes L[v]=L[L[v]] after every async sweep
                                       without exact counting (0..8, default 1) */
 #define CC_OPT_TILE_SPLIT 10       /* layout 4: independently src-sorted runs per window (default 2) */

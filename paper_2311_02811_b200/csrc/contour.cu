@@ -971,6 +971,7 @@ int cc_set_option(cc_ctx* c, int option, int64_t value) {
         case CC_OPT_TILE_SHIFT:
             if (value < 10 || value > 30) return fail(CC_EINVAL, "tile shift must be in [10, 30]");
             c->tile_shift = (int)value;
+            c->tile_shift_auto = false;
             return CC_OK;
         case CC_OPT_SWEEP_CTAS:
             if (value < 0 || value > 32) return fail(CC_EINVAL, "sweep CTAs per SM must be 0..32");
@@ -1035,6 +1036,7 @@ int cc_set_option(cc_ctx* c, int option, int64_t value) {
             if (value < 7 || value > 20)
                 return fail(CC_EINVAL, "check shift must be in [7, 20] (<= 128 KB of bits)");
             c->check_shift = (int)value;
+            c->check_shift_auto = false;
             return CC_OK;
         case CC_OPT_CANON_SWEEP:
             if (value < -1 || value > 2)
@@ -1078,7 +1080,23 @@ int cc_reorder_edges(cc_ctx* c, int mode) {
     DeviceGuard g(c->device);
     if (c->m < 2) return CC_OK;
     if (mode == 3 || mode == 5) return reorder_bucketed(c, mode);
-    if (mode == 4 || mode == 6) return reorder_l2tiles(c, mode);
+    if (mode == 4 || mode == 6) {
+        // Window and bucket sizes left to the library: 2^24-vertex L2 windows
+        // (64 MB of labels) and 2^20-vertex buckets, except on a dense graph
+        // (m >= 4n, where sweep 1 is split) with fewer than 2^28 vertices --
+        // there n/16-vertex windows, so that mid-size graphs get RMAT-28's
+        // sweep-1 schedule too (one window on the tiles, the rest as a bitmap
+        // part: RMAT-24 2.87 -> 1.38 ms per run, RMAT-25 5.83 -> 2.72, RMAT-26
+        // 6.07 -> 4.70, RMAT-27 9.9 -> 9.3; DESIGN 5.35)
+        if (c->tile_shift_auto) {
+            int lg = 0;
+            while (((int64_t)1 << lg) < c->n) ++lg;
+            const bool dense = mode == 6 && c->m >= 4 * c->n;
+            c->tile_shift = dense ? std::min(24, std::max(16, lg - 4)) : 24;
+        }
+        if (c->check_shift_auto) c->check_shift = std::min(20, c->tile_shift);
+        return reorder_l2tiles(c, mode);
+    }
     if (mode == 7) return reorder_relabel(c);
     c->layout = mode;
     // mode 1: one global sort by src; mode 2: independent sorts of
