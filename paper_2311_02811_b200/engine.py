@@ -148,7 +148,7 @@ AUTO_HYBRID_MIN_DEGREE = 8  # rows per vertex from which the bucketed copy pays 
 
 
 def resolve_layout(layout: str, m: int, n: int = 0, resident: bool = True,
-                   copies: bool = True) -> str:
+                   copies: bool = True, counted: bool = True) -> str:
     """"auto": input order below 2^16 rows (ER n=65,536, 524,282 rows: 0.088 ms
     per run chunk-sorted vs 0.11 ms in input order); while the label array fits
     comfortably in L2, chunk-sorted staging (it hides under the host->device
@@ -162,7 +162,13 @@ def resolve_layout(layout: str, m: int, n: int = 0, resident: bool = True,
     (``resident=False``) of dense graphs stay chunk-sorted, so sweep 1
     streams behind the copy and the tiling (0.5 s at RMAT-28) is skipped
     (DESIGN 5.20).  ``copies=False``: no extra copy of the rows (the
-    multi-GPU shards: their fused exchange walks one row array)."""
+    multi-GPU shards: their fused exchange walks one row array).
+    ``counted=False`` (the graph will be run without exact change counts,
+    ``run_staged(count_changes=False)``): dense resident graphs of at least
+    2^20 vertices get layout 6 also while their labels fit in L2 -- with
+    n/16-vertex windows their sweep 1 is split and the run ends on the uniting
+    check (RMAT-22 0.51 vs 0.82 ms per run on the hybrid layout, DESIGN 5.35);
+    counted runs keep the hybrid layout (plain check: 0.82 vs 1.28 ms)."""
     if layout == "auto":
         if m < AUTO_SORT_MIN_ROWS:
             return "input"
@@ -175,7 +181,7 @@ def resolve_layout(layout: str, m: int, n: int = 0, resident: bool = True,
             # back to the tiles when the input order carries no locality
             return "relabel" if copies and m < (1 << 31) else "l2_tiled"
         if resident and copies and m < (1 << 31) and m >= AUTO_HYBRID_MIN_DEGREE * n:
-            return "hybrid"
+            return "l2_tiled_check" if (not counted and n >= (1 << 20)) else "hybrid"
         return "chunk_sorted"
     if layout not in LAYOUTS:
         raise ValueError(f"unknown edge layout '{layout}'")
